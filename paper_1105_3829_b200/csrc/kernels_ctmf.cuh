@@ -1,0 +1,290 @@
+// kernels_ctmf.cuh -- 8-bit rank filter with per-column histograms in shared
+// memory and horizontal window sliding: O(1) window-histogram work per
+// output pixel in the radius (the reference's per-column trees + window
+// sync, _kernels.py:115-194, re-planned for a warp).
+//
+// Decomposition.  Each WARP owns an independent tile: output columns
+// [X0, X0 + 32*S) and rows [Y0, Y1).  Lane t owns the S consecutive output
+// columns x_t = X0 + t*S ... x_t + S-1 of every row.  The tile keeps one
+// 16-bin histogram per column of the halo'd stripe [X0-r, X0+32S+r)
+// ("column histograms", u16 counts, 32 B per column) for the current row;
+// moving down one row removes the pixel leaving each column's vertical
+// span and adds the one entering it (2 counter updates per column).
+//
+// Per row, lane t first brings its window histogram at x_t from row y-1
+// to row y (one-hot updates of the entering/leaving row segments, 2n
+// counters), then slides right S-1 times with
+//     W += C[x + r + 1] - C[x - r]       (16 bins = 8 packed u16 words, IADD3)
+// and resolves the rank at every position by a 4-step binary descent over
+// the 16 bins (the reference's extract_u, _kernels.py:229-253, 16-ary).
+//
+// Two levels (16 coarse bins of width 16, then 16 fine bins):
+//   pass 1 (coarse): bins v>>4; writes the coarse bin of each output into
+//           dst (scratch) and collects the set of coarse bins the tile uses;
+//   pass 2 (fine), once per coarse bin B used by the tile: histograms count
+//           only pixels with v>>4 == B (bins v&15) plus, per column, the
+//           number of pixels below 16*B; outputs whose coarse bin is B
+//           resolve their low nibble with rank - below.
+// All arithmetic is exact integer counting; window counts fit u16 because
+// n^2 <= 65535 is required (r <= 127; larger windows use kernels_vert).
+#pragma once
+#include "common.cuh"
+
+namespace mtb {
+
+constexpr int CT_WARPS = 4;
+
+struct CtmfGeom {
+    int S, TW, NC, NCP;    // lane segment, tile width, halo'd columns, padded
+    int colh_bytes;        // per warp: 2 chunk arrays of NCP x 16 B
+    int below_bytes;       // per warp: NCP u16
+    int stage_bytes;       // per warp: 2 rows x NCP bytes
+    int scratch_bytes;     // per warp: 17 counters x 32 lanes x i32
+    int warp_bytes;
+};
+
+__host__ __device__ inline CtmfGeom ctmf_geom(int S, int r) {
+    CtmfGeom g;
+    g.S = S;
+    g.TW = 32 * S;
+    g.NC = g.TW + 2 * r;
+    g.NCP = (g.NC + 31) & ~31;
+    g.colh_bytes = 2 * g.NCP * 16;
+    g.below_bytes = g.NCP * 2;
+    g.stage_bytes = 2 * g.NCP;
+    g.scratch_bytes = 17 * 32 * 4;
+    g.warp_bytes = g.colh_bytes + ((g.below_bytes + 15) & ~15) + ((g.stage_bytes + 15) & ~15) +
+                   g.scratch_bytes;
+    return g;
+}
+
+// column slot swizzle: lanes read columns S apart; XOR the low 3 bits with
+// (c/S) so the 32 lanes' 16-B records spread over all 8 bank groups.
+template <int S>
+__device__ __forceinline__ int ct_slot(int c) {
+    return c ^ ((c / S) & 7);
+}
+
+__device__ __forceinline__ uint32_t hsum16(uint32_t w) {  // lo + hi (sum < 2^16)
+    return (w * 0x10001u) >> 16;
+}
+
+// Smallest bin b with cumsum(bins[0..b]) >= k; returns b and leaves in k the
+// rank within bin b.  bins are 16 u16 counters packed in w[0..7].
+__device__ __forceinline__ int ct_descend(const uint32_t (&w)[8], uint32_t &k) {
+    uint32_t t = w[0] + w[1] + w[2] + w[3];
+    uint32_t s = hsum16(t);
+    const bool r1 = s < k;
+    k -= r1 ? s : 0u;
+    uint32_t a0 = r1 ? w[4] : w[0], a1 = r1 ? w[5] : w[1];
+    uint32_t a2 = r1 ? w[6] : w[2], a3 = r1 ? w[7] : w[3];
+    s = hsum16(a0 + a1);
+    const bool r2 = s < k;
+    k -= r2 ? s : 0u;
+    uint32_t b0 = r2 ? a2 : a0, b1 = r2 ? a3 : a1;
+    s = hsum16(b0);
+    const bool r3 = s < k;
+    k -= r3 ? s : 0u;
+    const uint32_t c = r3 ? b1 : b0;
+    s = c & 0xffffu;
+    const bool r4 = s < k;
+    k -= r4 ? s : 0u;
+    return (r1 ? 8 : 0) | (r2 ? 4 : 0) | (r3 ? 2 : 0) | (r4 ? 1 : 0);
+}
+
+template <int S>
+__global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int tiles_x, int tiles_y) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int tile = blockIdx.x * CT_WARPS + warp;
+    if (tile >= tiles_x * tiles_y) return;  // warp-uniform; no block barriers below
+    const int r = p.radius;
+    const CtmfGeom g = ctmf_geom(S, r);
+    unsigned char *base = smem_raw + (size_t)warp * g.warp_bytes;
+    uint4 *colA = reinterpret_cast<uint4 *>(base);               // bins 0-7
+    uint4 *colB = colA + g.NCP;                                  // bins 8-15
+    uint16_t *below = reinterpret_cast<uint16_t *>(base + g.colh_bytes);
+    uint8_t *stin = base + g.colh_bytes + ((g.below_bytes + 15) & ~15);
+    uint8_t *stout = stin + g.NCP;
+    int32_t *scr = reinterpret_cast<int32_t *>(base + g.colh_bytes + ((g.below_bytes + 15) & ~15) +
+                                               ((g.stage_bytes + 15) & ~15));
+
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int W = p.W, H = p.H;
+    const int X0 = tx * g.TW;
+    const int Y0 = p.row_begin + ty * p.rows_per_cta;
+    const int Y1 = min(Y0 + p.rows_per_cta, p.row_end);
+    const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
+    uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
+    const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
+    const int xt = X0 + lane * S;        // first output column of this lane
+    const int ct = lane * S;             // its window's first column index (c = x - X0 + r - r)
+    const uint32_t rank = p.rank;
+
+    for (int i = lane; i < 17 * 32; i += 32) scr[i] = 0;
+    // pass 0 = coarse; pass 1 = fine for coarse bin `beta`
+    uint32_t tile_mask = 0;
+    int beta = -1;
+    for (int pass = 0;; ++pass) {
+        if (pass > 0) {
+            if (tile_mask == 0) break;
+            beta = __ffs(tile_mask) - 1;
+            tile_mask &= tile_mask - 1;
+        }
+        const bool fine = pass > 0;
+        // --- column histograms for row Y0: rows clamp(Y0-r .. Y0+r)
+        for (int c = lane; c < g.NCP; c += 32) {
+            colA[c] = make_uint4(0, 0, 0, 0);
+            colB[c] = make_uint4(0, 0, 0, 0);
+            below[c] = 0;
+        }
+        __syncwarp();
+        for (int j = -r; j <= r; ++j) {
+            const uint8_t *row = src_row(p, src, clampi(Y0 + j, 0, H - 1));
+            for (int c = lane; c < g.NC; c += 32) {
+                const unsigned v = __ldg(row + clampi(X0 - r + c, 0, W - 1));
+                const int sl = ct_slot<S>(c);
+                if (!fine) {
+                    uint16_t *h = reinterpret_cast<uint16_t *>((v >> 7) ? colB + sl : colA + sl);
+                    h[(v >> 4) & 7] += 1;
+                } else if ((int)(v >> 4) == beta) {
+                    uint16_t *h = reinterpret_cast<uint16_t *>((v & 8) ? colB + sl : colA + sl);
+                    h[v & 7] += 1;
+                } else if ((int)(v >> 4) < beta) {
+                    below[c] += 1;
+                }
+            }
+        }
+        __syncwarp();
+        // --- lane window at x_t, row Y0: sum of columns ct .. ct+2r
+        uint32_t ws[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint32_t wb = 0;
+        for (int c = ct; c <= ct + 2 * r; ++c) {
+            const int sl = ct_slot<S>(c);
+            const uint4 a = colA[sl], b = colB[sl];
+            ws[0] += a.x; ws[1] += a.y; ws[2] += a.z; ws[3] += a.w;
+            ws[4] += b.x; ws[5] += b.y; ws[6] += b.z; ws[7] += b.w;
+            if (fine) wb += below[c];
+        }
+        for (int y = Y0; y < Y1; ++y) {
+            if (y > Y0) {
+                // --- advance column histograms one row; stage the two rows
+                const int yo = clampi(y - r - 1, 0, H - 1);
+                const int yi = clampi(y + r, 0, H - 1);
+                const uint8_t *ro = src_row(p, src, yo);
+                const uint8_t *ri = src_row(p, src, yi);
+                for (int c = lane; c < g.NC; c += 32) {
+                    const int X = clampi(X0 - r + c, 0, W - 1);
+                    const unsigned vo = __ldg(ro + X), vi = __ldg(ri + X);
+                    stin[c] = (uint8_t)vi;
+                    stout[c] = (uint8_t)vo;
+                    if (vo == vi) continue;
+                    const int sl = ct_slot<S>(c);
+                    if (!fine) {
+                        reinterpret_cast<uint16_t *>((vo >> 7) ? colB + sl : colA + sl)[(vo >> 4) & 7] -= 1;
+                        reinterpret_cast<uint16_t *>((vi >> 7) ? colB + sl : colA + sl)[(vi >> 4) & 7] += 1;
+                    } else {
+                        if ((int)(vo >> 4) == beta)
+                            reinterpret_cast<uint16_t *>((vo & 8) ? colB + sl : colA + sl)[vo & 7] -= 1;
+                        else if ((int)(vo >> 4) < beta)
+                            below[c] -= 1;
+                        if ((int)(vi >> 4) == beta)
+                            reinterpret_cast<uint16_t *>((vi & 8) ? colB + sl : colA + sl)[vi & 7] += 1;
+                        else if ((int)(vi >> 4) < beta)
+                            below[c] += 1;
+                    }
+                }
+                __syncwarp();
+                // --- vertical step of the lane window at x_t (one-hot deltas)
+                if (yo != yi) {
+                    for (int c = ct; c <= ct + 2 * r; ++c) {
+                        const unsigned vi = stin[c], vo = stout[c];
+                        if (vi == vo) continue;
+                        if (!fine) {
+                            scr[(vi >> 4) * 32 + lane] += 1;
+                            scr[(vo >> 4) * 32 + lane] -= 1;
+                        } else {
+                            const int bi = ((int)(vi >> 4) == beta) ? (int)(vi & 15)
+                                                                   : ((int)(vi >> 4) < beta ? 16 : -1);
+                            const int bo = ((int)(vo >> 4) == beta) ? (int)(vo & 15)
+                                                                   : ((int)(vo >> 4) < beta ? 16 : -1);
+                            if (bi >= 0) scr[bi * 32 + lane] += 1;
+                            if (bo >= 0) scr[bo * 32 + lane] -= 1;
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int d0 = scr[(2 * i) * 32 + lane], d1 = scr[(2 * i + 1) * 32 + lane];
+                        scr[(2 * i) * 32 + lane] = 0;
+                        scr[(2 * i + 1) * 32 + lane] = 0;
+                        const uint32_t lo = (ws[i] & 0xffffu) + d0;
+                        const uint32_t hi = (ws[i] >> 16) + d1;
+                        ws[i] = (lo & 0xffffu) | (hi << 16);
+                    }
+                    if (fine) {
+                        wb += scr[16 * 32 + lane];
+                        scr[16 * 32 + lane] = 0;
+                    }
+                }
+            }
+            // --- slide right over the lane's S outputs
+            uint32_t w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = ws[i];
+            uint32_t wbl = wb;
+            uint8_t *drow = dst + (int64_t)(y - p.row_begin) * p.dst_pitch;
+            uint32_t outw[S / 4];
+            const bool full = (xt + S <= W) && ((reinterpret_cast<uintptr_t>(drow + xt) & 3) == 0);
+            if (fine) {
+                if (full) {
+#pragma unroll
+                    for (int q = 0; q < S / 4; ++q) outw[q] = *reinterpret_cast<const uint32_t *>(drow + xt + 4 * q);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < S / 4; ++q) outw[q] = 0;
+                    for (int s = 0; s < S; ++s)
+                        if (xt + s < W) outw[s >> 2] |= (uint32_t)drow[xt + s] << (8 * (s & 3));
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (s > 0) {
+                    const int cin = ct + s + 2 * r, cout = ct + s - 1;
+                    const int si = ct_slot<S>(cin), so = ct_slot<S>(cout);
+                    const uint4 ia = colA[si], ib = colB[si], oa = colA[so], ob = colB[so];
+                    w[0] = w[0] + ia.x - oa.x; w[1] = w[1] + ia.y - oa.y;
+                    w[2] = w[2] + ia.z - oa.z; w[3] = w[3] + ia.w - oa.w;
+                    w[4] = w[4] + ib.x - ob.x; w[5] = w[5] + ib.y - ob.y;
+                    w[6] = w[6] + ib.z - ob.z; w[7] = w[7] + ib.w - ob.w;
+                    if (fine) wbl = wbl + below[cin] - below[cout];
+                }
+                const uint32_t cur = (outw[s >> 2] >> (8 * (s & 3))) & 0xffu;
+                if (!fine) {
+                    uint32_t k = rank;
+                    const int b = ct_descend(w, k);
+                    tile_mask |= (xt + s < W) ? (1u << b) : 0u;
+                    outw[s >> 2] = (s & 3) ? (outw[s >> 2] | ((uint32_t)b << (8 * (s & 3)))) : (uint32_t)b;
+                } else if ((int)cur == beta) {
+                    uint32_t k = rank - wbl;
+                    const int b = ct_descend(w, k);
+                    uint32_t v = (uint32_t)(beta << 4) | (uint32_t)b;
+                    if (lut) v = __ldg(lut + v);
+                    outw[s >> 2] = (outw[s >> 2] & ~(0xffu << (8 * (s & 3)))) | (v << (8 * (s & 3)));
+                }
+            }
+            if (full) {
+#pragma unroll
+                for (int q = 0; q < S / 4; ++q) *reinterpret_cast<uint32_t *>(drow + xt + 4 * q) = outw[q];
+            } else {
+                for (int s = 0; s < S; ++s)
+                    if (xt + s < W) drow[xt + s] = (uint8_t)(outw[s >> 2] >> (8 * (s & 3)));
+            }
+            __syncwarp();
+        }
+        if (!fine) tile_mask = __reduce_or_sync(0xffffffffu, tile_mask);
+        __syncwarp();
+    }
+}
+
+}  // namespace mtb

@@ -11,6 +11,8 @@
 #include "../../include/medtree_b200.h"
 #include "common.cuh"
 #include "kernels_vert.cuh"
+#include "kernels_ctmf.cuh"
+#include <cstdlib>
 
 namespace mtb {
 
@@ -98,6 +100,49 @@ static int rows_per_cta(const SlabParams &p, int blocks_x, int B, int ctas_per_s
     return rpc < 1 ? 1 : rpc;
 }
 
+static int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+
+// kernel choice: MTB_KERNEL=vert|ctmf forces a family (testing/tuning)
+static const char *forced_kernel() {
+    const char *v = getenv("MTB_KERNEL");
+    return v ? v : "";
+}
+
+static int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
+    constexpr int S = 16;
+    const CtmfGeom g = ctmf_geom(S, p.radius);
+    const int rows = p.row_end - p.row_begin;
+    const int tiles_x = (p.W + g.TW - 1) / g.TW;
+    const int n = 2 * p.radius + 1;
+    const int want = sm_count() * 2 * CT_WARPS * 2;
+    int ty = (want + tiles_x * B - 1) / (tiles_x * B);
+    int th = (rows + ty - 1) / ty;
+    const int min_th = env_int("MTB_CT_MIN_TH", n / 2 > 16 ? n / 2 : 16);
+    if (th < min_th) th = min_th;
+    th = env_int("MTB_CT_TH", th);
+    if (th > rows) th = rows;
+    if (th < 1) th = 1;
+    p.rows_per_cta = th;
+    const int tiles_y = (rows + th - 1) / th;
+    const int tiles = tiles_x * tiles_y;
+    dim3 grid((tiles + CT_WARPS - 1) / CT_WARPS, 1, B);
+    const size_t smem = (size_t)g.warp_bytes * CT_WARPS;
+    auto kern = k_ctmf_u8<S>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    }
+    kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_ctmf_u8: ") + cudaGetErrorString(e));
+    g_kernel = "k_ctmf_u8<16>";
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return MTB_OK;
+}
+
 template <typename P>
 static int run(SlabParams p, int B, cudaStream_t s) {
     int rc = validate(p, B);
@@ -105,6 +150,10 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     if (p.row_begin == p.row_end) return MTB_OK;
     const int64_t n = 2 * (int64_t)p.radius + 1;
     const bool wide = n * n > 65535;
+    const std::string force = forced_kernel();
+    if (sizeof(P) == 1 && !wide && force != "vert" &&
+        (force == "ctmf" || p.radius >= env_int("MTB_CT_MIN_R", 2)))
+        return run_ctmf_u8(p, B, s);
     if (sizeof(P) == 1) {
         constexpr int T = 128;
         const int bx = (p.W + T - 1) / T;
