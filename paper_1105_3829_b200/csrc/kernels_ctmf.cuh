@@ -129,8 +129,10 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
     for (int pass = 0;; ++pass) {
         if (pass > 0) {
             if (tile_mask == 0) break;
-            beta = __ffs(tile_mask) - 1;
-            tile_mask &= tile_mask - 1;
+            // descending: a pixel finalised by pass beta holds a value >= 16*beta,
+            // which can never be mistaken for a lower coarse bin still pending
+            beta = 31 - __clz(tile_mask);
+            tile_mask &= ~(1u << beta);
         }
         const bool fine = pass > 0;
         // --- column histograms for row Y0: rows clamp(Y0-r .. Y0+r)
