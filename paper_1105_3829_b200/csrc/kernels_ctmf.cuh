@@ -11,9 +11,9 @@
 // moving down one row removes the pixel leaving each column's vertical
 // span and adds the one entering it (2 counter updates per column).
 //
-// Per row, lane t first brings its window histogram at x_t from row y-1
-// to row y (one-hot updates of the entering/leaving row segments, 2n
-// counters), then slides right S-1 times with
+// Per row, lane t first rebuilds its window histogram at x_t from the
+// column histograms (chunk sums + warp shuffles, ct_window), then slides
+// right S-1 times with
 //     W += C[x + r + 1] - C[x - r]       (16 bins = 8 packed u16 words, IADD3)
 // and resolves the rank at every position by a 4-step binary descent over
 // the 16 bins (the reference's extract_u, _kernels.py:229-253, 16-ary).
@@ -38,8 +38,6 @@ struct CtmfGeom {
     int S, TW, NC, NCP;    // lane segment, tile width, halo'd columns, padded
     int colh_bytes;        // per warp: 2 chunk arrays of NCP x 16 B
     int below_bytes;       // per warp: NCP u16
-    int stage_bytes;       // per warp: 2 rows x NCP bytes
-    int scratch_bytes;     // per warp: 17 counters x 32 lanes x i32
     int warp_bytes;
 };
 
@@ -51,10 +49,7 @@ __host__ __device__ inline CtmfGeom ctmf_geom(int S, int r) {
     g.NCP = (g.NC + 31) & ~31;
     g.colh_bytes = 2 * g.NCP * 16;
     g.below_bytes = g.NCP * 2;
-    g.stage_bytes = 2 * g.NCP;
-    g.scratch_bytes = 17 * 32 * 4;
-    g.warp_bytes = g.colh_bytes + ((g.below_bytes + 15) & ~15) + ((g.stage_bytes + 15) & ~15) +
-                   g.scratch_bytes;
+    g.warp_bytes = g.colh_bytes + ((g.below_bytes + 15) & ~15);
     return g;
 }
 
@@ -92,6 +87,82 @@ __device__ __forceinline__ int ct_descend(const uint32_t (&w)[8], uint32_t &k) {
     return (r1 ? 8 : 0) | (r2 ? 4 : 0) | (r3 ? 2 : 0) | (r4 ? 1 : 0);
 }
 
+
+// Window histograms of every lane at its segment start, straight from the
+// column histograms: lane t needs columns [tS, tS+2r].  Each lane sums its
+// own chunk of S columns (and a second chunk when the halo'd stripe has
+// more than 32 chunks), keeping the partial sum of the chunk's first m
+// columns; the window is then q whole chunks plus one partial chunk,
+// gathered with warp shuffles (n = qS + m).  O(S + n/S) per lane per row,
+// independent of the radius' one-hot cost.
+template <int S>
+__device__ __forceinline__ void ct_chunk(const uint4 *colA, const uint4 *colB, const uint16_t *below,
+                                         bool fine, int j, int m, int NC, uint32_t (&L)[9],
+                                         uint32_t (&P)[9]) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) L[i] = 0;
+    const int c0 = j * S;
+    int c = c0;
+    for (; c < c0 + m; ++c) {
+        const int sl = ct_slot<S>(c);
+        const uint4 a = colA[sl], b = colB[sl];
+        L[0] += a.x; L[1] += a.y; L[2] += a.z; L[3] += a.w;
+        L[4] += b.x; L[5] += b.y; L[6] += b.z; L[7] += b.w;
+        if (fine && c < NC) L[8] += below[c];
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i) P[i] = L[i];
+    for (; c < c0 + S; ++c) {
+        const int sl = ct_slot<S>(c);
+        const uint4 a = colA[sl], b = colB[sl];
+        L[0] += a.x; L[1] += a.y; L[2] += a.z; L[3] += a.w;
+        L[4] += b.x; L[5] += b.y; L[6] += b.z; L[7] += b.w;
+        if (fine && c < NC) L[8] += below[c];
+    }
+}
+
+template <int S>
+__device__ __forceinline__ void ct_window(const uint4 *colA, const uint4 *colB, const uint16_t *below,
+                                          bool fine, int lane, int r, int NC, uint32_t (&ws)[8],
+                                          uint32_t &wb) {
+    const int n = 2 * r + 1, q = n / S, m = n - q * S;
+    const int J = (NC + S - 1) / S;
+    uint32_t LA[9], PA[9], LB[9], PB[9];
+    ct_chunk<S>(colA, colB, below, fine, lane, m, NC, LA, PA);
+    if (lane + 32 < J) {
+        ct_chunk<S>(colA, colB, below, fine, lane + 32, m, NC, LB, PB);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 9; ++i) LB[i] = PB[i] = 0;
+    }
+    uint32_t acc[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) acc[i] = 0;
+    for (int k = 0; k <= q; ++k) {
+        const int idx = lane + k;
+        const bool hiB = idx >= 32;
+        const int sl = idx & 31;
+        if (k < q) {
+#pragma unroll
+            for (int i = 0; i < 9; ++i) {
+                const uint32_t a = __shfl_sync(0xffffffffu, LA[i], sl);
+                const uint32_t b = __shfl_sync(0xffffffffu, LB[i], sl);
+                acc[i] += hiB ? b : a;
+            }
+        } else if (m > 0) {
+#pragma unroll
+            for (int i = 0; i < 9; ++i) {
+                const uint32_t a = __shfl_sync(0xffffffffu, PA[i], sl);
+                const uint32_t b = __shfl_sync(0xffffffffu, PB[i], sl);
+                acc[i] += hiB ? b : a;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ws[i] = acc[i];
+    wb = acc[8];
+}
+
 template <int S>
 __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int tiles_x, int tiles_y) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -105,10 +176,6 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
     uint4 *colA = reinterpret_cast<uint4 *>(base);               // bins 0-7
     uint4 *colB = colA + g.NCP;                                  // bins 8-15
     uint16_t *below = reinterpret_cast<uint16_t *>(base + g.colh_bytes);
-    uint8_t *stin = base + g.colh_bytes + ((g.below_bytes + 15) & ~15);
-    uint8_t *stout = stin + g.NCP;
-    int32_t *scr = reinterpret_cast<int32_t *>(base + g.colh_bytes + ((g.below_bytes + 15) & ~15) +
-                                               ((g.stage_bytes + 15) & ~15));
 
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int W = p.W, H = p.H;
@@ -122,7 +189,6 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
     const int ct = lane * S;             // its window's first column index (c = x - X0 + r - r)
     const uint32_t rank = p.rank;
 
-    for (int i = lane; i < 17 * 32; i += 32) scr[i] = 0;
     // pass 0 = coarse; pass 1 = fine for coarse bin `beta`
     uint32_t tile_mask = 0;
     int beta = -1;
@@ -159,19 +225,12 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
             }
         }
         __syncwarp();
-        // --- lane window at x_t, row Y0: sum of columns ct .. ct+2r
-        uint32_t ws[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        uint32_t wb = 0;
-        for (int c = ct; c <= ct + 2 * r; ++c) {
-            const int sl = ct_slot<S>(c);
-            const uint4 a = colA[sl], b = colB[sl];
-            ws[0] += a.x; ws[1] += a.y; ws[2] += a.z; ws[3] += a.w;
-            ws[4] += b.x; ws[5] += b.y; ws[6] += b.z; ws[7] += b.w;
-            if (fine) wb += below[c];
-        }
+        // --- lane window at x_t, row Y0
+        uint32_t ws[8], wb;
+        ct_window<S>(colA, colB, below, fine, lane, r, g.NC, ws, wb);
         for (int y = Y0; y < Y1; ++y) {
             if (y > Y0) {
-                // --- advance column histograms one row; stage the two rows
+                // --- advance column histograms one row
                 const int yo = clampi(y - r - 1, 0, H - 1);
                 const int yi = clampi(y + r, 0, H - 1);
                 const uint8_t *ro = src_row(p, src, yo);
@@ -179,8 +238,6 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
                 for (int c = lane; c < g.NC; c += 32) {
                     const int X = clampi(X0 - r + c, 0, W - 1);
                     const unsigned vo = __ldg(ro + X), vi = __ldg(ri + X);
-                    stin[c] = (uint8_t)vi;
-                    stout[c] = (uint8_t)vo;
                     if (vo == vi) continue;
                     const int sl = ct_slot<S>(c);
                     if (!fine) {
@@ -198,37 +255,8 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
                     }
                 }
                 __syncwarp();
-                // --- vertical step of the lane window at x_t (one-hot deltas)
-                if (yo != yi) {
-                    for (int c = ct; c <= ct + 2 * r; ++c) {
-                        const unsigned vi = stin[c], vo = stout[c];
-                        if (vi == vo) continue;
-                        if (!fine) {
-                            scr[(vi >> 4) * 32 + lane] += 1;
-                            scr[(vo >> 4) * 32 + lane] -= 1;
-                        } else {
-                            const int bi = ((int)(vi >> 4) == beta) ? (int)(vi & 15)
-                                                                   : ((int)(vi >> 4) < beta ? 16 : -1);
-                            const int bo = ((int)(vo >> 4) == beta) ? (int)(vo & 15)
-                                                                   : ((int)(vo >> 4) < beta ? 16 : -1);
-                            if (bi >= 0) scr[bi * 32 + lane] += 1;
-                            if (bo >= 0) scr[bo * 32 + lane] -= 1;
-                        }
-                    }
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int d0 = scr[(2 * i) * 32 + lane], d1 = scr[(2 * i + 1) * 32 + lane];
-                        scr[(2 * i) * 32 + lane] = 0;
-                        scr[(2 * i + 1) * 32 + lane] = 0;
-                        const uint32_t lo = (ws[i] & 0xffffu) + d0;
-                        const uint32_t hi = (ws[i] >> 16) + d1;
-                        ws[i] = (lo & 0xffffu) | (hi << 16);
-                    }
-                    if (fine) {
-                        wb += scr[16 * 32 + lane];
-                        scr[16 * 32 + lane] = 0;
-                    }
-                }
+                // --- lane window at x_t for the new row, from the column histograms
+                ct_window<S>(colA, colB, below, fine, lane, r, g.NC, ws, wb);
             }
             // --- slide right over the lane's S outputs
             uint32_t w[8];

@@ -120,7 +120,7 @@ static int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
     const int want = sm_count() * 2 * CT_WARPS * 2;
     int ty = (want + tiles_x * B - 1) / (tiles_x * B);
     int th = (rows + ty - 1) / ty;
-    const int min_th = env_int("MTB_CT_MIN_TH", n / 2 > 16 ? n / 2 : 16);
+    const int min_th = env_int("MTB_CT_MIN_TH", 16);
     if (th < min_th) th = min_th;
     th = env_int("MTB_CT_TH", th);
     if (th > rows) th = rows;
