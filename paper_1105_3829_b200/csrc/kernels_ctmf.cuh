@@ -33,11 +33,13 @@
 namespace mtb {
 
 constexpr int CT_WARPS = 4;
+constexpr int CT_STAGE_ROWS = 4;  // image rows staged per batch (init)
 
 struct CtmfGeom {
     int S, TW, NC, NCP;    // lane segment, tile width, halo'd columns, padded
     int colh_bytes;        // per warp: 2 chunk arrays of NCP x 16 B
     int below_bytes;       // per warp: NCP u16
+    int SPB;               // staged row pitch (bytes)
     int warp_bytes;
 };
 
@@ -49,7 +51,8 @@ __host__ __device__ inline CtmfGeom ctmf_geom(int S, int r) {
     g.NCP = (g.NC + 31) & ~31;
     g.colh_bytes = 2 * g.NCP * 16;
     g.below_bytes = g.NCP * 2;
-    g.warp_bytes = g.colh_bytes + ((g.below_bytes + 15) & ~15);
+    g.SPB = (g.NC + 8 + 15) & ~15;
+    g.warp_bytes = g.colh_bytes + ((g.below_bytes + 15) & ~15) + CT_STAGE_ROWS * g.SPB;
     return g;
 }
 
@@ -163,6 +166,33 @@ __device__ __forceinline__ void ct_window(const uint4 *colA, const uint4 *colB, 
     wb = acc[8];
 }
 
+// Stage `nrows` image rows (global rows g[k]) of the tile's halo'd column
+// span into shared memory: aligned 4-byte loads (all independent, so the
+// warp keeps many requests in flight), byte loads for the unaligned tail.
+// Column X of row k lands at stage + k*SPB + (X - A), A = span start & ~3.
+__device__ __forceinline__ void ct_stage(const SlabParams &p, const uint8_t *src, uint8_t *stage,
+                                         int SPB, const int *g, int nrows, int A, int sx1,
+                                         bool aligned, int lane) {
+    const int nbytes = sx1 - A;
+    if (aligned) {
+        const int nw = nbytes >> 2;
+        for (int k = 0; k < nrows; ++k) {
+            const uint32_t *rw = reinterpret_cast<const uint32_t *>(src_row(p, src, g[k]) + A);
+            uint32_t *sw = reinterpret_cast<uint32_t *>(stage + k * SPB);
+            for (int w = lane; w < nw; w += 32) sw[w] = __ldg(rw + w);
+        }
+        for (int k = 0; k < nrows; ++k) {
+            const uint8_t *rb = src_row(p, src, g[k]) + A;
+            for (int b = (nw << 2) + lane; b < nbytes; b += 32) stage[k * SPB + b] = __ldg(rb + b);
+        }
+    } else {
+        for (int k = 0; k < nrows; ++k) {
+            const uint8_t *rb = src_row(p, src, g[k]) + A;
+            for (int b = lane; b < nbytes; b += 32) stage[k * SPB + b] = __ldg(rb + b);
+        }
+    }
+}
+
 template <int S>
 __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int tiles_x, int tiles_y) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -176,6 +206,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
     uint4 *colA = reinterpret_cast<uint4 *>(base);               // bins 0-7
     uint4 *colB = colA + g.NCP;                                  // bins 8-15
     uint16_t *below = reinterpret_cast<uint16_t *>(base + g.colh_bytes);
+    uint8_t *stage = base + g.colh_bytes + ((g.below_bytes + 15) & ~15);
 
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int W = p.W, H = p.H;
@@ -186,8 +217,14 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
     uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
     const int xt = X0 + lane * S;        // first output column of this lane
-    const int ct = lane * S;             // its window's first column index (c = x - X0 + r - r)
+    const int ct = lane * S;             // column index of its window's left edge
     const uint32_t rank = p.rank;
+    // staged column span [A, sx1): covers clamp(X0-r .. X0+TW+r-1)
+    const int sx0 = max(0, X0 - r);
+    const int sx1 = min(W, X0 + g.TW + r);
+    const int A = sx0 & ~3;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)(p.src_pitch)) & 3) == 0;
+    const int SPB = g.SPB;
 
     // pass 0 = coarse; pass 1 = fine for coarse bin `beta`
     uint32_t tile_mask = 0;
@@ -201,27 +238,38 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
             tile_mask &= ~(1u << beta);
         }
         const bool fine = pass > 0;
+        // bin of value v in this pass: 0..15, 16 = "below" (fine only), -1 = ignored
+        auto bin_of = [&](unsigned v) -> int {
+            if (!fine) return (int)(v >> 4);
+            const int hb = (int)(v >> 4);
+            return hb == beta ? (int)(v & 15) : (hb < beta ? 16 : -1);
+        };
+        auto bump = [&](int c, int b, int d) {
+            if (b < 0) return;
+            if (b == 16) {
+                below[c] += d;
+            } else {
+                const int sl = ct_slot<S>(c);
+                reinterpret_cast<uint16_t *>((b & 8) ? colB + sl : colA + sl)[b & 7] += d;
+            }
+        };
         // --- column histograms for row Y0: rows clamp(Y0-r .. Y0+r)
         for (int c = lane; c < g.NCP; c += 32) {
             colA[c] = make_uint4(0, 0, 0, 0);
             colB[c] = make_uint4(0, 0, 0, 0);
             below[c] = 0;
         }
-        __syncwarp();
-        for (int j = -r; j <= r; ++j) {
-            const uint8_t *row = src_row(p, src, clampi(Y0 + j, 0, H - 1));
+        for (int j0 = -r; j0 <= r; j0 += CT_STAGE_ROWS) {
+            const int nr = min(CT_STAGE_ROWS, r - j0 + 1);
+            int gr[CT_STAGE_ROWS];
+#pragma unroll
+            for (int k = 0; k < CT_STAGE_ROWS; ++k) gr[k] = clampi(Y0 + j0 + k, 0, H - 1);
+            __syncwarp();
+            ct_stage(p, src, stage, SPB, gr, nr, A, sx1, aligned, lane);
+            __syncwarp();
             for (int c = lane; c < g.NC; c += 32) {
-                const unsigned v = __ldg(row + clampi(X0 - r + c, 0, W - 1));
-                const int sl = ct_slot<S>(c);
-                if (!fine) {
-                    uint16_t *h = reinterpret_cast<uint16_t *>((v >> 7) ? colB + sl : colA + sl);
-                    h[(v >> 4) & 7] += 1;
-                } else if ((int)(v >> 4) == beta) {
-                    uint16_t *h = reinterpret_cast<uint16_t *>((v & 8) ? colB + sl : colA + sl);
-                    h[v & 7] += 1;
-                } else if ((int)(v >> 4) < beta) {
-                    below[c] += 1;
-                }
+                const int si = clampi(X0 - r + c, 0, W - 1) - A;
+                for (int k = 0; k < nr; ++k) bump(c, bin_of(stage[k * SPB + si]), 1);
             }
         }
         __syncwarp();
@@ -231,27 +279,19 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
         for (int y = Y0; y < Y1; ++y) {
             if (y > Y0) {
                 // --- advance column histograms one row
-                const int yo = clampi(y - r - 1, 0, H - 1);
-                const int yi = clampi(y + r, 0, H - 1);
-                const uint8_t *ro = src_row(p, src, yo);
-                const uint8_t *ri = src_row(p, src, yi);
-                for (int c = lane; c < g.NC; c += 32) {
-                    const int X = clampi(X0 - r + c, 0, W - 1);
-                    const unsigned vo = __ldg(ro + X), vi = __ldg(ri + X);
-                    if (vo == vi) continue;
-                    const int sl = ct_slot<S>(c);
-                    if (!fine) {
-                        reinterpret_cast<uint16_t *>((vo >> 7) ? colB + sl : colA + sl)[(vo >> 4) & 7] -= 1;
-                        reinterpret_cast<uint16_t *>((vi >> 7) ? colB + sl : colA + sl)[(vi >> 4) & 7] += 1;
-                    } else {
-                        if ((int)(vo >> 4) == beta)
-                            reinterpret_cast<uint16_t *>((vo & 8) ? colB + sl : colA + sl)[vo & 7] -= 1;
-                        else if ((int)(vo >> 4) < beta)
-                            below[c] -= 1;
-                        if ((int)(vi >> 4) == beta)
-                            reinterpret_cast<uint16_t *>((vi & 8) ? colB + sl : colA + sl)[vi & 7] += 1;
-                        else if ((int)(vi >> 4) < beta)
-                            below[c] += 1;
+                int gr[CT_STAGE_ROWS];
+                gr[0] = clampi(y - r - 1, 0, H - 1);
+                gr[1] = clampi(y + r, 0, H - 1);
+                if (gr[0] != gr[1]) {
+                    __syncwarp();
+                    ct_stage(p, src, stage, SPB, gr, 2, A, sx1, aligned, lane);
+                    __syncwarp();
+                    for (int c = lane; c < g.NC; c += 32) {
+                        const int si = clampi(X0 - r + c, 0, W - 1) - A;
+                        const int bo = bin_of(stage[si]), bi = bin_of(stage[SPB + si]);
+                        if (bo == bi) continue;
+                        bump(c, bo, -1);
+                        bump(c, bi, 1);
                     }
                 }
                 __syncwarp();
