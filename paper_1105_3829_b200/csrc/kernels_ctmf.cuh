@@ -33,7 +33,7 @@
 namespace mtb {
 
 constexpr int CT_WARPS = 4;
-constexpr int CT_STAGE_ROWS = 4;  // image rows staged per batch (init)
+constexpr int CT_STAGE_ROWS = 8;  // image rows staged per batch (init); nibble counts stay < 16
 
 struct CtmfGeom {
     int S, TW, NC, NCP;    // lane segment, tile width, halo'd columns, padded
@@ -267,9 +267,38 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
             __syncwarp();
             ct_stage(p, src, stage, SPB, gr, nr, A, sx1, aligned, lane);
             __syncwarp();
+            // per column: count the batch's bins in 4-bit lanes of two words
+            // (no shared-memory read-modify-write chain), then add the
+            // expanded counts to the column record with two 16-B RMWs.
             for (int c = lane; c < g.NC; c += 32) {
                 const int si = clampi(X0 - r + c, 0, W - 1) - A;
-                for (int k = 0; k < nr; ++k) bump(c, bin_of(stage[k * SPB + si]), 1);
+                uint32_t n0 = 0, n1 = 0, nb = 0;  // nibble counts bins 0-7 / 8-15, below
+                for (int k = 0; k < nr; ++k) {
+                    const int b = bin_of(stage[k * SPB + si]);
+                    if (b >= 0 && b < 8) n0 += 1u << (4 * b);
+                    else if (b >= 8 && b < 16) n1 += 1u << (4 * (b - 8));
+                    else if (b == 16) nb += 1;
+                }
+                const int sl = ct_slot<S>(c);
+                if (n0) {
+                    const uint32_t t = n0 >> 4;
+                    uint4 h = colA[sl];
+                    h.x += __byte_perm(n0, t, 0x7470) & 0x000f000fu;
+                    h.y += __byte_perm(n0, t, 0x7571) & 0x000f000fu;
+                    h.z += __byte_perm(n0, t, 0x7672) & 0x000f000fu;
+                    h.w += __byte_perm(n0, t, 0x7773) & 0x000f000fu;
+                    colA[sl] = h;
+                }
+                if (n1) {
+                    const uint32_t t = n1 >> 4;
+                    uint4 h = colB[sl];
+                    h.x += __byte_perm(n1, t, 0x7470) & 0x000f000fu;
+                    h.y += __byte_perm(n1, t, 0x7571) & 0x000f000fu;
+                    h.z += __byte_perm(n1, t, 0x7672) & 0x000f000fu;
+                    h.w += __byte_perm(n1, t, 0x7773) & 0x000f000fu;
+                    colB[sl] = h;
+                }
+                if (nb) below[c] += nb;
             }
         }
         __syncwarp();
@@ -286,12 +315,41 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
                     __syncwarp();
                     ct_stage(p, src, stage, SPB, gr, 2, A, sx1, aligned, lane);
                     __syncwarp();
-                    for (int c = lane; c < g.NC; c += 32) {
-                        const int si = clampi(X0 - r + c, 0, W - 1) - A;
-                        const int bo = bin_of(stage[si]), bi = bin_of(stage[SPB + si]);
-                        if (bo == bi) continue;
-                        bump(c, bo, -1);
-                        bump(c, bi, 1);
+                    // two counter updates per column; U columns per batch with all
+                    // loads issued before any store (addresses are distinct)
+                    constexpr int U = 4;
+                    for (int c0 = lane; c0 < g.NC; c0 += 32 * U) {
+                        uint16_t *po[U], *pi[U];
+                        uint16_t vo[U], vi[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int c = c0 + 32 * u;
+                            po[u] = pi[u] = nullptr;
+                            if (c < g.NC) {
+                                const int si = clampi(X0 - r + c, 0, W - 1) - A;
+                                const int bo = bin_of(stage[si]), bi = bin_of(stage[SPB + si]);
+                                if (bo != bi) {
+                                    const int sl = ct_slot<S>(c);
+                                    auto ptr = [&](int b) -> uint16_t * {
+                                        if (b < 0) return nullptr;
+                                        if (b == 16) return below + c;
+                                        return reinterpret_cast<uint16_t *>((b & 8) ? colB + sl : colA + sl) + (b & 7);
+                                    };
+                                    po[u] = ptr(bo);
+                                    pi[u] = ptr(bi);
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            vo[u] = po[u] ? *po[u] : 0;
+                            vi[u] = pi[u] ? *pi[u] : 0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (po[u]) *po[u] = vo[u] - 1;
+                            if (pi[u]) *pi[u] = vi[u] + 1;
+                        }
                     }
                 }
                 __syncwarp();
