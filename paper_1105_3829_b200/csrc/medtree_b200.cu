@@ -111,12 +111,11 @@ static const char *forced_kernel() {
     return v ? v : "";
 }
 
-static int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
-    constexpr int S = 16;
+template <int S>
+static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     const CtmfGeom g = ctmf_geom(S, p.radius);
     const int rows = p.row_end - p.row_begin;
     const int tiles_x = (p.W + g.TW - 1) / g.TW;
-    const int n = 2 * p.radius + 1;
     const int want = sm_count() * 2 * CT_WARPS * 2;
     int ty = (want + tiles_x * B - 1) / (tiles_x * B);
     int th = (rows + ty - 1) / ty;
@@ -138,9 +137,13 @@ static int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
     kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_ctmf_u8: ") + cudaGetErrorString(e));
-    g_kernel = "k_ctmf_u8<16>";
+    g_kernel = S == 8 ? "k_ctmf_u8<8>" : "k_ctmf_u8<16>";
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return MTB_OK;
+}
+
+static int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
+    return env_int("MTB_CT_S", 16) == 8 ? run_ctmf_u8_s<8>(p, B, s) : run_ctmf_u8_s<16>(p, B, s);
 }
 
 template <typename P>
