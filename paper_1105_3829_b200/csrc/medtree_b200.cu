@@ -12,6 +12,7 @@
 #include "common.cuh"
 #include "kernels_vert.cuh"
 #include "kernels_ctmf.cuh"
+#include "kernels_lob.cuh"
 #include <cstdlib>
 
 namespace mtb {
@@ -146,6 +147,37 @@ static int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
     return env_int("MTB_CT_S", 16) == 8 ? run_ctmf_u8_s<8>(p, B, s) : run_ctmf_u8_s<16>(p, B, s);
 }
 
+template <int L>
+static int run_lob_u8_l(SlabParams p, int B, cudaStream_t s) {
+    const LobGeom g = lob_geom(L, p.radius);
+    const int rows = p.row_end - p.row_begin;
+    const int tiles_x = (p.W + g.TW - 1) / g.TW;
+    const int per_sm = (220 * 1024) / g.warp_bytes;
+    const int want = sm_count() * (per_sm < 1 ? 1 : per_sm) * 3;
+    int ty = (want + tiles_x * B - 1) / (tiles_x * B);
+    int th = (rows + ty - 1) / ty;
+    const int min_th = env_int("MTB_LOB_MIN_TH", 32);
+    if (th < min_th) th = min_th;
+    th = env_int("MTB_LOB_TH", th);
+    if (th > rows) th = rows;
+    if (th < 1) th = 1;
+    p.rows_per_cta = th;
+    const int tiles_y = (rows + th - 1) / th;
+    dim3 grid(tiles_x * tiles_y, 1, B);
+    const size_t smem = (size_t)g.warp_bytes;
+    auto kern = k_lob_u8<L>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    }
+    kern<<<grid, 32, smem, s>>>(p, tiles_x, tiles_y);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_lob_u8: ") + cudaGetErrorString(e));
+    g_kernel = L == 32 ? "k_lob_u8<32>" : "k_lob_u8<64>";
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return MTB_OK;
+}
+
 template <typename P>
 static int run(SlabParams p, int B, cudaStream_t s) {
     int rc = validate(p, B);
@@ -154,7 +186,10 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     const int64_t n = 2 * (int64_t)p.radius + 1;
     const bool wide = n * n > 65535;
     const std::string force = forced_kernel();
-    if (sizeof(P) == 1 && !wide && force != "vert" &&
+    if (sizeof(P) == 1 && p.radius <= 63 && (force == "lob" || force.empty()) &&
+        p.radius >= env_int("MTB_LOB_MIN_R", 1))
+        return env_int("MTB_LOB_L", 32) == 64 ? run_lob_u8_l<64>(p, B, s) : run_lob_u8_l<32>(p, B, s);
+    if (sizeof(P) == 1 && !wide && force == "ctmf" &&
         (force == "ctmf" || p.radius >= env_int("MTB_CT_MIN_R", 2)))
         return run_ctmf_u8(p, B, s);
     if (sizeof(P) == 1) {
