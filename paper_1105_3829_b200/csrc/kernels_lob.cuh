@@ -32,6 +32,7 @@ namespace mtb {
 struct LobGeom {
     int L, TW, NC, NCP;  // outputs per stream, tile width, halo'd columns, padded
     int col_bytes;       // NCP x 256
+    int cum_bytes;       // NCP x 16
     int stage_bytes;     // staged rows
     int out_bytes;       // one output row of the tile
     int warp_bytes;
@@ -46,9 +47,10 @@ __host__ __device__ inline LobGeom lob_geom(int L, int r) {
     g.NC = g.TW + 2 * r;
     g.NCP = (g.NC + 31) & ~31;
     g.col_bytes = g.NCP * 256;
+    g.cum_bytes = g.NCP * 16;
     g.stage_bytes = LOB_STAGE_ROWS * ((g.NC + 8 + 15) & ~15);
     g.out_bytes = (g.TW + 15) & ~15;
-    g.warp_bytes = g.col_bytes + g.stage_bytes + g.out_bytes;
+    g.warp_bytes = g.col_bytes + g.cum_bytes + g.stage_bytes + g.out_bytes;
     return g;
 }
 
@@ -83,6 +85,27 @@ __device__ __forceinline__ void lob_add(uint32_t (&w)[8], const uint4 in) {
     }
 }
 
+// cum[c][g] = number of pixels of column c below 16*g (g = 0..15), u8.
+// A one-hot at value v changes cum[c][g] for every g > v>>4: a 16-byte add
+// of 0x01 bytes above byte v>>4.
+__device__ __forceinline__ void lob_cum_bump(uint8_t *cum, int c, unsigned v, bool add) {
+    uint4 *p = reinterpret_cast<uint4 *>(cum + c * 16);
+    uint4 t = *p;
+    const int b = (int)(v >> 4) + 1;  // first g that counts v
+    uint32_t m[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int sh = 8 * (b - 4 * j);  // bytes >= b within word j
+        m[j] = sh <= 0 ? 0x01010101u : (sh >= 32 ? 0u : (0x01010101u << sh));
+    }
+    if (add) {
+        t.x += m[0]; t.y += m[1]; t.z += m[2]; t.w += m[3];
+    } else {
+        t.x -= m[0]; t.y -= m[1]; t.z -= m[2]; t.w -= m[3];
+    }
+    *p = t;
+}
+
 template <int L>
 __global__ void __launch_bounds__(32) k_lob_u8(SlabParams p, int tiles_x, int tiles_y) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -92,7 +115,8 @@ __global__ void __launch_bounds__(32) k_lob_u8(SlabParams p, int tiles_x, int ti
     const int r = p.radius;
     const LobGeom g = lob_geom(L, r);
     uint8_t *colh = smem_raw;                       // [NCP][256]
-    uint8_t *stage = smem_raw + g.col_bytes;        // [LOB_STAGE_ROWS][SPB]
+    uint8_t *cum = smem_raw + g.col_bytes;          // [NCP][16]
+    uint8_t *stage = cum + g.cum_bytes;             // [LOB_STAGE_ROWS][SPB]
     uint8_t *orow = stage + g.stage_bytes;          // [TW]
     const int SPB = (g.NC + 8 + 15) & ~15;
 
@@ -112,7 +136,7 @@ __global__ void __launch_bounds__(32) k_lob_u8(SlabParams p, int tiles_x, int ti
 
     const int q = lane & 15;        // bin slice [16q, 16q+16)
     const int sid = lane >> 4;      // stream
-    const int cs = sid * L;         // stream's first window column (column index = x - X0 + r - r)
+    const int cs = sid * L;         // stream's first window column index
 
     // --- column histograms at row Y0
     for (int i = lane; i < g.NCP * 16; i += 32) reinterpret_cast<uint4 *>(colh)[i] = make_uint4(0, 0, 0, 0);
@@ -130,6 +154,23 @@ __global__ void __launch_bounds__(32) k_lob_u8(SlabParams p, int tiles_x, int ti
         }
     }
     __syncwarp();
+    // cumulative chunk counts per column
+    for (int c = lane; c < g.NCP; c += 32) {
+        uint32_t acc = 0;
+        uint32_t out[4] = {0, 0, 0, 0};
+        for (int k = 0; k < 16; ++k) {
+            out[k >> 2] |= acc << (8 * (k & 3));
+            const uint4 v = *reinterpret_cast<const uint4 *>(colh + c * 256 + (((k + c) & 15) << 4));
+            // byte sum of 16 bytes (each <= 127, sum <= 127 per column)
+            uint32_t t = __vsadu4(v.x, 0) + __vsadu4(v.y, 0) + __vsadu4(v.z, 0) + __vsadu4(v.w, 0);
+            acc += t;
+        }
+        *reinterpret_cast<uint4 *>(cum + c * 16) = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+    __syncwarp();
+
+    // column c's slice for lane q: byte offset c*256 + ((q + c) & 15)*16
+    auto slice_off = [&](int c) -> uint32_t { return (uint32_t)(c * 256 + (((q + c) & 15) << 4)); };
 
     for (int y = Y0; y < Y1; ++y) {
         if (y > Y0) {
@@ -145,6 +186,10 @@ __global__ void __launch_bounds__(32) k_lob_u8(SlabParams p, int tiles_x, int ti
                     if (vo != vi) {
                         colh[lob_byte(c, vo)] -= 1;
                         colh[lob_byte(c, vi)] += 1;
+                        if ((vo >> 4) != (vi >> 4)) {
+                            lob_cum_bump(cum, c, vo, false);
+                            lob_cum_bump(cum, c, vi, true);
+                        }
                     }
                 }
                 __syncwarp();
@@ -154,36 +199,41 @@ __global__ void __launch_bounds__(32) k_lob_u8(SlabParams p, int tiles_x, int ti
         uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         {
             int c = cs;
-            // add in pairs in the u8 domain (two columns <= 254), then widen
             for (; c + 1 <= cs + 2 * r; c += 2) {
-                const uint4 a = *lob_slice(colh, c, q);
-                const uint4 b = *lob_slice(colh, c + 1, q);
+                const uint4 a = *reinterpret_cast<const uint4 *>(colh + slice_off(c));
+                const uint4 b = *reinterpret_cast<const uint4 *>(colh + slice_off(c + 1));
                 lob_add(w, make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w));
             }
-            if (c <= cs + 2 * r) lob_add(w, *lob_slice(colh, c, q));
+            if (c <= cs + 2 * r) lob_add(w, *reinterpret_cast<const uint4 *>(colh + slice_off(c)));
         }
-        // --- slide over the stream's L outputs
-#pragma unroll 2
+        int gq = 0;          // lane (bin slice) holding this stream's rank value
+        uint32_t E = 0;      // number of window pixels below 16*gq
+        bool known = false;  // gq/E valid for the current window
         for (int s = 0; s < L; ++s) {
             if (s > 0) {
                 const int cin = cs + s + 2 * r, cout = cs + s - 1;
-                const uint4 iv = *lob_slice(colh, cin, q);
-                const uint4 ov = *lob_slice(colh, cout, q);
+                const uint4 iv = *reinterpret_cast<const uint4 *>(colh + slice_off(cin));
+                const uint4 ov = *reinterpret_cast<const uint4 *>(colh + slice_off(cout));
                 lob_step(w, iv, ov);
+                E = E + cum[cin * 16 + gq] - cum[cout * 16 + gq];
             }
-            // lane sum, segmented inclusive scan over the 16 lanes
             const uint32_t tsum = hsum16(((w[0] + w[1]) + (w[2] + w[3])) + ((w[4] + w[5]) + (w[6] + w[7])));
-            uint32_t incl = tsum;
+            // fast path: the rank value stayed in slice gq
+            const bool ok_here = known && (q != gq || (E < rank && rank <= E + tsum));
+            if (!__all_sync(0xffffffffu, ok_here)) {
+                uint32_t incl = tsum;
 #pragma unroll
-            for (int d = 1; d < 16; d <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d, 16);
-                if (q >= d) incl += t;
+                for (int d = 1; d < 16; d <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d, 16);
+                    incl += (q >= d) ? t : 0u;
+                }
+                const uint32_t ball = __ballot_sync(0xffffffffu, incl >= rank);
+                gq = __ffs((ball >> (16 * sid)) & 0xffffu) - 1;
+                E = __shfl_sync(0xffffffffu, incl - tsum, (sid << 4) | gq);
+                known = true;
             }
-            const uint32_t ball = __ballot_sync(0xffffffffu, incl >= rank);
-            const uint32_t mine = (ball >> (16 * sid)) & 0xffffu;
-            const int qs = __ffs(mine) - 1;
-            if (q == qs) {
-                uint32_t k = rank - (incl - tsum);
+            if (q == gq) {
+                uint32_t k = rank - E;
                 const int b = ct_descend(w, k);
                 orow[cs + s] = (uint8_t)(16 * q + b);
             }
