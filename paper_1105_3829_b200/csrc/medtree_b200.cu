@@ -13,6 +13,7 @@
 #include "kernels_vert.cuh"
 #include "kernels_ctmf.cuh"
 #include "kernels_lob.cuh"
+#include "kernels_sortnet.cuh"
 #include <cstdlib>
 
 namespace mtb {
@@ -178,6 +179,35 @@ static int run_lob_u8_l(SlabParams p, int B, cudaStream_t s) {
     return MTB_OK;
 }
 
+template <int N, int K, int RT, typename P>
+static int run_sortnet_n(SlabParams p, int B, cudaStream_t s, const char *name) {
+    constexpr int TX = 32 * 2 * K, TY = 4 * RT;
+    const int rows = p.row_end - p.row_begin;
+    dim3 grid((p.W + TX - 1) / TX, (rows + TY - 1) / TY, B);
+    k_sortnet<N, K, RT, P><<<grid, dim3(32, 4), 0, s>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
+    g_kernel = name;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return MTB_OK;
+}
+
+// selection networks: median rank only, n = 3, 5, 7
+template <typename P>
+static bool sortnet_applies(const SlabParams &p) {
+    const int n = 2 * p.radius + 1;
+    return n <= 7 && (uint32_t)((n * n + 1) / 2) == p.rank;
+}
+
+template <typename P>
+static int run_sortnet(SlabParams p, int B, cudaStream_t s) {
+    switch (p.radius) {
+        case 1: return run_sortnet_n<3, 4, 8, P>(p, B, s, "k_sortnet<3>");
+        case 2: return run_sortnet_n<5, 2, 8, P>(p, B, s, "k_sortnet<5>");
+        default: return run_sortnet_n<7, 1, 8, P>(p, B, s, "k_sortnet<7>");
+    }
+}
+
 template <typename P>
 static int run(SlabParams p, int B, cudaStream_t s) {
     int rc = validate(p, B);
@@ -186,6 +216,7 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     const int64_t n = 2 * (int64_t)p.radius + 1;
     const bool wide = n * n > 65535;
     const std::string force = forced_kernel();
+    if ((force.empty() || force == "sortnet") && sortnet_applies<P>(p)) return run_sortnet<P>(p, B, s);
     if (sizeof(P) == 1 && p.radius <= 63 && (force == "lob" || force.empty()) &&
         p.radius >= env_int("MTB_LOB_MIN_R", 1))
         return env_int("MTB_LOB_L", 32) == 64 ? run_lob_u8_l<64>(p, B, s) : run_lob_u8_l<32>(p, B, s);
