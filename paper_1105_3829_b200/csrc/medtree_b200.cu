@@ -121,7 +121,7 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     const int want = sm_count() * 2 * CT_WARPS * 2;
     int ty = (want + tiles_x * B - 1) / (tiles_x * B);
     int th = (rows + ty - 1) / ty;
-    const int min_th = env_int("MTB_CT_MIN_TH", 16);
+    const int min_th = env_int("MTB_CT_MIN_TH", S == 8 ? 48 : 16);
     if (th < min_th) th = min_th;
     th = env_int("MTB_CT_TH", th);
     if (th > rows) th = rows;
@@ -145,7 +145,7 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
 }
 
 static int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
-    return env_int("MTB_CT_S", 16) == 8 ? run_ctmf_u8_s<8>(p, B, s) : run_ctmf_u8_s<16>(p, B, s);
+    return env_int("MTB_CT_S", 8) == 8 ? run_ctmf_u8_s<8>(p, B, s) : run_ctmf_u8_s<16>(p, B, s);
 }
 
 template <int L>
@@ -216,12 +216,14 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     const int64_t n = 2 * (int64_t)p.radius + 1;
     const bool wide = n * n > 65535;
     const std::string force = forced_kernel();
+    // Kernel choice (measured on B200, tools/probe.py):
+    //   median, n <= 7          -> selection networks (any bit depth)
+    //   8-bit, 24 <= r <= 127   -> column-histogram CTMF (O(1) in r)
+    //   otherwise               -> per-column vertical histograms (any r/rank)
     if ((force.empty() || force == "sortnet") && sortnet_applies<P>(p)) return run_sortnet<P>(p, B, s);
-    if (sizeof(P) == 1 && p.radius <= 63 && (force == "lob" || force.empty()) &&
-        p.radius >= env_int("MTB_LOB_MIN_R", 1))
-        return env_int("MTB_LOB_L", 32) == 64 ? run_lob_u8_l<64>(p, B, s) : run_lob_u8_l<32>(p, B, s);
-    if (sizeof(P) == 1 && !wide && force == "ctmf" &&
-        (force == "ctmf" || p.radius >= env_int("MTB_CT_MIN_R", 2)))
+    if (sizeof(P) == 1 && p.radius <= 63 && force == "lob") return run_lob_u8_l<32>(p, B, s);
+    if (sizeof(P) == 1 && !wide &&
+        (force == "ctmf" || (force.empty() && p.radius >= env_int("MTB_CT_MIN_R", 24))))
         return run_ctmf_u8(p, B, s);
     if (sizeof(P) == 1) {
         constexpr int T = 128;
