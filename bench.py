@@ -74,7 +74,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
@@ -239,6 +239,11 @@ def run_ours(args):
     torch.cuda.synchronize()
     if pg:
         pg.barrier()
+    kernels = {}
+    for r in RADII:
+        launch(r)
+        kernels[r] = _lib.last_kernel()
+    torch.cuda.synchronize()
     evs = {r: [] for r in RADII}
     launches0 = _lib.launch_count()
     with ClockSampler(local) as clk:
@@ -310,13 +315,13 @@ def run_ours(args):
         "config": {"workload": "config2_4096x4096_u8_radius_sweep", "radii": list(RADII),
                    "frame": [H, W], "l2": "flushed (256 MiB write) before every launch",
                    "parallelism": f"row slabs x{ws}, no collective"},
-        "per_radius": {str(r): {"ms": round(ms_r[r], 4),
+        "per_radius": {str(r): {"ms": round(ms_r[r], 4), "kernel": kernels[r],
                                 "mpix_s": round(H * W / (ms_r[r] * 1e-3) / 1e6, 1),
                                 "hbm_frac": round(alg_bytes / (ms_r[r] * 1e-3) / 1e9 / peak, 5)}
                        for r in RADII},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
-                     "kernel": f"{_lib.last_kernel()} r={dom}",
+                     "kernel": f"{kernels[dom]} r={dom}",
                      "algorithmic_bytes_per_launch": alg_bytes, "peak_kind": peak_kind},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -334,7 +339,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
