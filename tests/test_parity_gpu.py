@@ -268,3 +268,35 @@ def _cfg4():
     if "4" not in _cache:
         _cache["4"] = workloads.cfg4_three_gauss_u16()
     return _cache["4"]
+
+
+# ------------------------------------------ every kernel family vs the oracle
+
+_FAMILY_CASES = [c for c in G.small_cases() if c[0]["rank"] is None and c[0]["percentile"] is None]
+
+
+@pytest.mark.parametrize("family", ["vert", "ctmf", "lob", "sortnet"])
+def test_each_kernel_family_is_exact(family, monkeypatch):
+    """MTB_KERNEL forces one family; families that do not apply to a case
+    (ctmf/lob: 8-bit only; sortnet: median of n <= 7) fall through to the
+    general kernel, so every case must still be exact."""
+    from paper_1105_3829_b200 import _lib
+
+    monkeypatch.setenv("MTB_KERNEL", family)
+    seen = set()
+    for meta, px, ref in _FAMILY_CASES:
+        out, _ = mtb.filter_image(mtb.GrayImage(px, meta["bit_depth"]), meta["n"],
+                                  **_ref_args(meta))
+        assert np.array_equal(out.pixels, ref), (family, meta["idx"])
+        seen.add(_lib.last_kernel().split("<")[0])
+    rng = np.random.default_rng(7)
+    for r in (1, 2, 3, 5, 24, 40):
+        px = workloads.cfg2_blur_sp_u8(150, 700 + r)
+        out = mtb.rank_filter(torch.from_numpy(px).cuda(), r).cpu().numpy()
+        assert np.array_equal(out, O.iot_filter(px, 2 * r + 1)), (family, r)
+        seen.add(_lib.last_kernel().split("<")[0])
+        px16 = rng.integers(0, 65536, (70, 90)).astype(np.uint16)
+        out16 = mtb.rank_filter(torch.from_numpy(px16).cuda(), min(r, 34)).cpu().numpy()
+        assert np.array_equal(out16, O.iot_filter(px16, 2 * min(r, 34) + 1)), (family, r)
+    expect = {"vert": "k_vert_u8", "ctmf": "k_ctmf_u8", "lob": "k_lob_u8", "sortnet": "k_sortnet"}[family]
+    assert expect in seen, seen
