@@ -16,6 +16,7 @@
 // kernels_colhist.cuh take over where they apply.
 #pragma once
 #include "common.cuh"
+#include "kernels_ctmf.cuh"  // ct_stage
 
 namespace mtb {
 
@@ -80,6 +81,88 @@ __global__ void __launch_bounds__(T) k_vert_u8(SlabParams p) {
             acc += c;
         }
         dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
+    }
+}
+
+// 8-bit general path, v2: each warp stages the rows it needs (its 32
+// columns + 2r halo, clamped) in shared memory with coalesced loads, so the
+// 2n per-row counter updates read pixels from shared memory instead of 2n
+// dependent global loads; fine counters are u8 when the window holds at
+// most 255 pixels (r <= 7), halving the footprint and doubling occupancy.
+template <typename FC, int T>
+__global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint16_t *hc = reinterpret_cast<uint16_t *>(smem_raw);      // [16][T]
+    FC *hf = reinterpret_cast<FC *>(hc + 16 * T);               // [256][T]
+    const int r = p.radius, H = p.H, W = p.W;
+    const int SPW = (32 + 2 * r + 8 + 15) & ~15;                // staged row pitch
+    uint8_t *stg = reinterpret_cast<uint8_t *>(hf + 256 * T) + (threadIdx.x >> 5) * 2 * SPW;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int x = blockIdx.x * T + tid;
+    const int xw = blockIdx.x * T + (tid & ~31);                  // warp's first column
+    const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
+    if (y0 >= p.row_end || xw >= W) return;                       // warp-uniform
+    const int y1 = min(y0 + p.rows_per_cta, p.row_end);
+    const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
+    uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
+    const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
+    const int sx0 = max(0, xw - r), sx1 = min(W, xw + 32 + r);
+    const int A = sx0 & ~3;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)(p.src_pitch)) & 3) == 0;
+    // staged index of window column i (0..2r) of this thread
+    auto sidx = [&](int i) { return clampi(x - r + i, 0, W - 1) - A; };
+    // u8 counters: lane l of warp w at byte 4l+w, so a warp's 32 lanes hit
+    // 32 different banks whatever their values
+    const int fo = sizeof(FC) == 1 ? (((tid & 31) << 2) | (tid >> 5)) : tid;
+
+    for (int b = 0; b < 16; ++b) hc[b * T + tid] = 0;
+    for (int b = 0; b < 256; ++b) hf[b * T + fo] = 0;
+    for (int j = -r; j <= r; ++j) {
+        int g = clampi(y0 + j, 0, H - 1);
+        __syncwarp();
+        ct_stage(p, src, stg, SPW, &g, 1, A, sx1, aligned, lane);
+        __syncwarp();
+        for (int i = 0; i <= 2 * r; ++i) {
+            const unsigned v = stg[sidx(i)];
+            hc[(v >> 4) * T + tid] += 1;
+            hf[v * T + fo] += 1;
+        }
+    }
+    const uint32_t rank = p.rank;
+    for (int y = y0; y < y1; ++y) {
+        if (y > y0) {
+            int g[2] = {clampi(y - r - 1, 0, H - 1), clampi(y + r, 0, H - 1)};
+            if (g[0] != g[1]) {
+                __syncwarp();
+                ct_stage(p, src, stg, SPW, g, 2, A, sx1, aligned, lane);
+                __syncwarp();
+                for (int i = 0; i <= 2 * r; ++i) {
+                    const int si = sidx(i);
+                    const unsigned vo = stg[si], vi = stg[SPW + si];
+                    if (vo == vi) continue;
+                    if ((vo >> 4) != (vi >> 4)) {
+                        hc[(vo >> 4) * T + tid] -= 1;
+                        hc[(vi >> 4) * T + tid] += 1;
+                    }
+                    hf[vo * T + fo] -= 1;
+                    hf[vi * T + fo] += 1;
+                }
+            }
+        }
+        uint32_t acc = 0;
+        int b = 0;
+        for (; b < 15; ++b) {
+            const uint32_t c = hc[b * T + tid];
+            if (acc + c >= rank) break;
+            acc += c;
+        }
+        int v = b * 16;
+        for (const int e = v + 15; v < e; ++v) {
+            const uint32_t c = hf[v * T + fo];
+            if (acc + c >= rank) break;
+            acc += c;
+        }
+        if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
     }
 }
 
