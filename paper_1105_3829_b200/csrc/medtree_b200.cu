@@ -225,10 +225,10 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     if (sizeof(P) == 1 && !wide &&
         (force == "ctmf" || (force.empty() && p.radius >= env_int("MTB_CT_MIN_R", 24))))
         return run_ctmf_u8(p, B, s);
-    if (sizeof(P) == 1 && !wide && force != "vert") {
+    if (sizeof(P) == 1 && n * n <= 255 && force != "vert") {
         constexpr int T = 128;
         const int bx = (p.W + T - 1) / T;
-        const bool small = n * n <= 255;
+        const bool small = true;
         const int spw = (32 + 2 * p.radius + 8 + 15) & ~15;
         const size_t smem = (size_t)16 * T * 2 + (size_t)256 * T * (small ? 1 : 2) + (size_t)(T / 32) * 2 * spw;
         p.rows_per_cta = rows_per_cta(p, bx, B, small ? 6 : 3);
