@@ -51,7 +51,7 @@ __host__ __device__ inline CtmfGeom ctmf_geom(int S, int r) {
     g.NCP = (g.NC + 31) & ~31;
     g.colh_bytes = 2 * g.NCP * 16;
     g.below_bytes = g.NCP * 2;
-    g.SPB = (g.NC + 8 + 15) & ~15;
+    g.SPB = (g.NC + 16 + 15) & ~15;
     g.warp_bytes = g.colh_bytes + ((g.below_bytes + 15) & ~15) + CT_STAGE_ROWS * g.SPB;
     return g;
 }
@@ -166,14 +166,74 @@ __device__ __forceinline__ void ct_window(const uint4 *colA, const uint4 *colB, 
     wb = acc[8];
 }
 
-// Stage `nrows` image rows (global rows g[k]) of the tile's halo'd column
-// span into shared memory: aligned 4-byte loads (all independent, so the
-// warp keeps many requests in flight), byte loads for the unaligned tail.
-// Column X of row k lands at stage + k*SPB + (X - A), A = span start & ~3.
+// ---- row staging ---------------------------------------------------------
+// Stage `nrows` image rows (global rows g[k]) of a tile's halo'd column span
+// into shared memory: column X of staged row k lands at stage + k*SPB +
+// (X - A), with A = span start rounded down to 16 bytes.
+//
+// TMA path (rows 16-byte aligned): lane 0 of the warp arms the warp's
+// mbarrier with the byte count and issues one cp.async.bulk (global ->
+// shared, completion on the mbarrier) per row for the 16-byte-aligned body;
+// the other lanes load the <16-byte tail; everyone waits on the mbarrier.
+// Fallback path: independent 4-byte / 1-byte loads by all lanes.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+struct StageBar {
+    uint64_t *bar;   // this warp's mbarrier
+    uint32_t phase;  // parity of the next completion
+};
+
+// one mbarrier per warp; call once per warp before the first ct_stage
+__device__ __forceinline__ StageBar ct_stage_init(int lane) {
+    __shared__ __align__(8) uint64_t s_bar[32];
+    uint64_t *bar = &s_bar[threadIdx.x >> 5];
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    return StageBar{bar, 0u};
+}
+
 __device__ __forceinline__ void ct_stage(const SlabParams &p, const uint8_t *src, uint8_t *stage,
                                          int SPB, const int *g, int nrows, int A, int sx1,
-                                         bool aligned, int lane) {
+                                         bool aligned, int lane, StageBar *sb = nullptr) {
     const int nbytes = sx1 - A;
+    if (sb && aligned) {
+        const int body = nbytes & ~15;
+        if (body > 0) {
+            if (lane == 0) {
+                // order earlier generic-proxy reads of the stage before the TMA writes
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                             ::"r"(smem_addr(sb->bar)), "r"(body * nrows) : "memory");
+                for (int k = 0; k < nrows; ++k) {
+                    const uint8_t *rb = src_row(p, src, g[k]) + A;
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+                        "[%0], [%1], %2, [%3];"
+                        ::"r"(smem_addr(stage + k * SPB)), "l"(rb), "r"(body),
+                          "r"(smem_addr(sb->bar)) : "memory");
+                }
+            }
+            for (int k = 0; k < nrows; ++k) {
+                const uint8_t *rb = src_row(p, src, g[k]) + A;
+                for (int b = body + lane; b < nbytes; b += 32) stage[k * SPB + b] = __ldg(rb + b);
+            }
+            uint32_t done = 0;
+            while (!done) {
+                asm volatile(
+                    "{\n .reg .pred P;\n"
+                    " mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
+                    " selp.b32 %0, 1, 0, P;\n}\n"
+                    : "=r"(done) : "r"(smem_addr(sb->bar)), "r"(sb->phase) : "memory");
+            }
+            sb->phase ^= 1u;
+            return;
+        }
+    }
     if (aligned) {
         const int nw = nbytes >> 2;
         for (int k = 0; k < nrows; ++k) {
@@ -191,6 +251,12 @@ __device__ __forceinline__ void ct_stage(const SlabParams &p, const uint8_t *src
             for (int b = lane; b < nbytes; b += 32) stage[k * SPB + b] = __ldg(rb + b);
         }
     }
+}
+
+// span start aligned for staging; rows are TMA-eligible when 16-B aligned
+__device__ __forceinline__ int ct_span_base(int sx0) { return sx0 & ~15; }
+__device__ __forceinline__ bool ct_rows_aligned16(const void *src, int64_t pitch) {
+    return ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)pitch) & 15) == 0;
 }
 
 template <int S>
@@ -222,9 +288,10 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
     // staged column span [A, sx1): covers clamp(X0-r .. X0+TW+r-1)
     const int sx0 = max(0, X0 - r);
     const int sx1 = min(W, X0 + g.TW + r);
-    const int A = sx0 & ~3;
-    const bool aligned = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)(p.src_pitch)) & 3) == 0;
+    const int A = ct_span_base(sx0);
+    const bool aligned = ct_rows_aligned16(src, p.src_pitch);
     const int SPB = g.SPB;
+    StageBar sbar = ct_stage_init(lane);
 
     // pass 0 = coarse; pass 1 = fine for coarse bin `beta`
     uint32_t tile_mask = 0;
@@ -265,7 +332,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
 #pragma unroll
             for (int k = 0; k < CT_STAGE_ROWS; ++k) gr[k] = clampi(Y0 + j0 + k, 0, H - 1);
             __syncwarp();
-            ct_stage(p, src, stage, SPB, gr, nr, A, sx1, aligned, lane);
+            ct_stage(p, src, stage, SPB, gr, nr, A, sx1, aligned, lane, &sbar);
             __syncwarp();
             // per column: count the batch's bins in 4-bit lanes of two words
             // (no shared-memory read-modify-write chain), then add the
@@ -313,7 +380,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
                 gr[1] = clampi(y + r, 0, H - 1);
                 if (gr[0] != gr[1]) {
                     __syncwarp();
-                    ct_stage(p, src, stage, SPB, gr, 2, A, sx1, aligned, lane);
+                    ct_stage(p, src, stage, SPB, gr, 2, A, sx1, aligned, lane, &sbar);
                     __syncwarp();
                     // two counter updates per column; U columns per batch with all
                     // loads issued before any store (addresses are distinct)

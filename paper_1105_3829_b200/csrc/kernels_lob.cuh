@@ -48,7 +48,7 @@ __host__ __device__ inline LobGeom lob_geom(int L, int r) {
     g.NCP = (g.NC + 31) & ~31;
     g.col_bytes = g.NCP * 256;
     g.cum_bytes = g.NCP * 16;
-    g.stage_bytes = LOB_STAGE_ROWS * ((g.NC + 8 + 15) & ~15);
+    g.stage_bytes = LOB_STAGE_ROWS * ((g.NC + 16 + 15) & ~15);
     g.out_bytes = (g.TW + 15) & ~15;
     g.warp_bytes = g.col_bytes + g.cum_bytes + g.stage_bytes + g.out_bytes;
     return g;
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(32) k_lob_u8(SlabParams p, int tiles_x, int ti
     uint8_t *cum = smem_raw + g.col_bytes;          // [NCP][16]
     uint8_t *stage = cum + g.cum_bytes;             // [LOB_STAGE_ROWS][SPB]
     uint8_t *orow = stage + g.stage_bytes;          // [TW]
-    const int SPB = (g.NC + 8 + 15) & ~15;
+    const int SPB = (g.NC + 16 + 15) & ~15;
 
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int W = p.W, H = p.H;
@@ -131,8 +131,9 @@ __global__ void __launch_bounds__(32) k_lob_u8(SlabParams p, int tiles_x, int ti
     const uint32_t rank = p.rank;
     const int sx0 = max(0, X0 - r);
     const int sx1 = min(W, X0 + g.TW + r);
-    const int A = sx0 & ~3;
-    const bool aligned = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)(p.src_pitch)) & 3) == 0;
+    const int A = ct_span_base(sx0);
+    const bool aligned = ct_rows_aligned16(src, p.src_pitch);
+    StageBar sbar = ct_stage_init(lane);
 
     const int q = lane & 15;        // bin slice [16q, 16q+16)
     const int sid = lane >> 4;      // stream
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(32) k_lob_u8(SlabParams p, int tiles_x, int ti
 #pragma unroll
         for (int k = 0; k < LOB_STAGE_ROWS; ++k) gr[k] = clampi(Y0 + j0 + k, 0, H - 1);
         __syncwarp();
-        ct_stage(p, src, stage, SPB, gr, nr, A, sx1, aligned, lane);
+        ct_stage(p, src, stage, SPB, gr, nr, A, sx1, aligned, lane, &sbar);
         __syncwarp();
         for (int c = lane; c < g.NC; c += 32) {
             const int si = clampi(X0 - r + c, 0, W - 1) - A;
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(32) k_lob_u8(SlabParams p, int tiles_x, int ti
             gr[0] = clampi(y - r - 1, 0, H - 1);
             gr[1] = clampi(y + r, 0, H - 1);
             if (gr[0] != gr[1]) {
-                ct_stage(p, src, stage, SPB, gr, 2, A, sx1, aligned, lane);
+                ct_stage(p, src, stage, SPB, gr, 2, A, sx1, aligned, lane, &sbar);
                 __syncwarp();
                 for (int c = lane; c < g.NC; c += 32) {
                     const int si = clampi(X0 - r + c, 0, W - 1) - A;

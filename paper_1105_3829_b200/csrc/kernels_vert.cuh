@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
     uint16_t *hc = reinterpret_cast<uint16_t *>(smem_raw);      // [16][T]
     FC *hf = reinterpret_cast<FC *>(hc + 16 * T);               // [256][T]
     const int r = p.radius, H = p.H, W = p.W;
-    const int SPW = (32 + 2 * r + 8 + 15) & ~15;                // staged row pitch
+    const int SPW = (32 + 2 * r + 16 + 15) & ~15;               // staged row pitch
     uint8_t *stg = reinterpret_cast<uint8_t *>(hf + 256 * T) + (threadIdx.x >> 5) * 2 * SPW;
     const int tid = threadIdx.x, lane = tid & 31;
     const int x = blockIdx.x * T + tid;
@@ -107,8 +107,9 @@ __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
     uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
     const int sx0 = max(0, xw - r), sx1 = min(W, xw + 32 + r);
-    const int A = sx0 & ~3;
-    const bool aligned = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)(p.src_pitch)) & 3) == 0;
+    const int A = ct_span_base(sx0);
+    const bool aligned = ct_rows_aligned16(src, p.src_pitch);
+    StageBar sbar = ct_stage_init(lane);
     // staged index of window column i (0..2r) of this thread
     auto sidx = [&](int i) { return clampi(x - r + i, 0, W - 1) - A; };
     // u8 counters: lane l of warp w at byte 4l+w, so a warp's 32 lanes hit
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
     for (int j = -r; j <= r; ++j) {
         int g = clampi(y0 + j, 0, H - 1);
         __syncwarp();
-        ct_stage(p, src, stg, SPW, &g, 1, A, sx1, aligned, lane);
+        ct_stage(p, src, stg, SPW, &g, 1, A, sx1, aligned, lane, &sbar);
         __syncwarp();
         for (int i = 0; i <= 2 * r; ++i) {
             const unsigned v = stg[sidx(i)];
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
             int g[2] = {clampi(y - r - 1, 0, H - 1), clampi(y + r, 0, H - 1)};
             if (g[0] != g[1]) {
                 __syncwarp();
-                ct_stage(p, src, stg, SPW, g, 2, A, sx1, aligned, lane);
+                ct_stage(p, src, stg, SPW, g, 2, A, sx1, aligned, lane, &sbar);
                 __syncwarp();
                 for (int i = 0; i <= 2 * r; ++i) {
                     const int si = sidx(i);

@@ -229,7 +229,7 @@ static int run(SlabParams p, int B, cudaStream_t s) {
         constexpr int T = 128;
         const int bx = (p.W + T - 1) / T;
         const bool small = true;
-        const int spw = (32 + 2 * p.radius + 8 + 15) & ~15;
+        const int spw = (32 + 2 * p.radius + 16 + 15) & ~15;
         const size_t smem = (size_t)16 * T * 2 + (size_t)256 * T * (small ? 1 : 2) + (size_t)(T / 32) * 2 * spw;
         p.rows_per_cta = rows_per_cta(p, bx, B, small ? 6 : 3);
         dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
