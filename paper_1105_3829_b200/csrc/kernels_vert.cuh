@@ -274,3 +274,175 @@ __global__ void __launch_bounds__(T) k_vert_u16(SlabParams p) {
 }
 
 }  // namespace mtb
+
+namespace mtb {
+
+// ---------------------------------------------------------------------------
+// 16-bit general path, v2.  Same per-thread hierarchy as k_vert_u16 (high
+// byte: 16 + 256 counters, incremental; low byte: 16 + 256 counters
+// restricted to the selected high byte H), but the restricted level is
+// rebuilt from per-column SORTED arrays instead of rescanning the n x n
+// window: the CTA keeps, for every column of its halo'd stripe, the n
+// pixels of the column's current vertical span in ascending order.  The
+// window pixels with high byte H are then, in each of the 2r+1 columns, the
+// run [lower_bound(256H), lower_bound(256H+256)) -- two binary searches per
+// column plus the (short) runs, instead of n^2 loads.  Moving down a row
+// deletes the leaving value and inserts the entering one in each sorted
+// column (one shift of the elements between the two positions).
+__device__ __forceinline__ int lower_bound_u16(const uint16_t *a, int n, unsigned v) {
+    int lo = 0, len = n;
+    while (len > 0) {
+        const int half = len >> 1;
+        if (a[lo + half] < v) {
+            lo += half + 1;
+            len -= half + 1;
+        } else {
+            len = half;
+        }
+    }
+    return lo;
+}
+
+template <typename CNT, int T>
+__global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CNT *tc = reinterpret_cast<CNT *>(smem_raw);  // [16][T]   high nibble
+    CNT *tf = tc + 16 * T;                        // [256][T]  high byte
+    CNT *lc = tf + 256 * T;                       // [16][T]   bits 4..7 | high byte == curH
+    CNT *lf = lc + 16 * T;                        // [256][T]  low byte  | high byte == curH
+    uint16_t *scol = reinterpret_cast<uint16_t *>(lf + 256 * T);  // [NCOL][n] sorted columns
+    const int tid = threadIdx.x;
+    const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
+    const int NCOL = T + 2 * r;
+    const int X0 = blockIdx.x * T;
+    const int x = X0 + tid;
+    const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
+    if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
+    const int y1 = min(y0 + p.rows_per_cta, p.row_end);
+    const uint16_t *src = static_cast<const uint16_t *>(p.src) + blockIdx.z * p.src_img_stride;
+    uint16_t *dst = static_cast<uint16_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
+    const uint16_t *lut = static_cast<const uint16_t *>(p.lut);
+    const int xc = min(x, W - 1);  // threads beyond the edge compute a clamped column, store nothing
+
+    // sorted columns at row y0 (insertion sort of each column's span)
+    for (int k = tid; k < NCOL; k += T) {
+        uint16_t *a = scol + k * n;
+        const int gx = clampi(X0 - r + k, 0, W - 1);
+        for (int j = 0; j < n; ++j) {
+            const uint16_t v = __ldg(src_row(p, src, clampi(y0 - r + j, 0, H - 1)) + gx);
+            int i = j;
+            while (i > 0 && a[i - 1] > v) {
+                a[i] = a[i - 1];
+                --i;
+            }
+            a[i] = v;
+        }
+    }
+    for (int b = 0; b < 16; ++b) tc[b * T + tid] = 0;
+    for (int b = 0; b < 256; ++b) tf[b * T + tid] = 0;
+    for (int j = -r; j <= r; ++j) {
+        const uint16_t *row = src_row(p, src, clampi(y0 + j, 0, H - 1));
+        for (int i = -r; i <= r; ++i) {
+            const unsigned v = __ldg(row + clampi(xc + i, 0, W - 1));
+            tc[(v >> 12) * T + tid] += 1;
+            tf[(v >> 8) * T + tid] += 1;
+        }
+    }
+    __syncthreads();
+    int curH = -1;
+    const uint32_t rank = p.rank;
+    for (int y = y0; y < y1; ++y) {
+        if (y > y0) {
+            const int yo = clampi(y - r - 1, 0, H - 1);
+            const int yi = clampi(y + r, 0, H - 1);
+            if (yo != yi) {
+                const uint16_t *ro = src_row(p, src, yo);
+                const uint16_t *ri = src_row(p, src, yi);
+                // window counters of this thread
+                for (int i = -r; i <= r; ++i) {
+                    const int c = clampi(xc + i, 0, W - 1);
+                    const unsigned vo = __ldg(ro + c);
+                    const unsigned vi = __ldg(ri + c);
+                    if (vo == vi) continue;
+                    tc[(vo >> 12) * T + tid] -= 1;
+                    tf[(vo >> 8) * T + tid] -= 1;
+                    tc[(vi >> 12) * T + tid] += 1;
+                    tf[(vi >> 8) * T + tid] += 1;
+                    if ((int)(vo >> 8) == curH) {
+                        lc[((vo >> 4) & 15) * T + tid] -= 1;
+                        lf[(vo & 255) * T + tid] -= 1;
+                    }
+                    if ((int)(vi >> 8) == curH) {
+                        lc[((vi >> 4) & 15) * T + tid] += 1;
+                        lf[(vi & 255) * T + tid] += 1;
+                    }
+                }
+                __syncthreads();  // everyone done reading the sorted columns
+                // sorted columns: delete the leaving value, insert the entering one
+                for (int k = tid; k < NCOL; k += T) {
+                    const int gx = clampi(X0 - r + k, 0, W - 1);
+                    const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
+                    if (vo == vi) continue;
+                    uint16_t *a = scol + k * n;
+                    const int io = lower_bound_u16(a, n, vo);  // a[io] == vo
+                    int ii = lower_bound_u16(a, n, vi);
+                    if (ii > io) {
+                        for (int q = io; q < ii - 1; ++q) a[q] = a[q + 1];
+                        a[ii - 1] = (uint16_t)vi;
+                    } else {
+                        for (int q = io; q > ii; --q) a[q] = a[q - 1];
+                        a[ii] = (uint16_t)vi;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        uint32_t acc = 0;
+        int b = 0;
+        for (; b < 15; ++b) {
+            const uint32_t c = tc[b * T + tid];
+            if (acc + c >= rank) break;
+            acc += c;
+        }
+        int hb = b * 16;
+        for (const int e = hb + 15; hb < e; ++hb) {
+            const uint32_t c = tf[hb * T + tid];
+            if (acc + c >= rank) break;
+            acc += c;
+        }
+        if (hb != curH) {  // rebuild the restricted low-byte level from the sorted columns
+            curH = hb;
+            for (int k = 0; k < 16; ++k) lc[k * T + tid] = 0;
+            for (int k = 0; k < 256; ++k) lf[k * T + tid] = 0;
+            const unsigned lo_v = (unsigned)hb << 8, hi_v = lo_v + 256;
+            for (int j = 0; j <= 2 * r; ++j) {
+                const int k = clampi(xc - X0 + j, 0, NCOL - 1);  // stripe column of window column j
+                const uint16_t *a = scol + k * n;
+                const int e0 = lower_bound_u16(a, n, lo_v);
+                if (e0 >= n || a[e0] >= hi_v) continue;
+                const int e1 = lower_bound_u16(a, n, hi_v);
+                for (int e = e0; e < e1; ++e) {
+                    const unsigned v = a[e];
+                    lc[((v >> 4) & 15) * T + tid] += 1;
+                    lf[(v & 255) * T + tid] += 1;
+                }
+            }
+        }
+        int lb = 0;
+        for (; lb < 15; ++lb) {
+            const uint32_t c = lc[lb * T + tid];
+            if (acc + c >= rank) break;
+            acc += c;
+        }
+        int lo = lb * 16;
+        for (const int e = lo + 15; lo < e; ++lo) {
+            const uint32_t c = lf[lo * T + tid];
+            if (acc + c >= rank) break;
+            acc += c;
+        }
+        const unsigned v = ((unsigned)hb << 8) | (unsigned)lo;
+        if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint16_t)v;
+    }
+}
+
+}  // namespace mtb

@@ -118,10 +118,11 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     const CtmfGeom g = ctmf_geom(S, p.radius);
     const int rows = p.row_end - p.row_begin;
     const int tiles_x = (p.W + g.TW - 1) / g.TW;
-    const int want = sm_count() * 2 * CT_WARPS * 2;
+    const int want = sm_count() * 3 * CT_WARPS * 2;
     int ty = (want + tiles_x * B - 1) / (tiles_x * B);
     int th = (rows + ty - 1) / ty;
-    const int min_th = env_int("MTB_CT_MIN_TH", S == 8 ? 48 : 16);
+    const int n = 2 * p.radius + 1;
+    const int min_th = env_int("MTB_CT_MIN_TH", n / 3 > 16 ? n / 3 : 16);
     if (th < min_th) th = min_th;
     th = env_int("MTB_CT_TH", th);
     if (th > rows) th = rows;
@@ -244,7 +245,19 @@ static int run(SlabParams p, int B, cudaStream_t s) {
         dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
         return wide ? launch(k_vert_u8<uint32_t, T>, grid, T, smem, s, p, "k_vert_u8<u32>")
                     : launch(k_vert_u8<uint16_t, T>, grid, T, smem, s, p, "k_vert_u8<u16>");
-    } else {
+    } else if (!wide && force != "vert") {
+        constexpr int T = 64;
+        const int n16 = (int)n;
+        const size_t smem = (size_t)2 * (16 + 256) * T * 2 + (size_t)(T + 2 * p.radius) * n16 * 2;
+        if (smem <= 200 * 1024) {
+            const int bx = (p.W + T - 1) / T;
+            p.rows_per_cta = rows_per_cta(p, bx, B, 2);
+            if (p.rows_per_cta < 2 * n16) p.rows_per_cta = 2 * n16 < p.row_end - p.row_begin ? 2 * n16 : p.row_end - p.row_begin;
+            dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
+            return launch(k_vert2_u16<uint16_t, T>, grid, T, smem, s, p, "k_vert2_u16<u16>");
+        }
+    }
+    {
         constexpr int T = 64;
         const int bx = (p.W + T - 1) / T;
         const size_t smem = (size_t)2 * (16 + 256) * T * (wide ? 4 : 2);

@@ -33,6 +33,8 @@ def main():
         px = workloads.cfg1_uniform_u8(4096, 4096)
     elif a.cfg == 3:
         px = workloads.cfg3_uniform_u16()
+    elif a.cfg == 5:
+        px = workloads.cfg5_batch_u8(1, 2048, 2048)[0]
     elif a.cfg == 4:
         px = workloads.cfg4_three_gauss_u16()
     radii = [int(x) for x in a.radii.split(",")] if a.radii else list(workloads.CONFIG_RADII[a.cfg])
