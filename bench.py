@@ -328,12 +328,61 @@ def run_ours(args):
     }
     if e2e:
         line["e2e"] = e2e
+    if ws == 1 and not args.no_extra:
+        line["other_configs"] = other_configs(mtb, torch, flush)
     if ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(base, args.cpu_budget)
     print(json.dumps(line))
     if pg:
         pg.destroy_process_group()
     return 0
+
+
+def other_configs(mtb, torch, flush, reps: int = 2):
+    """The other BASELINE configs, device-resident, L2 flushed, event-timed
+    (informational: the headline `value` is config 2).  Mpix/s per radius and
+    HBM-roofline fraction (2 B/px for u8, 4 B/px for u16)."""
+    from paper_1105_3829_b200 import _lib
+
+    peak, _ = _peaks()
+    res = {}
+
+    def timed(src, r, out, **kw):
+        mtb.rank_filter(src, r, out=out, **kw)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            mtb.rank_filter(src, r, out=out, **kw)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return min(ts)
+
+    specs = [
+        ("config1_512x512_u8", lambda: workloads.cfg1_uniform_u8(), workloads.CONFIG_RADII[1], 2),
+        ("config3_4096x4096_u16", lambda: workloads.cfg3_uniform_u16(), workloads.CONFIG_RADII[3], 4),
+        ("config4_8192x8192_u16_adaptive", lambda: workloads.cfg4_three_gauss_u16(),
+         workloads.CONFIG_RADII[4], 4),
+        ("config5_64x2048x2048_u8_batch", lambda: workloads.cfg5_batch_u8(), workloads.CONFIG_RADII[5], 2),
+    ]
+    for name, gen, radii, bpp in specs:
+        px = gen()
+        src = torch.from_numpy(px).cuda()
+        out = torch.empty_like(src)
+        npx = px.size
+        entry = {}
+        for r in radii:
+            ms = timed(src, r, out, adaptive=("adaptive" in name))
+            entry[str(r)] = {"ms": round(ms, 4), "mpix_s": round(npx / (ms * 1e-3) / 1e6, 1),
+                             "hbm_frac": round(bpp * npx / (ms * 1e-3) / 1e9 / peak, 5),
+                             "kernel": _lib.last_kernel()}
+        res[name] = entry
+        del src, out
+        torch.cuda.empty_cache()
+    return res
 
 
 def main():
@@ -345,6 +394,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip configs 1,3,4,5")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     if args.impl == "reference":

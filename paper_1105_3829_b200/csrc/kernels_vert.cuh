@@ -415,16 +415,26 @@ __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
             for (int k = 0; k < 16; ++k) lc[k * T + tid] = 0;
             for (int k = 0; k < 256; ++k) lf[k * T + tid] = 0;
             const unsigned lo_v = (unsigned)hb << 8, hi_v = lo_v + 256;
-            for (int j = 0; j <= 2 * r; ++j) {
-                const int k = clampi(xc - X0 + j, 0, NCOL - 1);  // stripe column of window column j
-                const uint16_t *a = scol + k * n;
-                const int e0 = lower_bound_u16(a, n, lo_v);
-                if (e0 >= n || a[e0] >= hi_v) continue;
-                const int e1 = lower_bound_u16(a, n, hi_v);
-                for (int e = e0; e < e1; ++e) {
-                    const unsigned v = a[e];
-                    lc[((v >> 4) & 15) * T + tid] += 1;
-                    lf[(v & 255) * T + tid] += 1;
+            // batches of 8 columns: the 16 binary searches are independent
+            // (issued back to back), the counter updates follow
+            for (int j0 = 0; j0 <= 2 * r; j0 += 8) {
+                int e0[8], e1[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = clampi(xc - X0 + min(j0 + u, 2 * r), 0, NCOL - 1);
+                    const uint16_t *a = scol + k * n;
+                    e0[u] = lower_bound_u16(a, n, lo_v);
+                    e1[u] = (j0 + u <= 2 * r) ? lower_bound_u16(a, n, hi_v) : e0[u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = clampi(xc - X0 + min(j0 + u, 2 * r), 0, NCOL - 1);
+                    const uint16_t *a = scol + k * n;
+                    for (int e = e0[u]; e < e1[u]; ++e) {
+                        const unsigned v = a[e];
+                        lc[((v >> 4) & 15) * T + tid] += 1;
+                        lf[(v & 255) * T + tid] += 1;
+                    }
                 }
             }
         }
