@@ -50,7 +50,7 @@ __host__ __device__ inline CtmfGeom ctmf_geom(int S, int r) {
     g.NC = g.TW + 2 * r;
     g.NCP = (g.NC + 31) & ~31;
     g.colh_bytes = 2 * g.NCP * 16;
-    g.below_bytes = g.NCP * 2;
+    g.below_bytes = (g.NCP + 8) * 2;  // + dummy counter
     g.SPB = (g.NC + 16 + 15) & ~15;
     g.warp_bytes = g.colh_bytes + ((g.below_bytes + 15) & ~15) + CT_STAGE_ROWS * g.SPB;
     return g;
@@ -139,6 +139,37 @@ __device__ __forceinline__ void ct_window(const uint4 *colA, const uint4 *colB, 
         for (int i = 0; i < 9; ++i) LB[i] = PB[i] = 0;
     }
     uint32_t acc[9];
+    if (q >= 5 && (int64_t)NC * n < 65536) {
+        // exclusive prefix I_j over the (up to 64) chunk sums, two rounds of
+        // 32; window(t) = I_{t+q} + P_{t+q} - I_t.  Packed u16 lanes never
+        // carry: every prefix is <= NC*n < 2^16.
+        uint32_t IA[9], IB[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+            uint32_t a = LA[i], b = LB[i];
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t ta = __shfl_up_sync(0xffffffffu, a, d);
+                const uint32_t tb = __shfl_up_sync(0xffffffffu, b, d);
+                if (lane >= d) {
+                    a += ta;
+                    b += tb;
+                }
+            }
+            const uint32_t totA = __shfl_sync(0xffffffffu, a, 31);
+            IA[i] = a - LA[i];            // exclusive, round A
+            IB[i] = b - LB[i] + totA;     // exclusive, round B
+        }
+        const int idx = lane + q;
+        const bool hiB = idx >= 32;
+        const int sl = idx & 31;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+            const uint32_t xa = __shfl_sync(0xffffffffu, IA[i] + PA[i], sl);
+            const uint32_t xb = __shfl_sync(0xffffffffu, IB[i] + PB[i], sl);
+            acc[i] = (hiB ? xb : xa) - IA[i];
+        }
+    } else {
 #pragma unroll
     for (int i = 0; i < 9; ++i) acc[i] = 0;
     for (int k = 0; k <= q; ++k) {
@@ -160,6 +191,7 @@ __device__ __forceinline__ void ct_window(const uint4 *colA, const uint4 *colB, 
                 acc[i] += hiB ? b : a;
             }
         }
+    }
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) ws[i] = acc[i];
@@ -339,13 +371,19 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
             // expanded counts to the column record with two 16-B RMWs.
             for (int c = lane; c < g.NC; c += 32) {
                 const int si = clampi(X0 - r + c, 0, W - 1) - A;
-                uint32_t n0 = 0, n1 = 0, nb = 0;  // nibble counts bins 0-7 / 8-15, below
+                uint64_t nib = 0;  // 16 four-bit counts (batch <= 8 rows)
+                uint32_t nb = 0;   // below (fine passes)
                 for (int k = 0; k < nr; ++k) {
-                    const int b = bin_of(stage[k * SPB + si]);
-                    if (b >= 0 && b < 8) n0 += 1u << (4 * b);
-                    else if (b >= 8 && b < 16) n1 += 1u << (4 * (b - 8));
-                    else if (b == 16) nb += 1;
+                    const unsigned v = stage[k * SPB + si];
+                    if (!fine) {
+                        nib += 1ull << (4 * (v >> 4));
+                    } else {
+                        const int hb = (int)(v >> 4);
+                        nib += (hb == beta) ? (1ull << (4 * (v & 15))) : 0ull;
+                        nb += (hb < beta) ? 1u : 0u;
+                    }
                 }
+                const uint32_t n0 = (uint32_t)nib, n1 = (uint32_t)(nib >> 32);
                 const int sl = ct_slot<S>(c);
                 if (n0) {
                     const uint32_t t = n0 >> 4;
@@ -383,39 +421,39 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
                     ct_stage(p, src, stage, SPB, gr, 2, A, sx1, aligned, lane, &sbar);
                     __syncwarp();
                     // two counter updates per column; U columns per batch with all
-                    // loads issued before any store (addresses are distinct)
+                    // loads issued before any store (addresses are distinct;
+                    // ignored values hit a dummy counter)
                     constexpr int U = 4;
+                    uint16_t *h16 = reinterpret_cast<uint16_t *>(colA);  // colA | colB | below | dummy
+                    const int offB = g.NCP * 8, offBelow = 2 * g.NCP * 8, dummy = offBelow + g.NCP;
+                    auto idx_of = [&](int c, int sl, unsigned v) -> int {
+                        if (!fine) return ((v & 0x80) ? offB : 0) + sl * 8 + (int)((v >> 4) & 7);
+                        const int hb = (int)(v >> 4);
+                        const int in = ((v & 8) ? offB : 0) + sl * 8 + (int)(v & 7);
+                        return hb == beta ? in : (hb < beta ? offBelow + c : dummy);
+                    };
                     for (int c0 = lane; c0 < g.NC; c0 += 32 * U) {
-                        uint16_t *po[U], *pi[U];
+                        int io[U], ii[U];
                         uint16_t vo[U], vi[U];
 #pragma unroll
                         for (int u = 0; u < U; ++u) {
-                            const int c = c0 + 32 * u;
-                            po[u] = pi[u] = nullptr;
-                            if (c < g.NC) {
-                                const int si = clampi(X0 - r + c, 0, W - 1) - A;
-                                const int bo = bin_of(stage[si]), bi = bin_of(stage[SPB + si]);
-                                if (bo != bi) {
-                                    const int sl = ct_slot<S>(c);
-                                    auto ptr = [&](int b) -> uint16_t * {
-                                        if (b < 0) return nullptr;
-                                        if (b == 16) return below + c;
-                                        return reinterpret_cast<uint16_t *>((b & 8) ? colB + sl : colA + sl) + (b & 7);
-                                    };
-                                    po[u] = ptr(bo);
-                                    pi[u] = ptr(bi);
-                                }
-                            }
+                            const int c = min(c0 + 32 * u, g.NC - 1);
+                            const int si = clampi(X0 - r + c, 0, W - 1) - A;
+                            const int sl = ct_slot<S>(c);
+                            const unsigned a = stage[si], b = stage[SPB + si];
+                            io[u] = idx_of(c, sl, a);
+                            ii[u] = idx_of(c, sl, b);
+                            if (c0 + 32 * u >= g.NC || io[u] == ii[u]) io[u] = ii[u] = dummy;
                         }
 #pragma unroll
                         for (int u = 0; u < U; ++u) {
-                            vo[u] = po[u] ? *po[u] : 0;
-                            vi[u] = pi[u] ? *pi[u] : 0;
+                            vo[u] = h16[io[u]];
+                            vi[u] = h16[ii[u]];
                         }
 #pragma unroll
                         for (int u = 0; u < U; ++u) {
-                            if (po[u]) *po[u] = vo[u] - 1;
-                            if (pi[u]) *pi[u] = vi[u] + 1;
+                            if (io[u] != dummy) h16[io[u]] = vo[u] - 1;
+                            if (ii[u] != dummy) h16[ii[u]] = vi[u] + 1;
                         }
                     }
                 }
