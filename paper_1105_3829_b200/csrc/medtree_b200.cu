@@ -71,15 +71,19 @@ static int validate(const SlabParams &p, int B) {
     return MTB_OK;
 }
 
+// Opt in to the dynamic shared memory a launch needs (static __shared__
+// of the kernel counts against the default 48 KB too, so always set it).
+template <typename K>
+static int set_smem(K kernel, size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    return MTB_OK;
+}
+
 template <typename K>
 static int launch(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   const SlabParams &p, const char *name) {
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("cudaFuncSetAttribute: ") +
-                                                          cudaGetErrorString(e));
-    }
+    if (int rc = set_smem(kernel, smem)) return rc;
     kernel<<<grid, block, smem, s>>>(p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
@@ -133,10 +137,7 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     dim3 grid((tiles + CT_WARPS - 1) / CT_WARPS, 1, B);
     const size_t smem = (size_t)g.warp_bytes * CT_WARPS;
     auto kern = k_ctmf_u8<S>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    }
+    if (int rc = set_smem(kern, smem)) return rc;
     kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_ctmf_u8: ") + cudaGetErrorString(e));
@@ -168,10 +169,7 @@ static int run_lob_u8_l(SlabParams p, int B, cudaStream_t s) {
     dim3 grid(tiles_x * tiles_y, 1, B);
     const size_t smem = (size_t)g.warp_bytes;
     auto kern = k_lob_u8<L>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    }
+    if (int rc = set_smem(kern, smem)) return rc;
     kern<<<grid, 32, smem, s>>>(p, tiles_x, tiles_y);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_lob_u8: ") + cudaGetErrorString(e));
