@@ -126,7 +126,7 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     int ty = (want + tiles_x * B - 1) / (tiles_x * B);
     int th = (rows + ty - 1) / ty;
     const int n = 2 * p.radius + 1;
-    const int min_th = env_int("MTB_CT_MIN_TH", n / 3 > 16 ? n / 3 : 16);
+    const int min_th = env_int("MTB_CT_MIN_TH", n / 3 > 32 ? n / 3 : 32);
     if (th < min_th) th = min_th;
     th = env_int("MTB_CT_TH", th);
     if (th > rows) th = rows;
@@ -217,12 +217,12 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     const std::string force = forced_kernel();
     // Kernel choice (measured on B200, tools/probe.py):
     //   median, n <= 7          -> selection networks (any bit depth)
-    //   8-bit, 24 <= r <= 127   -> column-histogram CTMF (O(1) in r)
+    //   8-bit, 18 <= r <= 127   -> column-histogram CTMF (O(1) in r)
     //   otherwise               -> per-column vertical histograms (any r/rank)
     if ((force.empty() || force == "sortnet") && sortnet_applies<P>(p)) return run_sortnet<P>(p, B, s);
     if (sizeof(P) == 1 && p.radius <= 63 && force == "lob") return run_lob_u8_l<32>(p, B, s);
     if (sizeof(P) == 1 && !wide &&
-        (force == "ctmf" || (force.empty() && p.radius >= env_int("MTB_CT_MIN_R", 24))))
+        (force == "ctmf" || (force.empty() && p.radius >= env_int("MTB_CT_MIN_R", 18))))
         return run_ctmf_u8(p, B, s);
     if (sizeof(P) == 1 && n * n <= 255 && force != "vert") {
         constexpr int T = 128;
