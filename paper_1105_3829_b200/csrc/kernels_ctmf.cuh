@@ -285,71 +285,6 @@ __device__ __forceinline__ void ct_stage(const SlabParams &p, const uint8_t *src
     }
 }
 
-// ---- double-buffered row staging: issue the TMA for the next row while the
-// current one is consumed.  Two stage sets, one mbarrier per set per warp.
-struct StagePipe {
-    uint64_t *bar;      // bar[0], bar[1]
-    uint32_t phase[2];
-};
-
-__device__ __forceinline__ StagePipe ct_pipe_init(int lane) {
-    __shared__ __align__(8) uint64_t s_pbar[32][2];
-    uint64_t *bar = s_pbar[threadIdx.x >> 5];
-    if (lane == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar + 1)) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    StagePipe sp;
-    sp.bar = bar;
-    sp.phase[0] = sp.phase[1] = 0u;
-    return sp;
-}
-
-// returns true when the copy completes on the set's mbarrier (TMA path)
-__device__ __forceinline__ bool ct_pipe_issue(const SlabParams &p, const uint8_t *src, uint8_t *stage,
-                                              int SPB, const int *g, int nrows, int A, int sx1,
-                                              bool aligned, int lane, StagePipe &sp, int set) {
-    const int nbytes = sx1 - A;
-    const int body = nbytes & ~15;
-    if (aligned && body > 0) {
-        if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                         ::"r"(smem_addr(sp.bar + set)), "r"(body * nrows) : "memory");
-            for (int k = 0; k < nrows; ++k) {
-                const uint8_t *rb = src_row(p, src, g[k]) + A;
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
-                    "[%0], [%1], %2, [%3];"
-                    ::"r"(smem_addr(stage + k * SPB)), "l"(rb), "r"(body),
-                      "r"(smem_addr(sp.bar + set)) : "memory");
-            }
-        }
-        for (int k = 0; k < nrows; ++k) {
-            const uint8_t *rb = src_row(p, src, g[k]) + A;
-            for (int b = body + lane; b < nbytes; b += 32) stage[k * SPB + b] = __ldg(rb + b);
-        }
-        return true;
-    }
-    ct_stage(p, src, stage, SPB, g, nrows, A, sx1, aligned, lane, nullptr);
-    return false;
-}
-
-__device__ __forceinline__ void ct_pipe_wait(StagePipe &sp, int set, bool tma) {
-    if (!tma) return;
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n .reg .pred P;\n"
-            " mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
-            " selp.b32 %0, 1, 0, P;\n}\n"
-            : "=r"(done) : "r"(smem_addr(sp.bar + set)), "r"(sp.phase[set]) : "memory");
-    }
-    sp.phase[set] ^= 1u;
-}
-
 // span start aligned for staging; rows are TMA-eligible when 16-B aligned
 __device__ __forceinline__ int ct_span_base(int sx0) { return sx0 & ~15; }
 __device__ __forceinline__ bool ct_rows_aligned16(const void *src, int64_t pitch) {

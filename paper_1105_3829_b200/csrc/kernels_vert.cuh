@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
     FC *hf = reinterpret_cast<FC *>(hc + 16 * T);               // [256][T]
     const int r = p.radius, H = p.H, W = p.W;
     const int SPW = (32 + 2 * r + 16 + 15) & ~15;               // staged row pitch
-    uint8_t *stg = reinterpret_cast<uint8_t *>(hf + 256 * T) + (threadIdx.x >> 5) * 4 * SPW;  // 2 sets x 2 rows
+    uint8_t *stg = reinterpret_cast<uint8_t *>(hf + 256 * T) + (threadIdx.x >> 5) * 2 * SPW;
     const int tid = threadIdx.x, lane = tid & 31;
     const int x = blockIdx.x * T + tid;
     const int xw = blockIdx.x * T + (tid & ~31);                  // warp's first column
@@ -130,36 +130,16 @@ __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
         }
     }
     const uint32_t rank = p.rank;
-    StagePipe pipe = ct_pipe_init(lane);
-    bool tma = false;
-    auto rows_of = [&](int yy, int *g) {
-        g[0] = clampi(yy - r - 1, 0, H - 1);
-        g[1] = clampi(yy + r, 0, H - 1);
-    };
-    __syncwarp();
-    if (y0 + 1 < y1) {  // prefetch row y0+1 into set 0
-        int g[2];
-        rows_of(y0 + 1, g);
-        tma = ct_pipe_issue(p, src, stg, SPW, g, 2, A, sx1, aligned, lane, pipe, 0);
-    }
     for (int y = y0; y < y1; ++y) {
         if (y > y0) {
-            const int set = (y - y0 - 1) & 1;
-            uint8_t *cur = stg + set * 2 * SPW;
-            ct_pipe_wait(pipe, set, tma);
-            __syncwarp();
-            if (y + 1 < y1) {  // the other set was consumed by row y-1
-                int g[2];
-                rows_of(y + 1, g);
-                ct_pipe_issue(p, src, stg + (set ^ 1) * 2 * SPW, SPW, g, 2, A, sx1, aligned, lane,
-                              pipe, set ^ 1);
-            }
-            int g[2];
-            rows_of(y, g);
+            int g[2] = {clampi(y - r - 1, 0, H - 1), clampi(y + r, 0, H - 1)};
             if (g[0] != g[1]) {
+                __syncwarp();
+                ct_stage(p, src, stg, SPW, g, 2, A, sx1, aligned, lane, &sbar);
+                __syncwarp();
                 for (int i = 0; i <= 2 * r; ++i) {
                     const int si = sidx(i);
-                    const unsigned vo = cur[si], vi = cur[SPW + si];
+                    const unsigned vo = stg[si], vi = stg[SPW + si];
                     if (vo == vi) continue;
                     if ((vo >> 4) != (vi >> 4)) {
                         hc[(vo >> 4) * T + tid] -= 1;
@@ -184,7 +164,6 @@ __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
             acc += c;
         }
         if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
-        __syncwarp();  // row consumed: its stage set may be refilled
     }
 }
 

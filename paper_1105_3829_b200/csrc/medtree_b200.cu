@@ -224,13 +224,12 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     if (sizeof(P) == 1 && !wide &&
         (force == "ctmf" || (force.empty() && p.radius >= env_int("MTB_CT_MIN_R", 18))))
         return run_ctmf_u8(p, B, s);
-    if (sizeof(P) == 1 && !wide && force != "vert" &&
-        (n * n <= 255 || force == "vert2" || env_int("MTB_VERT2_U16", 0))) {
+    if (sizeof(P) == 1 && !wide && force != "vert" && (n * n <= 255 || force == "vert2")) {
         constexpr int T = 128;
         const int bx = (p.W + T - 1) / T;
         const bool small = n * n <= 255;
         const int spw = (32 + 2 * p.radius + 16 + 15) & ~15;
-        const size_t smem = (size_t)16 * T * 2 + (size_t)256 * T * (small ? 1 : 2) + (size_t)(T / 32) * 4 * spw;
+        const size_t smem = (size_t)16 * T * 2 + (size_t)256 * T * (small ? 1 : 2) + (size_t)(T / 32) * 2 * spw;
         p.rows_per_cta = rows_per_cta(p, bx, B, small ? 6 : 3);
         dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
         return small ? launch(k_vert2_u8<uint8_t, T>, grid, T, smem, s, p, "k_vert2_u8<u8>")
