@@ -20,6 +20,30 @@
 
 namespace mtb {
 
+// Incremental rank tracking for the vertical kernels.  m = previous output
+// value, L = number of window pixels below m (kept current by the row
+// updates).  Walk m down while L >= rank, up while L + h[m] < rank; the
+// median moves little from row to row, so this replaces the 32-counter
+// descent.  Returns false (caller falls back to the full descent) after
+// `limit` steps.
+template <typename FC>
+__device__ __forceinline__ bool walk_rank(const FC *hf, int T, int fo, uint32_t rank, int &m,
+                                          uint32_t &L, int limit) {
+    int steps = 0;
+    while (L >= rank) {
+        if (++steps > limit) return false;
+        --m;
+        L -= hf[m * T + fo];
+    }
+    while (true) {
+        const uint32_t c = hf[m * T + fo];
+        if (L + c >= rank) return true;
+        if (++steps > limit) return false;
+        L += c;
+        ++m;
+    }
+}
+
 // 8-bit: coarse[16] (v>>4) + fine[256] (v) counters per thread.
 template <typename CNT, int T>
 __global__ void __launch_bounds__(T) k_vert_u8(SlabParams p) {
@@ -47,6 +71,8 @@ __global__ void __launch_bounds__(T) k_vert_u8(SlabParams p) {
             hf[v * T + tid] += 1;
         }
     }
+    int mprev = -1;   // previous output value (-1: none yet)
+    uint32_t Lb = 0;  // window pixels below mprev
     const uint32_t rank = p.rank;
     for (int y = y0; y < y1; ++y) {
         if (y > y0) {
@@ -59,27 +85,38 @@ __global__ void __launch_bounds__(T) k_vert_u8(SlabParams p) {
                     const int c = clampi(x + i, 0, W - 1);
                     const unsigned vo = __ldg(ro + c);
                     const unsigned vi = __ldg(ri + c);
-                    hc[(vo >> 4) * T + tid] -= 1;
+                    if (vo == vi) continue;
+                    Lb += ((int)vi < mprev ? 1u : 0u) - ((int)vo < mprev ? 1u : 0u);
+                    if ((vo >> 4) != (vi >> 4)) {
+                        hc[(vo >> 4) * T + tid] -= 1;
+                        hc[(vi >> 4) * T + tid] += 1;
+                    }
                     hf[vo * T + tid] -= 1;
-                    hc[(vi >> 4) * T + tid] += 1;
                     hf[vi * T + tid] += 1;
                 }
             }
         }
-        // coarse-to-fine counting descent
-        uint32_t acc = 0;
-        int b = 0;
-        for (; b < 15; ++b) {
-            const uint32_t c = hc[b * T + tid];
-            if (acc + c >= rank) break;
-            acc += c;
+        int v = mprev;
+        uint32_t L = Lb;
+        if (mprev < 0 || !walk_rank(hf, T, tid, rank, v, L, 24)) {
+            // coarse-to-fine counting descent
+            uint32_t acc = 0;
+            int b = 0;
+            for (; b < 15; ++b) {
+                const uint32_t c = hc[b * T + tid];
+                if (acc + c >= rank) break;
+                acc += c;
+            }
+            v = b * 16;
+            for (const int e = v + 15; v < e; ++v) {
+                const uint32_t c = hf[v * T + tid];
+                if (acc + c >= rank) break;
+                acc += c;
+            }
+            L = acc;
         }
-        int v = b * 16;
-        for (const int e = v + 15; v < e; ++v) {
-            const uint32_t c = hf[v * T + tid];
-            if (acc + c >= rank) break;
-            acc += c;
-        }
+        mprev = v;
+        Lb = L;
         dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
     }
 }
@@ -129,6 +166,8 @@ __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
             hf[v * T + fo] += 1;
         }
     }
+    int mprev = -1;
+    uint32_t Lb = 0;
     const uint32_t rank = p.rank;
     for (int y = y0; y < y1; ++y) {
         if (y > y0) {
@@ -141,6 +180,7 @@ __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
                     const int si = sidx(i);
                     const unsigned vo = stg[si], vi = stg[SPW + si];
                     if (vo == vi) continue;
+                    Lb += ((int)vi < mprev ? 1u : 0u) - ((int)vo < mprev ? 1u : 0u);
                     if ((vo >> 4) != (vi >> 4)) {
                         hc[(vo >> 4) * T + tid] -= 1;
                         hc[(vi >> 4) * T + tid] += 1;
@@ -150,19 +190,26 @@ __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
                 }
             }
         }
-        uint32_t acc = 0;
-        int b = 0;
-        for (; b < 15; ++b) {
-            const uint32_t c = hc[b * T + tid];
-            if (acc + c >= rank) break;
-            acc += c;
+        int v = mprev;
+        uint32_t L = Lb;
+        if (mprev < 0 || !walk_rank(hf, T, fo, rank, v, L, 24)) {
+            uint32_t acc = 0;
+            int b = 0;
+            for (; b < 15; ++b) {
+                const uint32_t c = hc[b * T + tid];
+                if (acc + c >= rank) break;
+                acc += c;
+            }
+            v = b * 16;
+            for (const int e = v + 15; v < e; ++v) {
+                const uint32_t c = hf[v * T + fo];
+                if (acc + c >= rank) break;
+                acc += c;
+            }
+            L = acc;
         }
-        int v = b * 16;
-        for (const int e = v + 15; v < e; ++v) {
-            const uint32_t c = hf[v * T + fo];
-            if (acc + c >= rank) break;
-            acc += c;
-        }
+        mprev = v;
+        Lb = L;
         if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
     }
 }
