@@ -199,13 +199,19 @@ def run_ours(args):
     from paper_1105_3829_b200 import _lib
 
     ws, rank, local = _dist()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
+    backend = os.environ.get("MTB_BENCH_BACKEND", "nccl")  # gloo: CPU-side smoke of the N>1 logic
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         pg = dist
     base = workloads.cfg2_blur_sp_u8(H, W)
     # weak scaling: rank k owns rows [k*H, (k+1)*H) of N stacked copies
@@ -266,7 +272,7 @@ def run_ours(args):
     ms_r = {r: sum(e0.elapsed_time(e1) for e0, e1 in evs[r]) / args.steps for r in RADII}
     ms_step = sum(ms_r.values())
     if pg:
-        t = torch.tensor([ms_step] + [ms_r[r] for r in RADII], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms_step] + [ms_r[r] for r in RADII], device=red_dev, dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         ms_step = float(t[0])
         ms_r = {r: float(t[i + 1]) for i, r in enumerate(RADII)}
@@ -291,7 +297,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / e2e_steps
         if pg:
-            tt = torch.tensor([dt], device=dev, dtype=torch.float64)
+            tt = torch.tensor([dt], device=red_dev, dtype=torch.float64)
             pg.all_reduce(tt, op=pg.ReduceOp.MAX)
             dt = float(tt[0])
         e2e = {"value": round(len(RADII) * H * W * ws / dt / 1e6, 3), "unit": UNIT,

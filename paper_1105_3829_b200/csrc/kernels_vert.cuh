@@ -85,13 +85,10 @@ __global__ void __launch_bounds__(T) k_vert_u8(SlabParams p) {
                     const int c = clampi(x + i, 0, W - 1);
                     const unsigned vo = __ldg(ro + c);
                     const unsigned vi = __ldg(ri + c);
-                    if (vo == vi) continue;
                     Lb += ((int)vi < mprev ? 1u : 0u) - ((int)vo < mprev ? 1u : 0u);
-                    if ((vo >> 4) != (vi >> 4)) {
-                        hc[(vo >> 4) * T + tid] -= 1;
-                        hc[(vi >> 4) * T + tid] += 1;
-                    }
+                    hc[(vo >> 4) * T + tid] -= 1;
                     hf[vo * T + tid] -= 1;
+                    hc[(vi >> 4) * T + tid] += 1;
                     hf[vi * T + tid] += 1;
                 }
             }
