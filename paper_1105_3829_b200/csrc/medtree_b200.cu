@@ -18,6 +18,29 @@
 
 namespace mtb {
 
+// Spread of the 16-bit value distribution: number of distinct high bytes
+// among a strided sample of the source rows.  Selects the 16-bit kernel:
+// a wide spread (high byte of the median changes often) favours the
+// sorted-column rebuild of k_vert2_u16; a compact one (changes rare)
+// favours the leaner k_vert_u16.  Both are exact.
+__global__ void k_highbyte_spread(const uint16_t *src, int64_t pitch, int rows, int W, int *out) {
+    __shared__ int seen[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) seen[i] = 0;
+    __syncthreads();
+    const int total = 1 << 14;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+        const int y = (int)(((int64_t)i * 7919) % rows);
+        const int x = (int)(((int64_t)i * 104729) % W);
+        atomicAdd(&seen[src[(int64_t)y * pitch + x] >> 8], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int d = 0;
+        for (int b = 0; b < 256; ++b) d += seen[b] > 0 ? 1 : 0;  // distinct high bytes
+        *out = d;
+    }
+}
+
 static thread_local std::string g_err;
 static thread_local const char *g_kernel = "";
 static std::atomic<uint64_t> g_launches{0};
@@ -207,6 +230,25 @@ static int run_sortnet(SlabParams p, int B, cudaStream_t s) {
     }
 }
 
+// true when the 16-bit image's high bytes are widely spread (see k_highbyte_spread)
+static bool wide_spread_u16(const SlabParams &p, cudaStream_t s) {
+    static int *d_out = nullptr;
+    static int h_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!d_out || h_dev != dev) {
+        if (cudaMalloc(&d_out, sizeof(int)) != cudaSuccess) return true;
+        h_dev = dev;
+    }
+    const int rows = p.src_rows;
+    k_highbyte_spread<<<1, 256, 0, s>>>(static_cast<const uint16_t *>(p.src), p.src_pitch, rows, p.W, d_out);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    int h = 256;
+    cudaMemcpyAsync(&h, d_out, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    return h > env_int("MTB_U16_SPREAD", 24);
+}
+
 template <typename P>
 static int run(SlabParams p, int B, cudaStream_t s) {
     int rc = validate(p, B);
@@ -243,7 +285,7 @@ static int run(SlabParams p, int B, cudaStream_t s) {
         dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
         return wide ? launch(k_vert_u8<uint32_t, T>, grid, T, smem, s, p, "k_vert_u8<u32>")
                     : launch(k_vert_u8<uint16_t, T>, grid, T, smem, s, p, "k_vert_u8<u16>");
-    } else if (!wide && force != "vert") {
+    } else if (!wide && force != "vert" && (force == "vert2" || wide_spread_u16(p, s))) {
         constexpr int T = 64;
         const int n16 = (int)n;
         const size_t smem = (size_t)2 * (16 + 256) * T * 2 + (size_t)(T + 2 * p.radius) * n16 * 2;
