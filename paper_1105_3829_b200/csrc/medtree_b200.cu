@@ -225,8 +225,12 @@ template <typename P>
 static int run_sortnet(SlabParams p, int B, cudaStream_t s) {
     switch (p.radius) {
         case 1: return run_sortnet_n<3, 4, 8, P>(p, B, s, "k_sortnet<3>");
-        case 2: return run_sortnet_n<5, 2, 8, P>(p, B, s, "k_sortnet<5>");
-        default: return run_sortnet_n<7, 1, 8, P>(p, B, s, "k_sortnet<7>");
+        case 2:
+            if (env_int("MTB_SN5_K", 2) == 3) return run_sortnet_n<5, 3, 8, P>(p, B, s, "k_sortnet<5,K3>");
+            return run_sortnet_n<5, 2, 8, P>(p, B, s, "k_sortnet<5>");
+        default:
+            if (env_int("MTB_SN7_K", 2) == 2) return run_sortnet_n<7, 2, 8, P>(p, B, s, "k_sortnet<7,K2>");
+            return run_sortnet_n<7, 1, 8, P>(p, B, s, "k_sortnet<7>");
     }
 }
 
