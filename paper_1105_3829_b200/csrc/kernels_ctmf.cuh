@@ -234,7 +234,10 @@ __device__ __forceinline__ void ct_stage(const SlabParams &p, const uint8_t *src
                                          bool aligned, int lane, StageBar *sb = nullptr) {
     const int nbytes = sx1 - A;
     if (sb && aligned) {
-        const int body = nbytes & ~15;
+        // rows are 16-B aligned with a pitch that is a multiple of 16, so the
+        // span rounded up to 16 bytes stays inside the row's pitch: one bulk
+        // copy per row, no tail (bytes past sx1 are never indexed)
+        const int body = (nbytes + 15) & ~15;
         if (body > 0) {
             if (lane == 0) {
                 // order earlier generic-proxy reads of the stage before the TMA writes
@@ -249,10 +252,6 @@ __device__ __forceinline__ void ct_stage(const SlabParams &p, const uint8_t *src
                         ::"r"(smem_addr(stage + k * SPB)), "l"(rb), "r"(body),
                           "r"(smem_addr(sb->bar)) : "memory");
                 }
-            }
-            for (int k = 0; k < nrows; ++k) {
-                const uint8_t *rb = src_row(p, src, g[k]) + A;
-                for (int b = body + lane; b < nbytes; b += 32) stage[k * SPB + b] = __ldg(rb + b);
             }
             uint32_t done = 0;
             while (!done) {

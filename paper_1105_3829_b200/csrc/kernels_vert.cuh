@@ -48,8 +48,9 @@ __device__ __forceinline__ bool walk_rank(const FC *hf, int T, int fo, uint32_t 
 template <typename CNT, int T>
 __global__ void __launch_bounds__(T) k_vert_u8(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    CNT *hc = reinterpret_cast<CNT *>(smem_raw);  // [16][T]
-    CNT *hf = hc + 16 * T;                        // [256][T]
+    // distinct restrict pointers: the coarse and fine update chains may overlap
+    CNT *__restrict__ hc = reinterpret_cast<CNT *>(smem_raw);  // [16][T]
+    CNT *__restrict__ hf = reinterpret_cast<CNT *>(smem_raw) + 16 * T;  // [256][T]
     const int tid = threadIdx.x;
     const int x = blockIdx.x * T + tid;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
@@ -126,8 +127,8 @@ __global__ void __launch_bounds__(T) k_vert_u8(SlabParams p) {
 template <typename FC, int T>
 __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint16_t *hc = reinterpret_cast<uint16_t *>(smem_raw);      // [16][T]
-    FC *hf = reinterpret_cast<FC *>(hc + 16 * T);               // [256][T]
+    uint16_t *__restrict__ hc = reinterpret_cast<uint16_t *>(smem_raw);           // [16][T]
+    FC *__restrict__ hf = reinterpret_cast<FC *>(smem_raw + 16 * T * sizeof(uint16_t));  // [256][T]
     const int r = p.radius, H = p.H, W = p.W;
     const int SPW = (32 + 2 * r + 16 + 15) & ~15;               // staged row pitch
     uint8_t *stg = reinterpret_cast<uint8_t *>(hf + 256 * T) + (threadIdx.x >> 5) * 2 * SPW;
