@@ -291,7 +291,8 @@ __device__ __forceinline__ bool ct_rows_aligned16(const void *src, int64_t pitch
 }
 
 template <int S>
-__global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int tiles_x, int tiles_y) {
+__global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int tiles_x, int tiles_y,
+                                                        uint8_t *__restrict__ snap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -324,6 +325,51 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
     const int SPB = g.SPB;
     StageBar sbar = ct_stage_init(lane);
 
+    // ---- per-tile snapshot of every column's initial span (rows clamp(Y0-r ..
+    // Y0+r)): its full 256-bin histogram and its cumulative coarse counts,
+    // built once in a global workspace; every pass then initialises its
+    // column histograms from it in O(columns) instead of rescanning n rows.
+    const size_t snap_stride = (size_t)g.NCP * (256 + 16);
+    uint8_t *snap_f = nullptr, *snap_c = nullptr;
+    if (snap) {
+        const size_t tg = (size_t)blockIdx.z * tiles_x * tiles_y + tile;
+        snap_f = snap + tg * snap_stride;              // [NCP][256] fine counts
+        snap_c = snap_f + (size_t)g.NCP * 256;         // [NCP][16]  count below 16*b
+        uint8_t *scr = reinterpret_cast<uint8_t *>(colA) + lane * 260;  // lane-private column
+        for (int g0 = 0; g0 < g.NC; g0 += 32) {
+            const int c = g0 + lane;
+            const int gx = clampi(X0 - r + min(c, g.NC - 1), 0, W - 1);
+            for (int i = 0; i < 65; ++i) reinterpret_cast<uint32_t *>(scr)[i] = 0;
+            int j = -r;
+            for (; j + 3 <= r; j += 4) {
+                const unsigned v0 = __ldg(src_row(p, src, clampi(Y0 + j, 0, H - 1)) + gx);
+                const unsigned v1 = __ldg(src_row(p, src, clampi(Y0 + j + 1, 0, H - 1)) + gx);
+                const unsigned v2 = __ldg(src_row(p, src, clampi(Y0 + j + 2, 0, H - 1)) + gx);
+                const unsigned v3 = __ldg(src_row(p, src, clampi(Y0 + j + 3, 0, H - 1)) + gx);
+                scr[v0] += 1;
+                scr[v1] += 1;
+                scr[v2] += 1;
+                scr[v3] += 1;
+            }
+            for (; j <= r; ++j) scr[__ldg(src_row(p, src, clampi(Y0 + j, 0, H - 1)) + gx)] += 1;
+            if (c < g.NC) {
+                uint4 *outf = reinterpret_cast<uint4 *>(snap_f + (size_t)c * 256);
+                uint32_t acc = 0, cw[4] = {0, 0, 0, 0};
+                for (int q = 0; q < 16; ++q) {
+                    const uint32_t *w4 = reinterpret_cast<const uint32_t *>(scr) + 4 * q;
+                    const uint4 chunk = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                    outf[q] = chunk;
+                    cw[q >> 2] |= acc << (8 * (q & 3));
+                    acc += __vsadu4(chunk.x, 0) + __vsadu4(chunk.y, 0) + __vsadu4(chunk.z, 0) +
+                           __vsadu4(chunk.w, 0);
+                }
+                *reinterpret_cast<uint4 *>(snap_c + (size_t)c * 16) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+            }
+        }
+        __syncwarp();
+    }
+    const uint32_t nspan = (uint32_t)(2 * r + 1);
+
     // pass 0 = coarse; pass 1 = fine for coarse bin `beta`
     uint32_t tile_mask = 0;
     int beta = -1;
@@ -352,6 +398,35 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
             }
         };
         // --- column histograms for row Y0: rows clamp(Y0-r .. Y0+r)
+        __syncwarp();
+        if (snap) {
+            for (int c = lane; c < g.NCP; c += 32) {
+                uint32_t cnt[4] = {0, 0, 0, 0};
+                uint32_t bl = 0;
+                if (c < g.NC) {
+                    const uint4 cu = __ldcg(reinterpret_cast<const uint4 *>(snap_c + (size_t)c * 16));
+                    if (!fine) {
+                        // coarse counts = next cumulative - cumulative (bytewise, no borrow)
+                        const uint32_t cwv[4] = {cu.x, cu.y, cu.z, cu.w};
+                        const uint32_t nxt[4] = {__funnelshift_r(cwv[0], cwv[1], 8), __funnelshift_r(cwv[1], cwv[2], 8),
+                                                 __funnelshift_r(cwv[2], cwv[3], 8), __funnelshift_r(cwv[3], nspan, 8)};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) cnt[i] = nxt[i] - cwv[i];
+                    } else {
+                        const uint4 f = __ldcg(reinterpret_cast<const uint4 *>(snap_f + (size_t)c * 256 + 16 * beta));
+                        cnt[0] = f.x; cnt[1] = f.y; cnt[2] = f.z; cnt[3] = f.w;
+                        const uint32_t wsel = beta < 8 ? (beta < 4 ? cu.x : cu.y) : (beta < 12 ? cu.z : cu.w);
+                        bl = (wsel >> (8 * (beta & 3))) & 0xffu;
+                    }
+                }
+                const int sl = c < g.NC ? ct_slot<S>(c) : c;
+                colA[sl] = make_uint4(__byte_perm(cnt[0], 0, 0x4140), __byte_perm(cnt[0], 0, 0x4342),
+                                      __byte_perm(cnt[1], 0, 0x4140), __byte_perm(cnt[1], 0, 0x4342));
+                colB[sl] = make_uint4(__byte_perm(cnt[2], 0, 0x4140), __byte_perm(cnt[2], 0, 0x4342),
+                                      __byte_perm(cnt[3], 0, 0x4140), __byte_perm(cnt[3], 0, 0x4342));
+                below[c] = (uint16_t)bl;
+            }
+        } else {
         for (int c = lane; c < g.NCP; c += 32) {
             colA[c] = make_uint4(0, 0, 0, 0);
             colB[c] = make_uint4(0, 0, 0, 0);
@@ -404,6 +479,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
                 }
                 if (nb) below[c] += nb;
             }
+        }
         }
         __syncwarp();
         // --- lane window at x_t, row Y0

@@ -140,6 +140,21 @@ static const char *forced_kernel() {
     return v ? v : "";
 }
 
+// keep freed stream-ordered allocations in the device's default pool so the
+// per-launch workspace does not go back to the driver at every sync
+static void keep_pool_memory() {
+    static int done[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = 4ull << 30;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = 1;
+}
+
 template <int S>
 static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     const CtmfGeom g = ctmf_geom(S, p.radius);
@@ -161,8 +176,19 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     const size_t smem = (size_t)g.warp_bytes * CT_WARPS;
     auto kern = k_ctmf_u8<S>;
     if (int rc = set_smem(kern, smem)) return rc;
-    kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y);
+    // per-tile column snapshots (stream-ordered pool allocation, kept cached)
+    uint8_t *snap = nullptr;
+    const size_t snap_bytes = (size_t)tiles * B * g.NCP * (256 + 16);
+    if (env_int("MTB_CT_SNAP", 1)) {
+        keep_pool_memory();
+        if (cudaMallocAsync(reinterpret_cast<void **>(&snap), snap_bytes, s) != cudaSuccess) {
+            cudaGetLastError();
+            snap = nullptr;  // fall back to rescanning the spans
+        }
+    }
+    kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y, snap);
     cudaError_t e = cudaGetLastError();
+    if (snap) cudaFreeAsync(snap, s);
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_ctmf_u8: ") + cudaGetErrorString(e));
     g_kernel = S == 8 ? "k_ctmf_u8<8>" : "k_ctmf_u8<16>";
     g_launches.fetch_add(1, std::memory_order_relaxed);
