@@ -291,13 +291,15 @@ __device__ __forceinline__ bool ct_rows_aligned16(const void *src, int64_t pitch
 }
 
 template <int S>
-__global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int tiles_x, int tiles_y,
+__global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int tiles_x, int tiles_y,
                                                         uint8_t *__restrict__ snap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int tile = blockIdx.x * CT_WARPS + warp;
-    if (tile >= tiles_x * tiles_y) return;  // warp-uniform; no block barriers below
+    // persistent warps: tiles are dealt round-robin to the resident warps
+    // (no partial last wave); warp-uniform control, no block barriers
+    const int first_tile = blockIdx.x * CT_WARPS + warp;
+    if (first_tile >= tiles_x * tiles_y) return;
     const int r = p.radius;
     const CtmfGeom g = ctmf_geom(S, r);
     unsigned char *base = smem_raw + (size_t)warp * g.warp_bytes;
@@ -306,6 +308,8 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
     uint16_t *below = reinterpret_cast<uint16_t *>(base + g.colh_bytes);
     uint8_t *stage = base + g.colh_bytes + ((g.below_bytes + 15) & ~15);
 
+    StageBar sbar = ct_stage_init(lane);
+    for (int tile = first_tile; tile < tiles_x * tiles_y; tile += gridDim.x * CT_WARPS) {
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int W = p.W, H = p.H;
     const int X0 = tx * g.TW;
@@ -323,7 +327,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
     const int A = ct_span_base(sx0);
     const bool aligned = ct_rows_aligned16(src, p.src_pitch);
     const int SPB = g.SPB;
-    StageBar sbar = ct_stage_init(lane);
+    __syncwarp();
 
     // ---- per-tile snapshot of every column's initial span (rows clamp(Y0-r ..
     // Y0+r)): its full 256-bin histogram and its cumulative coarse counts,
@@ -593,6 +597,8 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_ctmf_u8(SlabParams p, int til
         if (!fine) tile_mask = __reduce_or_sync(0xffffffffu, tile_mask);
         __syncwarp();
     }
+    __syncwarp();
+    }  // tiles
 }
 
 }  // namespace mtb

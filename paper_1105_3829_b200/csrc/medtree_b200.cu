@@ -164,7 +164,7 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     int ty = (want + tiles_x * B - 1) / (tiles_x * B);
     int th = (rows + ty - 1) / ty;
     const int n = 2 * p.radius + 1;
-    const int min_th = env_int("MTB_CT_MIN_TH", n / 3 > 32 ? n / 3 : 32);
+    const int min_th = env_int("MTB_CT_MIN_TH", n / 3 > 24 ? n / 3 : 24);
     if (th < min_th) th = min_th;
     th = env_int("MTB_CT_TH", th);
     if (th > rows) th = rows;
@@ -172,10 +172,17 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     p.rows_per_cta = th;
     const int tiles_y = (rows + th - 1) / th;
     const int tiles = tiles_x * tiles_y;
-    dim3 grid((tiles + CT_WARPS - 1) / CT_WARPS, 1, B);
     const size_t smem = (size_t)g.warp_bytes * CT_WARPS;
     auto kern = k_ctmf_u8<S>;
     if (int rc = set_smem(kern, smem)) return rc;
+    // persistent grid: as many CTAs as are resident at once (per image)
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CT_WARPS * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    int ctas = (tiles + CT_WARPS - 1) / CT_WARPS;
+    const int resident = (sm_count() * per_sm + B - 1) / B;
+    if (env_int("MTB_CT_PERSIST", 1) && ctas > resident) ctas = resident > 0 ? resident : 1;
+    dim3 grid(ctas, 1, B);
     // per-tile column snapshots (stream-ordered pool allocation, kept cached)
     uint8_t *snap = nullptr;
     const size_t snap_bytes = (size_t)tiles * B * g.NCP * (256 + 16);
