@@ -160,27 +160,35 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     const CtmfGeom g = ctmf_geom(S, p.radius);
     const int rows = p.row_end - p.row_begin;
     const int tiles_x = (p.W + g.TW - 1) / g.TW;
-    const int want = sm_count() * 3 * CT_WARPS * 2;
-    int ty = (want + tiles_x * B - 1) / (tiles_x * B);
-    int th = (rows + ty - 1) / ty;
-    const int n = 2 * p.radius + 1;
-    const int min_th = env_int("MTB_CT_MIN_TH", n / 3 > 24 ? n / 3 : 24);
-    if (th < min_th) th = min_th;
-    th = env_int("MTB_CT_TH", th);
-    if (th > rows) th = rows;
-    if (th < 1) th = 1;
-    p.rows_per_cta = th;
-    const int tiles_y = (rows + th - 1) / th;
-    const int tiles = tiles_x * tiles_y;
     const size_t smem = (size_t)g.warp_bytes * CT_WARPS;
     auto kern = k_ctmf_u8<S>;
     if (int rc = set_smem(kern, smem)) return rc;
-    // persistent grid: as many CTAs as are resident at once (per image)
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CT_WARPS * 32, smem);
     if (per_sm < 1) per_sm = 1;
+    // Tile height: near max(24, n/3) rows, adjusted so that the tiles divide
+    // evenly over the resident warps (k full rounds, no ragged last round).
+    const int n = 2 * p.radius + 1;
+    const int64_t warps = (int64_t)sm_count() * per_sm * CT_WARPS;
+    const double per_stripe = (double)warps / ((double)tiles_x * B);  // warps per column stripe
+    const int target = env_int("MTB_CT_MIN_TH", n / 3 > 24 ? n / 3 : 24);
+    int th;
+    if (per_stripe >= 1.0) {
+        int k = (int)((double)rows / (target * per_stripe) + 0.5);
+        if (k < 1) k = 1;
+        th = (int)((rows + (int64_t)(k * per_stripe) - 1) / (int64_t)(k * per_stripe));
+    } else {
+        th = target;
+    }
+    th = env_int("MTB_CT_TH", th);
+    if (th < 8) th = 8 < rows ? 8 : rows;
+    if (th > rows) th = rows;
+    p.rows_per_cta = th;
+    const int tiles_y = (rows + th - 1) / th;
+    const int tiles = tiles_x * tiles_y;
+    // persistent grid: as many CTAs as are resident at once (per image)
     int ctas = (tiles + CT_WARPS - 1) / CT_WARPS;
-    const int resident = (sm_count() * per_sm + B - 1) / B;
+    const int resident = (int)((sm_count() * per_sm + B - 1) / B);
     if (env_int("MTB_CT_PERSIST", 1) && ctas > resident) ctas = resident > 0 ? resident : 1;
     dim3 grid(ctas, 1, B);
     // per-tile column snapshots (stream-ordered pool allocation, kept cached)
