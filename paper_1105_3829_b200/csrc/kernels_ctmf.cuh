@@ -377,6 +377,11 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
     // pass 0 = coarse; pass 1 = fine for coarse bin `beta`
     uint32_t tile_mask = 0;
     int beta = -1;
+    // rows of the tile (relative to Y0) where coarse bin b = lane occurs,
+    // recorded by the coarse pass; fine pass b sweeps only up to rlast and
+    // resolves only from rfirst (before it, only the column histograms move)
+    int rfirst = 1 << 30, rlast = -1;
+    int yfirst = Y0, ylast = Y1 - 1;
     for (int pass = 0;; ++pass) {
         if (pass > 0) {
             if (tile_mask == 0) break;
@@ -386,6 +391,10 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
             tile_mask &= ~(1u << beta);
         }
         const bool fine = pass > 0;
+        if (fine) {
+            yfirst = Y0 + __shfl_sync(0xffffffffu, rfirst, beta);
+            ylast = Y0 + __shfl_sync(0xffffffffu, rlast, beta);
+        }
         // bin of value v in this pass: 0..15, 16 = "below" (fine only), -1 = ignored
         auto bin_of = [&](unsigned v) -> int {
             if (!fine) return (int)(v >> 4);
@@ -489,7 +498,8 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
         // --- lane window at x_t, row Y0
         uint32_t ws[8], wb;
         ct_window<S>(colA, colB, below, fine, lane, r, g.NC, ws, wb);
-        for (int y = Y0; y < Y1; ++y) {
+        const int yend = fine ? ylast + 1 : Y1;
+        for (int y = Y0; y < yend; ++y) {
             if (y > Y0) {
                 // --- advance column histograms one row
                 int gr[CT_STAGE_ROWS];
@@ -537,8 +547,11 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
                     }
                 }
                 __syncwarp();
+                if (y < yfirst) continue;  // no output of this row needs this pass
                 // --- lane window at x_t for the new row, from the column histograms
                 ct_window<S>(colA, colB, below, fine, lane, r, g.NC, ws, wb);
+            } else if (y < yfirst) {
+                continue;
             }
             // --- slide right over the lane's S outputs
             uint32_t w[8];
@@ -547,6 +560,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
             uint32_t wbl = wb;
             uint8_t *drow = dst + (int64_t)(y - p.row_begin) * p.dst_pitch;
             uint32_t outw[S / 4];
+            uint32_t row_mask = 0;  // coarse pass: bins of this row's outputs
             const bool full = (xt + S <= W) && ((reinterpret_cast<uintptr_t>(drow + xt) & 3) == 0);
             if (fine) {
                 if (full) {
@@ -575,7 +589,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
                 if (!fine) {
                     uint32_t k = rank;
                     const int b = ct_descend(w, k);
-                    tile_mask |= (xt + s < W) ? (1u << b) : 0u;
+                    row_mask |= (xt + s < W) ? (1u << b) : 0u;
                     outw[s >> 2] = (s & 3) ? (outw[s >> 2] | ((uint32_t)b << (8 * (s & 3)))) : (uint32_t)b;
                 } else if ((int)cur == beta) {
                     uint32_t k = rank - wbl;
@@ -583,6 +597,14 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
                     uint32_t v = (uint32_t)(beta << 4) | (uint32_t)b;
                     if (lut) v = __ldg(lut + v);
                     outw[s >> 2] = (outw[s >> 2] & ~(0xffu << (8 * (s & 3)))) | (v << (8 * (s & 3)));
+                }
+            }
+            if (!fine) {
+                const uint32_t rm = __reduce_or_sync(0xffffffffu, row_mask);
+                tile_mask |= rm;
+                if (lane < 16 && ((rm >> lane) & 1u)) {
+                    if (rlast < 0) rfirst = y - Y0;
+                    rlast = y - Y0;
                 }
             }
             if (full) {
@@ -594,7 +616,6 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
             }
             __syncwarp();
         }
-        if (!fine) tile_mask = __reduce_or_sync(0xffffffffu, tile_mask);
         __syncwarp();
     }
     __syncwarp();

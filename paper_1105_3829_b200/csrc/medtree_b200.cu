@@ -304,12 +304,12 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     const std::string force = forced_kernel();
     // Kernel choice (measured on B200, tools/probe.py):
     //   median, n <= 7          -> selection networks (any bit depth)
-    //   8-bit, 13 <= r <= 127   -> column-histogram CTMF (O(1) in r)
+    //   8-bit, 14 <= r <= 127   -> column-histogram CTMF (O(1) in r)
     //   otherwise               -> per-column vertical histograms (any r/rank)
     if ((force.empty() || force == "sortnet") && sortnet_applies<P>(p)) return run_sortnet<P>(p, B, s);
     if (sizeof(P) == 1 && p.radius <= 63 && force == "lob") return run_lob_u8_l<32>(p, B, s);
     if (sizeof(P) == 1 && !wide &&
-        (force == "ctmf" || (force.empty() && p.radius >= env_int("MTB_CT_MIN_R", 13))))
+        (force == "ctmf" || (force.empty() && p.radius >= env_int("MTB_CT_MIN_R", 14))))
         return run_ctmf_u8(p, B, s);
     if (sizeof(P) == 1 && !wide && force != "vert" && (n * n <= 255 || force == "vert2")) {
         constexpr int T = 128;
