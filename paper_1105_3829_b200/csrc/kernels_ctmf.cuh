@@ -125,7 +125,7 @@ __device__ __forceinline__ void ct_chunk(const uint4 *colA, const uint4 *colB, c
 }
 
 template <int S>
-__device__ __forceinline__ void ct_window(const uint4 *colA, const uint4 *colB, const uint16_t *below,
+__device__ __noinline__ void ct_window(const uint4 *colA, const uint4 *colB, const uint16_t *below,
                                           bool fine, int lane, int r, int NC, uint32_t (&ws)[8],
                                           uint32_t &wb) {
     const int n = 2 * r + 1, q = n / S, m = n - q * S;
