@@ -348,6 +348,25 @@ __device__ __forceinline__ int lower_bound_u16(const uint16_t *a, int n, unsigne
     return lo;
 }
 
+// U independent branchless lower_bounds over sorted arrays of the same
+// length n, interleaved step by step so their shared-memory loads overlap
+// (the step count depends only on n, so the loop is warp-uniform).
+template <int U>
+__device__ __forceinline__ void lower_bound_multi(const uint16_t *const (&a)[U], int n,
+                                                  const unsigned (&v)[U], int (&out)[U]) {
+    int base[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) base[u] = 0;
+    for (int len = n; len > 1;) {
+        const int half = len >> 1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) base[u] += (a[u][base[u] + half] < v[u]) ? half : 0;
+        len -= half;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) out[u] = base[u] + ((a[u][base[u]] < v[u]) ? 1 : 0);
+}
+
 template <typename CNT, int T>
 __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -429,8 +448,12 @@ __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
                     const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
                     if (vo == vi) continue;
                     uint16_t *a = scol + k * n;
-                    const int io = lower_bound_u16(a, n, vo);  // a[io] == vo
-                    int ii = lower_bound_u16(a, n, vi);
+                    const uint16_t *const aa[2] = {a, a};
+                    const unsigned vv[2] = {vo, vi};
+                    int pos[2];
+                    lower_bound_multi<2>(aa, n, vv, pos);
+                    const int io = pos[0];  // a[io] == vo
+                    const int ii = pos[1];
                     if (ii > io) {
                         for (int q = io; q < ii - 1; ++q) a[q] = a[q + 1];
                         a[ii - 1] = (uint16_t)vi;
@@ -462,21 +485,25 @@ __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
             const unsigned lo_v = (unsigned)hb << 8, hi_v = lo_v + 256;
             // batches of 8 columns: the 16 binary searches are independent
             // (issued back to back), the counter updates follow
+            // the run of each column starts at lower_bound(256H) and is
+            // scanned up to the first value >= 256H+256
             for (int j0 = 0; j0 <= 2 * r; j0 += 8) {
-                int e0[8], e1[8];
+                const uint16_t *aa[8];
+                unsigned vv[8];
+                int e0[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const int k = clampi(xc - X0 + min(j0 + u, 2 * r), 0, NCOL - 1);
-                    const uint16_t *a = scol + k * n;
-                    e0[u] = lower_bound_u16(a, n, lo_v);
-                    e1[u] = (j0 + u <= 2 * r) ? lower_bound_u16(a, n, hi_v) : e0[u];
+                    aa[u] = scol + clampi(xc - X0 + min(j0 + u, 2 * r), 0, NCOL - 1) * n;
+                    vv[u] = lo_v;
                 }
+                lower_bound_multi<8>(aa, n, vv, e0);
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const int k = clampi(xc - X0 + min(j0 + u, 2 * r), 0, NCOL - 1);
-                    const uint16_t *a = scol + k * n;
-                    for (int e = e0[u]; e < e1[u]; ++e) {
+                    if (j0 + u > 2 * r) break;
+                    const uint16_t *a = aa[u];
+                    for (int e = e0[u]; e < n; ++e) {
                         const unsigned v = a[e];
+                        if (v >= hi_v) break;
                         lc[((v >> 4) & 15) * T + tid] += 1;
                         lf[(v & 255) * T + tid] += 1;
                     }
