@@ -367,14 +367,44 @@ __device__ __forceinline__ void lower_bound_multi(const uint16_t *const (&a)[U],
     for (int u = 0; u < U; ++u) out[u] = base[u] + ((a[u][base[u]] < v[u]) ? 1 : 0);
 }
 
+// Counts, per 4-bit digit (v >> shift) & 15, the window values in [lo_v, hi_v)
+// from the sorted columns c0 .. c0+2r of the CTA stripe (sc zeroed first).
+template <typename CNT, int T>
+__device__ __forceinline__ void v2_count_runs(CNT *sc, const uint16_t *scol, int c0, int NCOL, int n, int r,
+                                              unsigned lo_v, unsigned hi_v, int shift) {
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) sc[q * T + tid] = 0;
+    for (int j0 = 0; j0 <= 2 * r; j0 += 8) {
+        const uint16_t *aa[8];
+        unsigned vv[8];
+        int e0[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            aa[u] = scol + min(c0 + min(j0 + u, 2 * r), NCOL - 1) * n;
+            vv[u] = lo_v;
+        }
+        lower_bound_multi<8>(aa, n, vv, e0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (j0 + u > 2 * r) break;
+            const uint16_t *a = aa[u];
+            for (int e = e0[u]; e < n; ++e) {
+                const unsigned v = a[e];
+                if (v >= hi_v) break;
+                sc[((v >> shift) & 15) * T + tid] += 1;
+            }
+        }
+    }
+}
+
 template <typename CNT, int T>
 __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CNT *tc = reinterpret_cast<CNT *>(smem_raw);  // [16][T]   high nibble
     CNT *tf = tc + 16 * T;                        // [256][T]  high byte
-    CNT *lc = tf + 256 * T;                       // [16][T]   bits 4..7 | high byte == curH
-    CNT *lf = lc + 16 * T;                        // [256][T]  low byte  | high byte == curH
-    uint16_t *scol = reinterpret_cast<uint16_t *>(lf + 256 * T);  // [NCOL][n] sorted columns
+    CNT *sc = tf + 256 * T;                       // [16][T]   scratch: nibble counts inside H
+    uint16_t *scol = reinterpret_cast<uint16_t *>(sc + 16 * T);  // [NCOL][n] sorted columns
     const int tid = threadIdx.x;
     const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
     const int NCOL = T + 2 * r;
@@ -413,7 +443,6 @@ __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
         }
     }
     __syncthreads();
-    int curH = -1;
     const uint32_t rank = p.rank;
     for (int y = y0; y < y1; ++y) {
         if (y > y0) {
@@ -432,14 +461,6 @@ __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
                     tf[(vo >> 8) * T + tid] -= 1;
                     tc[(vi >> 12) * T + tid] += 1;
                     tf[(vi >> 8) * T + tid] += 1;
-                    if ((int)(vo >> 8) == curH) {
-                        lc[((vo >> 4) & 15) * T + tid] -= 1;
-                        lf[(vo & 255) * T + tid] -= 1;
-                    }
-                    if ((int)(vi >> 8) == curH) {
-                        lc[((vi >> 4) & 15) * T + tid] += 1;
-                        lf[(vi & 255) * T + tid] += 1;
-                    }
                 }
                 __syncthreads();  // everyone done reading the sorted columns
                 // sorted columns: delete the leaving value, insert the entering one
@@ -478,47 +499,24 @@ __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
             if (acc + c >= rank) break;
             acc += c;
         }
-        if (hb != curH) {  // rebuild the restricted low-byte level from the sorted columns
-            curH = hb;
-            for (int k = 0; k < 16; ++k) lc[k * T + tid] = 0;
-            for (int k = 0; k < 256; ++k) lf[k * T + tid] = 0;
-            const unsigned lo_v = (unsigned)hb << 8, hi_v = lo_v + 256;
-            // batches of 8 columns: the 16 binary searches are independent
-            // (issued back to back), the counter updates follow
-            // the run of each column starts at lower_bound(256H) and is
-            // scanned up to the first value >= 256H+256
-            for (int j0 = 0; j0 <= 2 * r; j0 += 8) {
-                const uint16_t *aa[8];
-                unsigned vv[8];
-                int e0[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    aa[u] = scol + clampi(xc - X0 + min(j0 + u, 2 * r), 0, NCOL - 1) * n;
-                    vv[u] = lo_v;
-                }
-                lower_bound_multi<8>(aa, n, vv, e0);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (j0 + u > 2 * r) break;
-                    const uint16_t *a = aa[u];
-                    for (int e = e0[u]; e < n; ++e) {
-                        const unsigned v = a[e];
-                        if (v >= hi_v) break;
-                        lc[((v >> 4) & 15) * T + tid] += 1;
-                        lf[(v & 255) * T + tid] += 1;
-                    }
-                }
-            }
-        }
+        // low byte: the (rank - acc)-th smallest window value in
+        // [256H, 256H+256).  In every window column those values are one run
+        // of the sorted column; count them per bits 4..7, then count the
+        // selected 16-value sub-run per bits 0..3.
+        const unsigned vb = (unsigned)hb << 8;
+        const int c0 = clampi(xc - X0, 0, NCOL - 1);
+        v2_count_runs<CNT, T>(sc, scol, c0, NCOL, n, r, vb, vb + 256, 4);
         int lb = 0;
         for (; lb < 15; ++lb) {
-            const uint32_t c = lc[lb * T + tid];
+            const uint32_t c = sc[lb * T + tid];
             if (acc + c >= rank) break;
             acc += c;
         }
+        const unsigned vs = vb + 16u * (unsigned)lb;
+        v2_count_runs<CNT, T>(sc, scol, c0, NCOL, n, r, vs, vs + 16, 0);
         int lo = lb * 16;
         for (const int e = lo + 15; lo < e; ++lo) {
-            const uint32_t c = lf[lo * T + tid];
+            const uint32_t c = sc[(lo & 15) * T + tid];
             if (acc + c >= rank) break;
             acc += c;
         }

@@ -333,10 +333,11 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     } else if (!wide && force != "vert" && (force == "vert2" || wide_spread_u16(p, s))) {
         constexpr int T = 64;
         const int n16 = (int)n;
-        const size_t smem = (size_t)2 * (16 + 256) * T * 2 + (size_t)(T + 2 * p.radius) * n16 * 2;
+        const size_t smem = (size_t)(16 + 256 + 16) * T * 2 + (size_t)(T + 2 * p.radius) * n16 * 2;
         if (smem <= 200 * 1024) {
             const int bx = (p.W + T - 1) / T;
-            p.rows_per_cta = rows_per_cta(p, bx, B, 2);
+            const int occ = (int)((227 * 1024) / (smem + 1024));
+            p.rows_per_cta = rows_per_cta(p, bx, B, occ < 1 ? 1 : occ);
             if (p.rows_per_cta < 2 * n16) p.rows_per_cta = 2 * n16 < p.row_end - p.row_begin ? 2 * n16 : p.row_end - p.row_begin;
             dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
             return launch(k_vert2_u16<uint16_t, T>, grid, T, smem, s, p, "k_vert2_u16<u16>");

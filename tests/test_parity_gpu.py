@@ -275,7 +275,7 @@ def _cfg4():
 _FAMILY_CASES = [c for c in G.small_cases() if c[0]["rank"] is None and c[0]["percentile"] is None]
 
 
-@pytest.mark.parametrize("family", ["vert", "ctmf", "lob", "sortnet"])
+@pytest.mark.parametrize("family", ["vert", "vert2", "ctmf", "lob", "sortnet"])
 def test_each_kernel_family_is_exact(family, monkeypatch):
     """MTB_KERNEL forces one family; families that do not apply to a case
     (ctmf/lob: 8-bit only; sortnet: median of n <= 7) fall through to the
@@ -298,5 +298,27 @@ def test_each_kernel_family_is_exact(family, monkeypatch):
         px16 = rng.integers(0, 65536, (70, 90)).astype(np.uint16)
         out16 = mtb.rank_filter(torch.from_numpy(px16).cuda(), min(r, 34)).cpu().numpy()
         assert np.array_equal(out16, O.iot_filter(px16, 2 * min(r, 34) + 1)), (family, r)
-    expect = {"vert": "k_vert_u8", "ctmf": "k_ctmf_u8", "lob": "k_lob_u8", "sortnet": "k_sortnet"}[family]
+    expect = {"vert": "k_vert_u8", "vert2": "k_vert2_u16", "ctmf": "k_ctmf_u8", "lob": "k_lob_u8",
+              "sortnet": "k_sortnet"}[family]
     assert expect in seen, seen
+
+
+@pytest.mark.parametrize("r", [1, 4, 9, 20, 130])
+def test_vert2_u16_ranks_and_counter_widths(r, monkeypatch):
+    """k_vert2_u16 (sorted-column low byte) on wide-spread and compact 16-bit
+    images, at min / max / off-centre ranks.  r=130 (n^2 > 65535, the sorted
+    columns exceed shared memory) must fall back to k_vert_u16, still exact."""
+    from paper_1105_3829_b200 import _lib
+
+    monkeypatch.setenv("MTB_KERNEL", "vert2")
+    rng = np.random.default_rng(40 + r)
+    h, w = (300, 280) if r == 130 else (90, 110)
+    n = 2 * r + 1
+    imgs = [rng.integers(0, 65536, (h, w)).astype(np.uint16),
+            (30000 + rng.normal(0, 300, (h, w))).clip(0, 65535).astype(np.uint16)]
+    for px in imgs:
+        for rank in (1, n * n, (n * n) // 3 + 1):
+            out = mtb.rank_filter(torch.from_numpy(px).cuda(), r, rank=rank).cpu().numpy()
+            expect = "k_vert_u16" if r == 130 else "k_vert2_u16"
+            assert _lib.last_kernel().startswith(expect), _lib.last_kernel()
+            assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (r, rank)
