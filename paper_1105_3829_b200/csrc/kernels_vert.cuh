@@ -323,30 +323,20 @@ __global__ void __launch_bounds__(T) k_vert_u16(SlabParams p) {
 namespace mtb {
 
 // ---------------------------------------------------------------------------
-// 16-bit general path, v2.  Same per-thread hierarchy as k_vert_u16 (high
-// byte: 16 + 256 counters, incremental; low byte: 16 + 256 counters
-// restricted to the selected high byte H), but the restricted level is
-// rebuilt from per-column SORTED arrays instead of rescanning the n x n
-// window: the CTA keeps, for every column of its halo'd stripe, the n
-// pixels of the column's current vertical span in ascending order.  The
-// window pixels with high byte H are then, in each of the 2r+1 columns, the
-// run [lower_bound(256H), lower_bound(256H+256)) -- two binary searches per
-// column plus the (short) runs, instead of n^2 loads.  Moving down a row
-// deletes the leaving value and inserts the entering one in each sorted
-// column (one shift of the elements between the two positions).
-__device__ __forceinline__ int lower_bound_u16(const uint16_t *a, int n, unsigned v) {
-    int lo = 0, len = n;
-    while (len > 0) {
-        const int half = len >> 1;
-        if (a[lo + half] < v) {
-            lo += half + 1;
-            len -= half + 1;
-        } else {
-            len = half;
-        }
-    }
-    return lo;
-}
+// 16-bit general path, v2.  The high byte H of the result comes from the
+// same incremental per-thread counters as k_vert_u16 (16 + 256); the low
+// byte comes from per-column SORTED arrays instead of a second counter
+// level: the CTA keeps, for every column of its halo'd stripe, the n pixels
+// of the column's current vertical span in ascending order, so the window
+// values with high byte H are one run per window column, starting at
+// lower_bound(256H) (2r+1 interleaved branchless binary searches, whose
+// results are kept as u8 run starts for the second pass).  The low byte is
+// then two counting passes over the runs (bits 4..7, then bits 0..3 of the
+// selected 16-value sub-run) into 16 scratch counters.  (Moving the run
+// starts incrementally instead of searching was measured slower: the walk
+// is a chain of dependent loads per column, the searches overlap.)
+// Moving down a row deletes the leaving value and inserts the entering one
+// in each sorted column (one shift of the elements between the positions).
 
 // U independent branchless lower_bounds over sorted arrays of the same
 // length n, interleaved step by step so their shared-memory loads overlap
@@ -367,37 +357,6 @@ __device__ __forceinline__ void lower_bound_multi(const uint16_t *const (&a)[U],
     for (int u = 0; u < U; ++u) out[u] = base[u] + ((a[u][base[u]] < v[u]) ? 1 : 0);
 }
 
-// Counts, per 4-bit digit (v >> shift) & 15, the window values in [lo_v, hi_v)
-// from the sorted columns c0 .. c0+2r of the CTA stripe (sc zeroed first).
-template <typename CNT, int T>
-__device__ __forceinline__ void v2_count_runs(CNT *sc, const uint16_t *scol, int c0, int NCOL, int n, int r,
-                                              unsigned lo_v, unsigned hi_v, int shift) {
-    const int tid = threadIdx.x;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) sc[q * T + tid] = 0;
-    for (int j0 = 0; j0 <= 2 * r; j0 += 8) {
-        const uint16_t *aa[8];
-        unsigned vv[8];
-        int e0[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            aa[u] = scol + min(c0 + min(j0 + u, 2 * r), NCOL - 1) * n;
-            vv[u] = lo_v;
-        }
-        lower_bound_multi<8>(aa, n, vv, e0);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            if (j0 + u > 2 * r) break;
-            const uint16_t *a = aa[u];
-            for (int e = e0[u]; e < n; ++e) {
-                const unsigned v = a[e];
-                if (v >= hi_v) break;
-                sc[((v >> shift) & 15) * T + tid] += 1;
-            }
-        }
-    }
-}
-
 template <typename CNT, int T>
 __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -408,6 +367,7 @@ __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
     const int tid = threadIdx.x;
     const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
     const int NCOL = T + 2 * r;
+    uint8_t *rpos = reinterpret_cast<uint8_t *>(scol + NCOL * n);  // [n][T] run starts
     const int X0 = blockIdx.x * T;
     const int x = X0 + tid;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
@@ -417,6 +377,8 @@ __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
     uint16_t *dst = static_cast<uint16_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint16_t *lut = static_cast<const uint16_t *>(p.lut);
     const int xc = min(x, W - 1);  // threads beyond the edge compute a clamped column, store nothing
+    // window column j of this thread is stripe column c0 + j (global xc - r + j, clamped)
+    const uint16_t *wcol = scol + (xc - X0) * n;
 
     // sorted columns at row y0 (insertion sort of each column's span)
     for (int k = tid; k < NCOL; k += T) {
@@ -499,21 +461,50 @@ __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
             if (acc + c >= rank) break;
             acc += c;
         }
-        // low byte: the (rank - acc)-th smallest window value in
-        // [256H, 256H+256).  In every window column those values are one run
-        // of the sorted column; count them per bits 4..7, then count the
-        // selected 16-value sub-run per bits 0..3.
-        const unsigned vb = (unsigned)hb << 8;
-        const int c0 = clampi(xc - X0, 0, NCOL - 1);
-        v2_count_runs<CNT, T>(sc, scol, c0, NCOL, n, r, vb, vb + 256, 4);
+        // low byte: the (rank - acc)-th smallest window value in [vb, vb+256)
+        const unsigned vb = (unsigned)hb << 8, ve = vb + 256;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) sc[q * T + tid] = 0;
+        for (int j0 = 0; j0 < n; j0 += 8) {
+            const uint16_t *aa[8];
+            unsigned vv[8];
+            int e0[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                aa[u] = wcol + min(j0 + u, n - 1) * n;
+                vv[u] = vb;
+            }
+            lower_bound_multi<8>(aa, n, vv, e0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (j0 + u >= n) break;
+                rpos[(j0 + u) * T + tid] = (uint8_t)e0[u];
+                const uint16_t *a = aa[u];
+                for (int e = e0[u]; e < n; ++e) {
+                    const unsigned v = a[e];
+                    if (v >= ve) break;
+                    sc[((v >> 4) & 15) * T + tid] += 1;
+                }
+            }
+        }
         int lb = 0;
         for (; lb < 15; ++lb) {
             const uint32_t c = sc[lb * T + tid];
             if (acc + c >= rank) break;
             acc += c;
         }
-        const unsigned vs = vb + 16u * (unsigned)lb;
-        v2_count_runs<CNT, T>(sc, scol, c0, NCOL, n, r, vs, vs + 16, 0);
+        // bits 0..3 inside the 16-value sub-run [vs, vs+16)
+        const unsigned vs = vb + 16u * (unsigned)lb, vse = vs + 16;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) sc[q * T + tid] = 0;
+        for (int j = 0; j < n; ++j) {
+            const uint16_t *a = wcol + j * n;
+            for (int e = rpos[j * T + tid]; e < n; ++e) {
+                const unsigned v = a[e];
+                if (v >= vse) break;
+                if (v >= vs) sc[(v & 15) * T + tid] += 1;
+            }
+        }
         int lo = lb * 16;
         for (const int e = lo + 15; lo < e; ++lo) {
             const uint32_t c = sc[(lo & 15) * T + tid];

@@ -333,7 +333,8 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     } else if (!wide && force != "vert" && (force == "vert2" || wide_spread_u16(p, s))) {
         constexpr int T = 64;
         const int n16 = (int)n;
-        const size_t smem = (size_t)(16 + 256 + 16) * T * 2 + (size_t)(T + 2 * p.radius) * n16 * 2;
+        const size_t smem = (size_t)(16 + 256 + 16) * T * 2 + (size_t)(T + 2 * p.radius) * n16 * 2 +
+                            (size_t)n16 * T;
         if (smem <= 200 * 1024) {
             const int bx = (p.W + T - 1) / T;
             const int occ = (int)((227 * 1024) / (smem + 1024));
