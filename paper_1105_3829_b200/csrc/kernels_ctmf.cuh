@@ -333,13 +333,22 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
     // Y0+r)): its full 256-bin histogram and its cumulative coarse counts,
     // built once in a global workspace; every pass then initialises its
     // column histograms from it in O(columns) instead of rescanning n rows.
-    const size_t snap_stride = (size_t)g.NCP * (256 + 16);
-    uint8_t *snap_f = nullptr, *snap_c = nullptr;
+    // Layout per resident warp (reused for each of its tiles, so the live
+    // set stays L2-resident): cu[NCP] (16 B: count below 16*b, bytes),
+    // off[NCP] (u16), then a heap of 16-B fine chunks -- per column only
+    // the bins present in its span, ascending, starting at chunk off[c].
+    const size_t heap_off = ((size_t)g.NCP * 18 + 15) & ~(size_t)15;
+    const size_t snap_stride = heap_off + (size_t)g.NCP * 256;
+    uint4 *snap_cu = nullptr, *snap_heap = nullptr;
+    uint16_t *snap_off = nullptr;
     if (snap) {
-        const size_t tg = (size_t)blockIdx.z * tiles_x * tiles_y + tile;
-        snap_f = snap + tg * snap_stride;              // [NCP][256] fine counts
-        snap_c = snap_f + (size_t)g.NCP * 256;         // [NCP][16]  count below 16*b
+        const size_t slot = ((size_t)blockIdx.z * gridDim.x + blockIdx.x) * CT_WARPS + warp;
+        uint8_t *rec = snap + slot * snap_stride;
+        snap_cu = reinterpret_cast<uint4 *>(rec);
+        snap_off = reinterpret_cast<uint16_t *>(rec + (size_t)g.NCP * 16);
+        snap_heap = reinterpret_cast<uint4 *>(rec + heap_off);
         uint8_t *scr = reinterpret_cast<uint8_t *>(colA) + lane * 260;  // lane-private column
+        int heap_top = 0;
         for (int g0 = 0; g0 < g.NC; g0 += 32) {
             const int c = g0 + lane;
             const int gx = clampi(X0 - r + min(c, g.NC - 1), 0, W - 1);
@@ -356,18 +365,34 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
                 scr[v3] += 1;
             }
             for (; j <= r; ++j) scr[__ldg(src_row(p, src, clampi(Y0 + j, 0, H - 1)) + gx)] += 1;
+            const uint32_t *w = reinterpret_cast<const uint32_t *>(scr);
+            uint32_t acc = 0, pres = 0, cw[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                cw[q >> 2] |= acc << (8 * (q & 3));
+                const uint32_t cb = __vsadu4(w[4 * q], 0) + __vsadu4(w[4 * q + 1], 0) +
+                                    __vsadu4(w[4 * q + 2], 0) + __vsadu4(w[4 * q + 3], 0);
+                pres |= (cb ? 1u : 0u) << q;
+                acc += cb;
+            }
+            // warp exclusive scan of the chunk counts -> heap positions
+            const int K = c < g.NC ? __popc(pres) : 0;
+            int incl = K;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const int off = heap_top + incl - K;
+            heap_top += __shfl_sync(0xffffffffu, incl, 31);
             if (c < g.NC) {
-                uint4 *outf = reinterpret_cast<uint4 *>(snap_f + (size_t)c * 256);
-                uint32_t acc = 0, cw[4] = {0, 0, 0, 0};
-                for (int q = 0; q < 16; ++q) {
-                    const uint32_t *w4 = reinterpret_cast<const uint32_t *>(scr) + 4 * q;
-                    const uint4 chunk = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-                    outf[q] = chunk;
-                    cw[q >> 2] |= acc << (8 * (q & 3));
-                    acc += __vsadu4(chunk.x, 0) + __vsadu4(chunk.y, 0) + __vsadu4(chunk.z, 0) +
-                           __vsadu4(chunk.w, 0);
+                snap_cu[c] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+                snap_off[c] = (uint16_t)off;
+                int k = off;
+                for (uint32_t m = pres; m; m &= m - 1) {
+                    const int q = __ffs(m) - 1;
+                    snap_heap[k++] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
                 }
-                *reinterpret_cast<uint4 *>(snap_c + (size_t)c * 16) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
             }
         }
         __syncwarp();
@@ -417,19 +442,33 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
                 uint32_t cnt[4] = {0, 0, 0, 0};
                 uint32_t bl = 0;
                 if (c < g.NC) {
-                    const uint4 cu = __ldcg(reinterpret_cast<const uint4 *>(snap_c + (size_t)c * 16));
-                    if (!fine) {
-                        // coarse counts = next cumulative - cumulative (bytewise, no borrow)
-                        const uint32_t cwv[4] = {cu.x, cu.y, cu.z, cu.w};
-                        const uint32_t nxt[4] = {__funnelshift_r(cwv[0], cwv[1], 8), __funnelshift_r(cwv[1], cwv[2], 8),
-                                                 __funnelshift_r(cwv[2], cwv[3], 8), __funnelshift_r(cwv[3], nspan, 8)};
+                    const uint4 cu = __ldcg(snap_cu + c);
+                    // coarse counts = next cumulative - cumulative (bytewise, no borrow)
+                    const uint32_t cwv[4] = {cu.x, cu.y, cu.z, cu.w};
+                    const uint32_t nxt[4] = {__funnelshift_r(cwv[0], cwv[1], 8), __funnelshift_r(cwv[1], cwv[2], 8),
+                                             __funnelshift_r(cwv[2], cwv[3], 8), __funnelshift_r(cwv[3], nspan, 8)};
+                    uint32_t d[4];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) cnt[i] = nxt[i] - cwv[i];
+                    for (int i = 0; i < 4; ++i) d[i] = nxt[i] - cwv[i];
+                    if (!fine) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) cnt[i] = d[i];
                     } else {
-                        const uint4 f = __ldcg(reinterpret_cast<const uint4 *>(snap_f + (size_t)c * 256 + 16 * beta));
-                        cnt[0] = f.x; cnt[1] = f.y; cnt[2] = f.z; cnt[3] = f.w;
                         const uint32_t wsel = beta < 8 ? (beta < 4 ? cu.x : cu.y) : (beta < 12 ? cu.z : cu.w);
                         bl = (wsel >> (8 * (beta & 3))) & 0xffu;
+                        const uint32_t dsel = beta < 8 ? (beta < 4 ? d[0] : d[1]) : (beta < 12 ? d[2] : d[3]);
+                        if ((dsel >> (8 * (beta & 3))) & 0xffu) {
+                            // chunk index = off + number of present bins below beta
+                            int k = __ldcg(snap_off + c);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const int nb = min(max(beta - 4 * i, 0), 4);
+                                const uint32_t sel = nb >= 4 ? 0xffffffffu : ((1u << (8 * nb)) - 1u);
+                                k += __popc(__vcmpne4(d[i], 0) & sel) >> 3;
+                            }
+                            const uint4 f = __ldcg(snap_heap + k);
+                            cnt[0] = f.x; cnt[1] = f.y; cnt[2] = f.z; cnt[3] = f.w;
+                        }
                     }
                 }
                 const int sl = c < g.NC ? ct_slot<S>(c) : c;

@@ -193,7 +193,7 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     dim3 grid(ctas, 1, B);
     // per-tile column snapshots (stream-ordered pool allocation, kept cached)
     uint8_t *snap = nullptr;
-    const size_t snap_bytes = (size_t)tiles * B * g.NCP * (256 + 16);
+    const size_t snap_bytes = (size_t)ctas * CT_WARPS * B * ((((size_t)g.NCP * 18 + 15) & ~(size_t)15) + (size_t)g.NCP * 256);
     if (env_int("MTB_CT_SNAP", 1)) {
         keep_pool_memory();
         if (cudaMallocAsync(reinterpret_cast<void **>(&snap), snap_bytes, s) != cudaSuccess) {
