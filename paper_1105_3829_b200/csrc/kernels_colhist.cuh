@@ -1,0 +1,208 @@
+// kernels_colhist.cuh -- 8-bit rank filter from u8 column histograms with a
+// per-pixel window GATHER (one pass, no per-tile fine passes).
+//
+// The CTA owns output columns [X0, X0 + T*S) for rows [y0, y1) of a slab and
+// keeps, for every column of the halo'd stripe [X0-r, X0+T*S+r), the full
+// 256-bin histogram of the column's current vertical span (u8 counts: a
+// column holds n <= 255 pixels) plus its 16 coarse counts.  Moving down a row
+// is one decrement + one increment per column and level (the reference's
+// per-column trees, _kernels.py:115-165, with the sync step replaced by a
+// gather).
+//
+// Thread t outputs the S pixels x = X0 + t*S + s.  For the first it GATHERS
+// the window's coarse histogram from its 2r+1 columns: a column's 16 coarse
+// counts are one 16-B record (4 words of 4 u8 lanes) and up to
+// floor(255/n) records add with plain 32-bit adds without a carry crossing a
+// byte lane; each group is then widened into 8 packed u16 pairs.  A 4-step
+// binary descent (ct_descend) picks the coarse bin B and the residual rank;
+// the same gather over the columns' 16-B fine record of bin B gives the low
+// nibble.  Pixels s > 0 slide the coarse window by one column
+// (+C[x+r] - C[x-r-1]) and slide the fine window as well when their coarse
+// bin equals the previous pixel's (regather otherwise).
+//
+// Shared-memory layout (bank-conflict free gathers): records are stored as
+// [chunk][column position] with pos(c) = (c % S) * NCS + c / S, so the 32
+// threads of a warp, which read columns c = t*S + j for the same j, hit 32
+// consecutive 16-B records.  Chunks 0..15 are the fine records (bins
+// 16B..16B+15), chunk 16 the coarse record.
+#pragma once
+#include "common.cuh"
+#include "kernels_ctmf.cuh"  // ct_descend
+
+namespace mtb {
+
+struct ColhistGeom {
+    int TW, NC, NCS, NPOS;  // tile width, stripe columns, columns per phase, positions
+    int bytes;              // dynamic shared memory
+};
+
+__host__ __device__ inline ColhistGeom colhist_geom(int T, int S, int r) {
+    ColhistGeom g;
+    g.TW = T * S;
+    g.NC = g.TW + 2 * r;
+    g.NCS = (g.NC + S - 1) / S;
+    g.NPOS = g.NCS * S;
+    g.bytes = 17 * g.NPOS * 16;
+    return g;
+}
+
+template <int S>
+__device__ __forceinline__ int ch_pos(int c, int NCS) {
+    return (c % S) * NCS + c / S;
+}
+
+// widen 4 u8 lanes into two packed u16 pairs and add
+__device__ __forceinline__ void ch_widen_add(uint32_t (&w)[8], const uint4 &t) {
+    w[0] += __byte_perm(t.x, 0, 0x4140);
+    w[1] += __byte_perm(t.x, 0, 0x4342);
+    w[2] += __byte_perm(t.y, 0, 0x4140);
+    w[3] += __byte_perm(t.y, 0, 0x4342);
+    w[4] += __byte_perm(t.z, 0, 0x4140);
+    w[5] += __byte_perm(t.z, 0, 0x4342);
+    w[6] += __byte_perm(t.w, 0, 0x4140);
+    w[7] += __byte_perm(t.w, 0, 0x4342);
+}
+
+// w += widen(a) - widen(b): per-lane results stay >= 0, so no borrow crosses lanes
+__device__ __forceinline__ void ch_widen_slide(uint32_t (&w)[8], const uint4 &a, const uint4 &b) {
+    w[0] += __byte_perm(a.x, 0, 0x4140) - __byte_perm(b.x, 0, 0x4140);
+    w[1] += __byte_perm(a.x, 0, 0x4342) - __byte_perm(b.x, 0, 0x4342);
+    w[2] += __byte_perm(a.y, 0, 0x4140) - __byte_perm(b.y, 0, 0x4140);
+    w[3] += __byte_perm(a.y, 0, 0x4342) - __byte_perm(b.y, 0, 0x4342);
+    w[4] += __byte_perm(a.z, 0, 0x4140) - __byte_perm(b.z, 0, 0x4140);
+    w[5] += __byte_perm(a.z, 0, 0x4342) - __byte_perm(b.z, 0, 0x4342);
+    w[6] += __byte_perm(a.w, 0, 0x4140) - __byte_perm(b.w, 0, 0x4140);
+    w[7] += __byte_perm(a.w, 0, 0x4342) - __byte_perm(b.w, 0, 0x4342);
+}
+
+// window histogram (16 bins, packed u16 pairs) of chunk `chunk` over the
+// columns k0 .. k0+n-1, G columns per carry-free u8 group
+template <int S>
+__device__ __forceinline__ void ch_gather(const uint4 *rec, int chunk, int k0, int n, int G, int NCS,
+                                          uint32_t (&w)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = 0;
+    const uint4 *base = rec + chunk * (NCS * S);
+    int j = 0;
+    while (j < n) {
+        const int e = min(j + G, n);
+        uint4 t = make_uint4(0, 0, 0, 0);
+        for (; j + 4 <= e; j += 4) {
+            const uint4 a = base[ch_pos<S>(k0 + j, NCS)];
+            const uint4 b = base[ch_pos<S>(k0 + j + 1, NCS)];
+            const uint4 c = base[ch_pos<S>(k0 + j + 2, NCS)];
+            const uint4 d = base[ch_pos<S>(k0 + j + 3, NCS)];
+            t.x += (a.x + b.x) + (c.x + d.x);
+            t.y += (a.y + b.y) + (c.y + d.y);
+            t.z += (a.z + b.z) + (c.z + d.z);
+            t.w += (a.w + b.w) + (c.w + d.w);
+        }
+        for (; j < e; ++j) {
+            const uint4 a = base[ch_pos<S>(k0 + j, NCS)];
+            t.x += a.x;
+            t.y += a.y;
+            t.z += a.z;
+            t.w += a.w;
+        }
+        ch_widen_add(w, t);
+    }
+}
+
+template <int T, int S>
+__global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x;
+    const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
+    const ColhistGeom g = colhist_geom(T, S, r);
+    const int NCS = g.NCS, NPOS = g.NPOS;
+    uint4 *rec = reinterpret_cast<uint4 *>(smem_raw);       // [17][NPOS] 16-B records
+    uint8_t *recb = smem_raw;
+    const int X0 = blockIdx.x * g.TW;
+    const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
+    if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
+    const int y1 = min(y0 + p.rows_per_cta, p.row_end);
+    const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
+    uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
+    const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
+    const uint32_t rank = p.rank;
+    const int G = 255 / n;  // columns per carry-free u8 group (>= 1: n <= 255)
+
+    // ---- column histograms of rows clamp(y0-r .. y0+r)
+    for (int pos = tid; pos < 17 * NPOS; pos += T) rec[pos] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    for (int c = tid; c < g.NC; c += T) {
+        const int gx = clampi(X0 - r + c, 0, W - 1);
+        const int pc = ch_pos<S>(c, NCS);
+        for (int j = -r; j <= r; ++j) {
+            const unsigned v = __ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx);
+            recb[((v >> 4) * NPOS + pc) * 16 + (v & 15)] += 1;
+            recb[(16 * NPOS + pc) * 16 + (v >> 4)] += 1;
+        }
+    }
+    __syncthreads();
+
+    const int k0 = tid * S;  // stripe column of the first window's left edge
+    const int xt = X0 + k0;
+    for (int y = y0; y < y1; ++y) {
+        if (y > y0) {
+            const int yo = clampi(y - r - 1, 0, H - 1);
+            const int yi = clampi(y + r, 0, H - 1);
+            if (yo != yi) {
+                __syncthreads();  // previous row's gathers done
+                const uint8_t *ro = src_row(p, src, yo);
+                const uint8_t *ri = src_row(p, src, yi);
+                for (int c = tid; c < g.NC; c += T) {
+                    const int gx = clampi(X0 - r + c, 0, W - 1);
+                    const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
+                    if (vo == vi) continue;
+                    const int pc = ch_pos<S>(c, NCS);
+                    recb[((vo >> 4) * NPOS + pc) * 16 + (vo & 15)] -= 1;
+                    recb[((vi >> 4) * NPOS + pc) * 16 + (vi & 15)] += 1;
+                    recb[(16 * NPOS + pc) * 16 + (vo >> 4)] -= 1;
+                    recb[(16 * NPOS + pc) * 16 + (vi >> 4)] += 1;
+                }
+                __syncthreads();
+            }
+        }
+        uint32_t wc[8], wf[8];
+        int prevB = -1;
+        uint32_t outw = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (s == 0) {
+                ch_gather<S>(rec, 16, k0, n, G, NCS, wc);
+            } else {
+                ch_widen_slide(wc, rec[16 * NPOS + ch_pos<S>(k0 + s + 2 * r, NCS)],
+                               rec[16 * NPOS + ch_pos<S>(k0 + s - 1, NCS)]);
+            }
+            uint32_t k = rank;
+            const int B = ct_descend(wc, k);
+            if (B == prevB) {
+                ch_widen_slide(wf, rec[B * NPOS + ch_pos<S>(k0 + s + 2 * r, NCS)],
+                               rec[B * NPOS + ch_pos<S>(k0 + s - 1, NCS)]);
+            } else {
+                ch_gather<S>(rec, B, k0 + s, n, G, NCS, wf);
+                prevB = B;
+            }
+            const int lo = ct_descend(wf, k);
+            unsigned v = (unsigned)(B * 16 + lo);
+            if (lut) v = xt + s < W ? __ldg(lut + v) : 0u;
+            outw |= v << (8 * (s & 3));
+            if ((s & 3) == 3 || s == S - 1) {
+                // store the (up to) 4 bytes of this group
+                const int xs = xt + (s & ~3);
+                uint8_t *o = dst + (int64_t)(y - p.row_begin) * p.dst_pitch + xs;
+                const int cnt = (s & 3) + 1;
+                if (xs + cnt <= W && cnt == 4 && (reinterpret_cast<uintptr_t>(o) & 3) == 0) {
+                    *reinterpret_cast<uint32_t *>(o) = outw;
+                } else {
+                    for (int q = 0; q < cnt; ++q)
+                        if (xs + q < W) o[q] = (uint8_t)(outw >> (8 * q));
+                }
+                outw = 0;
+            }
+        }
+    }
+}
+
+}  // namespace mtb

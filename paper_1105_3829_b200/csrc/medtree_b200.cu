@@ -14,6 +14,7 @@
 #include "kernels_ctmf.cuh"
 #include "kernels_lob.cuh"
 #include "kernels_sortnet.cuh"
+#include "kernels_colhist.cuh"
 #include <cstdlib>
 
 namespace mtb {
@@ -210,6 +211,32 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     return MTB_OK;
 }
 
+template <int T, int S>
+static int run_colhist_u8_ts(SlabParams p, int B, cudaStream_t s, const char *name) {
+    const ColhistGeom g = colhist_geom(T, S, p.radius);
+    const size_t smem = (size_t)g.bytes;
+    auto kern = k_colhist_u8<T, S>;
+    if (int rc = set_smem(kern, smem)) return rc;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int bx = (p.W + g.TW - 1) / g.TW;
+    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm);
+    dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
+    return launch(kern, grid, T, smem, s, p, name);
+}
+
+static int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
+    switch (env_int("MTB_CH_VAR", 1)) {
+        case 0: return run_colhist_u8_ts<128, 1>(p, B, s, "k_colhist_u8<128,1>");
+        case 2: return run_colhist_u8_ts<128, 2>(p, B, s, "k_colhist_u8<128,2>");
+        case 3: return run_colhist_u8_ts<64, 4>(p, B, s, "k_colhist_u8<64,4>");
+        case 4: return run_colhist_u8_ts<32, 8>(p, B, s, "k_colhist_u8<32,8>");
+        case 5: return run_colhist_u8_ts<32, 4>(p, B, s, "k_colhist_u8<32,4>");
+        default: return run_colhist_u8_ts<64, 2>(p, B, s, "k_colhist_u8<64,2>");
+    }
+}
+
 static int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
     return env_int("MTB_CT_S", 8) == 8 ? run_ctmf_u8_s<8>(p, B, s) : run_ctmf_u8_s<16>(p, B, s);
 }
@@ -308,6 +335,7 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     //   otherwise               -> per-column vertical histograms (any r/rank)
     if ((force.empty() || force == "sortnet") && sortnet_applies<P>(p)) return run_sortnet<P>(p, B, s);
     if (sizeof(P) == 1 && p.radius <= 63 && force == "lob") return run_lob_u8_l<32>(p, B, s);
+    if (sizeof(P) == 1 && n <= 255 && force == "colhist") return run_colhist_u8(p, B, s);
     if (sizeof(P) == 1 && !wide &&
         (force == "ctmf" || (force.empty() && p.radius >= env_int("MTB_CT_MIN_R", 14))))
         return run_ctmf_u8(p, B, s);
