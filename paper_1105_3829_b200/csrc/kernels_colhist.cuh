@@ -11,9 +11,9 @@
 //
 // Thread t outputs the S pixels x = X0 + t*S + s.  For the first it GATHERS
 // the window's coarse histogram from its 2r+1 columns: a column's 16 coarse
-// counts are one 16-B record (4 words of 4 u8 lanes) and up to
-// floor(255/n) records add with plain 32-bit adds without a carry crossing a
-// byte lane; each group is then widened into 8 packed u16 pairs.  A 4-step
+// counts are one 16-B record (4 words of 4 u8 lanes) and G records with
+// G*n <= 255 add with plain 32-bit adds without a carry crossing a byte
+// lane; each group is then widened into 8 packed u16 pairs.  A 4-step
 // binary descent (ct_descend) picks the coarse bin B and the residual rank;
 // the same gather over the columns' 16-B fine record of bin B gives the low
 // nibble.  Pixels s > 0 slide the coarse window by one column
@@ -76,39 +76,46 @@ __device__ __forceinline__ void ch_widen_slide(uint32_t (&w)[8], const uint4 &a,
 }
 
 // window histogram (16 bins, packed u16 pairs) of chunk `chunk` over the
-// columns k0 .. k0+n-1, G columns per carry-free u8 group
-template <int S>
-__device__ __forceinline__ void ch_gather(const uint4 *rec, int chunk, int k0, int n, int G, int NCS,
+// columns k0 .. k0+n-1: groups of G records (G*n <= 255, so the u8 lanes of a
+// group sum never carry) added with IADD3, then widened into the u16 pairs.
+// Fully unrolled groups; the ragged tail is a predicated group.
+template <int S, int G>
+__device__ __forceinline__ void ch_gather(const uint4 *rec, int chunk, int k0, int n, int NCS,
                                           uint32_t (&w)[8]) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) w[i] = 0;
     const uint4 *base = rec + chunk * (NCS * S);
     int j = 0;
-    while (j < n) {
-        const int e = min(j + G, n);
+    for (; j + G <= n; j += G) {
         uint4 t = make_uint4(0, 0, 0, 0);
-        for (; j + 4 <= e; j += 4) {
-            const uint4 a = base[ch_pos<S>(k0 + j, NCS)];
-            const uint4 b = base[ch_pos<S>(k0 + j + 1, NCS)];
-            const uint4 c = base[ch_pos<S>(k0 + j + 2, NCS)];
-            const uint4 d = base[ch_pos<S>(k0 + j + 3, NCS)];
-            t.x += (a.x + b.x) + (c.x + d.x);
-            t.y += (a.y + b.y) + (c.y + d.y);
-            t.z += (a.z + b.z) + (c.z + d.z);
-            t.w += (a.w + b.w) + (c.w + d.w);
+#pragma unroll
+        for (int q = 0; q < G; q += 2) {
+            const uint4 a = base[ch_pos<S>(k0 + j + q, NCS)];
+            const uint4 b = base[ch_pos<S>(k0 + j + q + 1, NCS)];
+            t.x += a.x + b.x;
+            t.y += a.y + b.y;
+            t.z += a.z + b.z;
+            t.w += a.w + b.w;
         }
-        for (; j < e; ++j) {
-            const uint4 a = base[ch_pos<S>(k0 + j, NCS)];
-            t.x += a.x;
-            t.y += a.y;
-            t.z += a.z;
-            t.w += a.w;
+        ch_widen_add(w, t);
+    }
+    if (j < n) {
+        uint4 t = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int q = 0; q < G - 1; ++q) {
+            if (j + q < n) {
+                const uint4 a = base[ch_pos<S>(k0 + j + q, NCS)];
+                t.x += a.x;
+                t.y += a.y;
+                t.z += a.z;
+                t.w += a.w;
+            }
         }
         ch_widen_add(w, t);
     }
 }
 
-template <int T, int S>
+template <int T, int S, int G>
 __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
@@ -125,7 +132,6 @@ __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
     uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
     const uint32_t rank = p.rank;
-    const int G = 255 / n;  // columns per carry-free u8 group (>= 1: n <= 255)
 
     // ---- column histograms of rows clamp(y0-r .. y0+r)
     for (int pos = tid; pos < 17 * NPOS; pos += T) rec[pos] = make_uint4(0, 0, 0, 0);
@@ -170,7 +176,7 @@ __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             if (s == 0) {
-                ch_gather<S>(rec, 16, k0, n, G, NCS, wc);
+                ch_gather<S, G>(rec, 16, k0, n, NCS, wc);
             } else {
                 ch_widen_slide(wc, rec[16 * NPOS + ch_pos<S>(k0 + s + 2 * r, NCS)],
                                rec[16 * NPOS + ch_pos<S>(k0 + s - 1, NCS)]);
@@ -181,7 +187,7 @@ __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
                 ch_widen_slide(wf, rec[B * NPOS + ch_pos<S>(k0 + s + 2 * r, NCS)],
                                rec[B * NPOS + ch_pos<S>(k0 + s - 1, NCS)]);
             } else {
-                ch_gather<S>(rec, B, k0 + s, n, G, NCS, wf);
+                ch_gather<S, G>(rec, B, k0 + s, n, NCS, wf);
                 prevB = B;
             }
             const int lo = ct_descend(wf, k);

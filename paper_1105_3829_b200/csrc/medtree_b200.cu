@@ -211,11 +211,11 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     return MTB_OK;
 }
 
-template <int T, int S>
-static int run_colhist_u8_ts(SlabParams p, int B, cudaStream_t s, const char *name) {
+template <int T, int S, int G>
+static int run_colhist_u8_g(SlabParams p, int B, cudaStream_t s, const char *name) {
     const ColhistGeom g = colhist_geom(T, S, p.radius);
     const size_t smem = (size_t)g.bytes;
-    auto kern = k_colhist_u8<T, S>;
+    auto kern = k_colhist_u8<T, S, G>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
@@ -226,13 +226,21 @@ static int run_colhist_u8_ts(SlabParams p, int B, cudaStream_t s, const char *na
     return launch(kern, grid, T, smem, s, p, name);
 }
 
+// carry-free group size: G columns of counts <= n sum to <= 255 per u8 lane
+template <int T, int S>
+static int run_colhist_u8_ts(SlabParams p, int B, cudaStream_t s, const char *name) {
+    const int n = 2 * p.radius + 1;
+    if (8 * n <= 255) return run_colhist_u8_g<T, S, 8>(p, B, s, name);
+    if (4 * n <= 255) return run_colhist_u8_g<T, S, 4>(p, B, s, name);
+    return run_colhist_u8_g<T, S, 2>(p, B, s, name);
+}
+
 static int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
     switch (env_int("MTB_CH_VAR", 1)) {
         case 0: return run_colhist_u8_ts<128, 1>(p, B, s, "k_colhist_u8<128,1>");
         case 2: return run_colhist_u8_ts<128, 2>(p, B, s, "k_colhist_u8<128,2>");
-        case 3: return run_colhist_u8_ts<64, 4>(p, B, s, "k_colhist_u8<64,4>");
-        case 4: return run_colhist_u8_ts<32, 8>(p, B, s, "k_colhist_u8<32,8>");
-        case 5: return run_colhist_u8_ts<32, 4>(p, B, s, "k_colhist_u8<32,4>");
+        case 3: return run_colhist_u8_ts<256, 1>(p, B, s, "k_colhist_u8<256,1>");
+        case 4: return run_colhist_u8_ts<64, 1>(p, B, s, "k_colhist_u8<64,1>");
         default: return run_colhist_u8_ts<64, 2>(p, B, s, "k_colhist_u8<64,2>");
     }
 }
