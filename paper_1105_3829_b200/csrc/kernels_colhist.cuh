@@ -79,19 +79,19 @@ __device__ __forceinline__ void ch_widen_slide(uint32_t (&w)[8], const uint4 &a,
 // columns k0 .. k0+n-1: groups of G records (G*n <= 255, so the u8 lanes of a
 // group sum never carry) added with IADD3, then widened into the u16 pairs.
 // Fully unrolled groups; the ragged tail is a predicated group.
-template <int S, int G>
+template <int S, int G, int M>
 __device__ __forceinline__ void ch_gather(const uint4 *rec, int chunk, int k0, int n, int NCS,
                                           uint32_t (&w)[8]) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) w[i] = 0;
     const uint4 *base = rec + chunk * (NCS * S);
     int j = 0;
-    for (; j + G <= n; j += G) {
+    for (; j < n - M; j += G) {
         uint4 t = make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int q = 0; q < G; q += 2) {
             const uint4 a = base[ch_pos<S>(k0 + j + q, NCS)];
-            const uint4 b = base[ch_pos<S>(k0 + j + q + 1, NCS)];
+            const uint4 b = q + 1 < G ? base[ch_pos<S>(k0 + j + q + 1, NCS)] : make_uint4(0, 0, 0, 0);
             t.x += a.x + b.x;
             t.y += a.y + b.y;
             t.z += a.z + b.z;
@@ -99,23 +99,21 @@ __device__ __forceinline__ void ch_gather(const uint4 *rec, int chunk, int k0, i
         }
         ch_widen_add(w, t);
     }
-    if (j < n) {
+    if (M > 0) {
         uint4 t = make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int q = 0; q < G - 1; ++q) {
-            if (j + q < n) {
-                const uint4 a = base[ch_pos<S>(k0 + j + q, NCS)];
-                t.x += a.x;
-                t.y += a.y;
-                t.z += a.z;
-                t.w += a.w;
-            }
+        for (int q = 0; q < M; ++q) {
+            const uint4 a = base[ch_pos<S>(k0 + j + q, NCS)];
+            t.x += a.x;
+            t.y += a.y;
+            t.z += a.z;
+            t.w += a.w;
         }
         ch_widen_add(w, t);
     }
 }
 
-template <int T, int S, int G>
+template <int T, int S, int G, int M>
 __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
@@ -149,26 +147,50 @@ __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
 
     const int k0 = tid * S;  // stripe column of the first window's left edge
     const int xt = X0 + k0;
+    auto bump = [&](int c, unsigned vo, unsigned vi) {
+        const int pc = ch_pos<S>(c, NCS);
+        recb[((vo >> 4) * NPOS + pc) * 16 + (vo & 15)] -= 1;
+        recb[((vi >> 4) * NPOS + pc) * 16 + (vi & 15)] += 1;
+        recb[(16 * NPOS + pc) * 16 + (vo >> 4)] -= 1;
+        recb[(16 * NPOS + pc) * 16 + (vi >> 4)] += 1;
+    };
+    // the stripe columns this thread moves down each row; their leaving /
+    // entering pixels of the NEXT row are loaded a row ahead (latency hidden
+    // behind the gathers)
+    constexpr int CH_PF = 2;
+    int gxs[CH_PF];
+#pragma unroll
+    for (int u = 0; u < CH_PF; ++u) gxs[u] = clampi(X0 - r + min(tid + u * T, g.NC - 1), 0, W - 1);
+    unsigned pvo[CH_PF], pvi[CH_PF];
+    auto prefetch = [&](int yn) {
+        const uint8_t *ro = src_row(p, src, clampi(yn - r - 1, 0, H - 1));
+        const uint8_t *ri = src_row(p, src, clampi(yn + r, 0, H - 1));
+#pragma unroll
+        for (int u = 0; u < CH_PF; ++u) {
+            pvo[u] = __ldg(ro + gxs[u]);
+            pvi[u] = __ldg(ri + gxs[u]);
+        }
+    };
+    if (y0 + 1 < y1) prefetch(y0 + 1);
     for (int y = y0; y < y1; ++y) {
         if (y > y0) {
-            const int yo = clampi(y - r - 1, 0, H - 1);
-            const int yi = clampi(y + r, 0, H - 1);
-            if (yo != yi) {
-                __syncthreads();  // previous row's gathers done
-                const uint8_t *ro = src_row(p, src, yo);
-                const uint8_t *ri = src_row(p, src, yi);
-                for (int c = tid; c < g.NC; c += T) {
+            __syncthreads();  // previous row's gathers done
+#pragma unroll
+            for (int u = 0; u < CH_PF; ++u) {
+                const int c = tid + u * T;
+                if (c < g.NC && pvo[u] != pvi[u]) bump(c, pvo[u], pvi[u]);
+            }
+            if (g.NC > CH_PF * T) {  // narrow CTA, wide halo: the rest without prefetch
+                const uint8_t *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
+                const uint8_t *ri = src_row(p, src, clampi(y + r, 0, H - 1));
+                for (int c = tid + CH_PF * T; c < g.NC; c += T) {
                     const int gx = clampi(X0 - r + c, 0, W - 1);
                     const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
-                    if (vo == vi) continue;
-                    const int pc = ch_pos<S>(c, NCS);
-                    recb[((vo >> 4) * NPOS + pc) * 16 + (vo & 15)] -= 1;
-                    recb[((vi >> 4) * NPOS + pc) * 16 + (vi & 15)] += 1;
-                    recb[(16 * NPOS + pc) * 16 + (vo >> 4)] -= 1;
-                    recb[(16 * NPOS + pc) * 16 + (vi >> 4)] += 1;
+                    if (vo != vi) bump(c, vo, vi);
                 }
-                __syncthreads();
             }
+            if (y + 1 < y1) prefetch(y + 1);
+            __syncthreads();
         }
         uint32_t wc[8], wf[8];
         int prevB = -1;
@@ -176,7 +198,7 @@ __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             if (s == 0) {
-                ch_gather<S, G>(rec, 16, k0, n, NCS, wc);
+                ch_gather<S, G, M>(rec, 16, k0, n, NCS, wc);
             } else {
                 ch_widen_slide(wc, rec[16 * NPOS + ch_pos<S>(k0 + s + 2 * r, NCS)],
                                rec[16 * NPOS + ch_pos<S>(k0 + s - 1, NCS)]);
@@ -187,7 +209,7 @@ __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
                 ch_widen_slide(wf, rec[B * NPOS + ch_pos<S>(k0 + s + 2 * r, NCS)],
                                rec[B * NPOS + ch_pos<S>(k0 + s - 1, NCS)]);
             } else {
-                ch_gather<S, G>(rec, B, k0 + s, n, NCS, wf);
+                ch_gather<S, G, M>(rec, B, k0 + s, n, NCS, wf);
                 prevB = B;
             }
             const int lo = ct_descend(wf, k);
@@ -208,6 +230,152 @@ __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
                 outw = 0;
             }
         }
+    }
+}
+
+}  // namespace mtb
+
+namespace mtb {
+
+// ---------------------------------------------------------------------------
+// Radix-4 variant: four levels of 4 bins (base-4 digits of the value), every
+// column record one u32 of 4 u8 counts.  Per pixel the thread gathers 4 x n
+// words (16 B per window column instead of 32 B for the 16 x 16 split: the
+// 16-bin gathers above are bound by shared-memory bandwidth) and descends 2
+// steps per level.  Records per column: level 0 (1), level 1 (4, by the top
+// digit), level 2 (16, by the top two digits), level 3 (64) = 85 words.
+// Layout [record id][column]: thread t reads column t + j, so a warp's 32
+// loads are 32 consecutive words.
+constexpr int CH4_RECS = 85;
+
+__host__ __device__ inline int colhist4_bytes(int T, int r) { return CH4_RECS * (T + 2 * r) * 4; }
+
+// 4 bins (packed u16 pairs w0 = {b0, b1}, w1 = {b2, b3}): smallest digit d
+// with cumsum(bins[0..d]) >= k; leaves the rank within bin d in k
+__device__ __forceinline__ int ch4_descend(uint32_t w0, uint32_t w1, uint32_t &k) {
+    const uint32_t s = hsum16(w0);
+    const bool r1 = s < k;
+    k -= r1 ? s : 0u;
+    const uint32_t w = r1 ? w1 : w0;
+    const uint32_t s2 = w & 0xffffu;
+    const bool r2 = s2 < k;
+    k -= r2 ? s2 : 0u;
+    return (r1 ? 2 : 0) | (r2 ? 1 : 0);
+}
+
+// window counts of record row `rp` over columns k0 .. k0+n-1: full groups of
+// G words (carry-free), then the M = n mod G tail words (compile-time)
+template <int G, int M>
+__device__ __forceinline__ void ch4_gather(const uint32_t *rp, int n, uint32_t &w0, uint32_t &w1) {
+    w0 = 0;
+    w1 = 0;
+    const uint32_t *e = rp + (n - M);
+    for (; rp < e; rp += G) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int q = 0; q < G; q += 2) t += rp[q] + (q + 1 < G ? rp[q + 1] : 0u);
+        w0 += __byte_perm(t, 0, 0x4140);
+        w1 += __byte_perm(t, 0, 0x4342);
+    }
+    if (M > 0) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int q = 0; q < M; ++q) t += rp[q];
+        w0 += __byte_perm(t, 0, 0x4140);
+        w1 += __byte_perm(t, 0, 0x4342);
+    }
+}
+
+__device__ __forceinline__ void ch4_bump(uint8_t *recb, int NCOL, int c, unsigned v, int d) {
+    // record ids: 0 | 1 + (v>>6) | 5 + (v>>4) | 21 + (v>>2); byte = next digit
+    recb[(0 * NCOL + c) * 4 + (v >> 6)] += d;
+    recb[((1 + (v >> 6)) * NCOL + c) * 4 + ((v >> 4) & 3)] += d;
+    recb[((5 + (v >> 4)) * NCOL + c) * 4 + ((v >> 2) & 3)] += d;
+    recb[((21 + (v >> 2)) * NCOL + c) * 4 + (v & 3)] += d;
+}
+
+template <int T, int G, int M>
+__global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x;
+    const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
+    const int NCOL = T + 2 * r;
+    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCOL]
+    uint8_t *recb = smem_raw;
+    const int X0 = blockIdx.x * T;
+    const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
+    if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
+    const int y1 = min(y0 + p.rows_per_cta, p.row_end);
+    const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
+    uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
+    const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
+    const uint32_t rank = p.rank;
+
+    for (int i = tid; i < CH4_RECS * NCOL; i += T) rec[i] = 0;
+    __syncthreads();
+    for (int c = tid; c < NCOL; c += T) {
+        const int gx = clampi(X0 - r + c, 0, W - 1);
+        for (int j = -r; j <= r; ++j) ch4_bump(recb, NCOL, c, __ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx), 1);
+    }
+    __syncthreads();
+
+    const int x = X0 + tid;
+    // the (<= CH_PF) stripe columns this thread moves down each row, and their
+    // leaving / entering pixels for the NEXT row, loaded a row ahead so the
+    // global-load latency hides behind the gathers
+    constexpr int CH_PF = 2;
+    int gxs[CH_PF];
+#pragma unroll
+    for (int u = 0; u < CH_PF; ++u) gxs[u] = clampi(X0 - r + min(tid + u * T, NCOL - 1), 0, W - 1);
+    unsigned pvo[CH_PF], pvi[CH_PF];
+    auto prefetch = [&](int yn) {
+        const uint8_t *ro = src_row(p, src, clampi(yn - r - 1, 0, H - 1));
+        const uint8_t *ri = src_row(p, src, clampi(yn + r, 0, H - 1));
+#pragma unroll
+        for (int u = 0; u < CH_PF; ++u) {
+            pvo[u] = __ldg(ro + gxs[u]);
+            pvi[u] = __ldg(ri + gxs[u]);
+        }
+    };
+    if (y0 + 1 < y1) prefetch(y0 + 1);
+    for (int y = y0; y < y1; ++y) {
+        if (y > y0) {
+            __syncthreads();  // previous row's gathers done
+#pragma unroll
+            for (int u = 0; u < CH_PF; ++u) {
+                const int c = tid + u * T;
+                if (c < NCOL && pvo[u] != pvi[u]) {
+                    ch4_bump(recb, NCOL, c, pvo[u], -1);
+                    ch4_bump(recb, NCOL, c, pvi[u], 1);
+                }
+            }
+            if (NCOL > CH_PF * T) {  // narrow CTA, wide halo: the rest without prefetch
+                const uint8_t *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
+                const uint8_t *ri = src_row(p, src, clampi(y + r, 0, H - 1));
+                for (int c = tid + CH_PF * T; c < NCOL; c += T) {
+                    const int gx = clampi(X0 - r + c, 0, W - 1);
+                    const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
+                    if (vo == vi) continue;
+                    ch4_bump(recb, NCOL, c, vo, -1);
+                    ch4_bump(recb, NCOL, c, vi, 1);
+                }
+            }
+            if (y + 1 < y1) prefetch(y + 1);
+            __syncthreads();
+        }
+        uint32_t k = rank, w0, w1;
+        ch4_gather<G, M>(rec + tid, n, w0, w1);
+        const int d3 = ch4_descend(w0, w1, k);
+        ch4_gather<G, M>(rec + (1 + d3) * NCOL + tid, n, w0, w1);
+        const int d2 = ch4_descend(w0, w1, k);
+        const int p2 = d3 * 4 + d2;
+        ch4_gather<G, M>(rec + (5 + p2) * NCOL + tid, n, w0, w1);
+        const int d1 = ch4_descend(w0, w1, k);
+        const int p3 = p2 * 4 + d1;
+        ch4_gather<G, M>(rec + (21 + p3) * NCOL + tid, n, w0, w1);
+        const int d0 = ch4_descend(w0, w1, k);
+        unsigned v = (unsigned)(p3 * 4 + d0);
+        if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
     }
 }
 

@@ -211,11 +211,11 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     return MTB_OK;
 }
 
-template <int T, int S, int G>
-static int run_colhist_u8_g(SlabParams p, int B, cudaStream_t s, const char *name) {
+template <int T, int S, int G, int M>
+static int run_colhist_u8_gm(SlabParams p, int B, cudaStream_t s, const char *name) {
     const ColhistGeom g = colhist_geom(T, S, p.radius);
     const size_t smem = (size_t)g.bytes;
-    auto kern = k_colhist_u8<T, S, G>;
+    auto kern = k_colhist_u8<T, S, G, M>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
@@ -226,17 +226,73 @@ static int run_colhist_u8_g(SlabParams p, int B, cudaStream_t s, const char *nam
     return launch(kern, grid, T, smem, s, p, name);
 }
 
+template <int T, int S, int G>
+static int run_colhist_u8_g(SlabParams p, int B, cudaStream_t s, const char *name) {
+    switch ((2 * p.radius + 1) % G) {
+        case 0: return run_colhist_u8_gm<T, S, G, 0>(p, B, s, name);
+        case 1: return run_colhist_u8_gm<T, S, G, (G > 1 ? 1 : 0)>(p, B, s, name);
+        case 2: return run_colhist_u8_gm<T, S, G, (G > 2 ? 2 : 0)>(p, B, s, name);
+        case 3: return run_colhist_u8_gm<T, S, G, (G > 3 ? 3 : 0)>(p, B, s, name);
+        case 4: return run_colhist_u8_gm<T, S, G, (G > 4 ? 4 : 0)>(p, B, s, name);
+        case 5: return run_colhist_u8_gm<T, S, G, (G > 5 ? 5 : 0)>(p, B, s, name);
+        case 6: return run_colhist_u8_gm<T, S, G, (G > 6 ? 6 : 0)>(p, B, s, name);
+        default: return run_colhist_u8_gm<T, S, G, (G > 7 ? 7 : 0)>(p, B, s, name);
+    }
+}
+
 // carry-free group size: G columns of counts <= n sum to <= 255 per u8 lane
 template <int T, int S>
 static int run_colhist_u8_ts(SlabParams p, int B, cudaStream_t s, const char *name) {
     const int n = 2 * p.radius + 1;
     if (8 * n <= 255) return run_colhist_u8_g<T, S, 8>(p, B, s, name);
     if (4 * n <= 255) return run_colhist_u8_g<T, S, 4>(p, B, s, name);
-    return run_colhist_u8_g<T, S, 2>(p, B, s, name);
+    if (2 * n <= 255) return run_colhist_u8_g<T, S, 2>(p, B, s, name);
+    return run_colhist_u8_g<T, S, 1>(p, B, s, name);
+}
+
+template <int T, int G, int M>
+static int run_colhist4_u8_gm(SlabParams p, int B, cudaStream_t s, const char *name) {
+    const size_t smem = (size_t)colhist4_bytes(T, p.radius);
+    auto kern = k_colhist4_u8<T, G, M>;
+    if (int rc = set_smem(kern, smem)) return rc;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int bx = (p.W + T - 1) / T;
+    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm);
+    dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
+    return launch(kern, grid, T, smem, s, p, name);
+}
+
+template <int T, int G>
+static int run_colhist4_u8_g(SlabParams p, int B, cudaStream_t s, const char *name) {
+    switch ((2 * p.radius + 1) % G) {
+        case 0: return run_colhist4_u8_gm<T, G, 0>(p, B, s, name);
+        case 1: return run_colhist4_u8_gm<T, G, (G > 1 ? 1 : 0)>(p, B, s, name);
+        case 2: return run_colhist4_u8_gm<T, G, (G > 2 ? 2 : 0)>(p, B, s, name);
+        case 3: return run_colhist4_u8_gm<T, G, (G > 3 ? 3 : 0)>(p, B, s, name);
+        case 4: return run_colhist4_u8_gm<T, G, (G > 4 ? 4 : 0)>(p, B, s, name);
+        case 5: return run_colhist4_u8_gm<T, G, (G > 5 ? 5 : 0)>(p, B, s, name);
+        case 6: return run_colhist4_u8_gm<T, G, (G > 6 ? 6 : 0)>(p, B, s, name);
+        default: return run_colhist4_u8_gm<T, G, (G > 7 ? 7 : 0)>(p, B, s, name);
+    }
+}
+
+template <int T>
+static int run_colhist4_u8(SlabParams p, int B, cudaStream_t s, const char *name) {
+    const int n = 2 * p.radius + 1;
+    if (8 * n <= 255) return run_colhist4_u8_g<T, 8>(p, B, s, name);
+    if (4 * n <= 255) return run_colhist4_u8_g<T, 4>(p, B, s, name);
+    if (2 * n <= 255) return run_colhist4_u8_g<T, 2>(p, B, s, name);
+    return run_colhist4_u8_g<T, 1>(p, B, s, name);
 }
 
 static int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
     switch (env_int("MTB_CH_VAR", 1)) {
+        case 10: return run_colhist4_u8<64>(p, B, s, "k_colhist4_u8<64>");
+        case 11: return run_colhist4_u8<128>(p, B, s, "k_colhist4_u8<128>");
+        case 12: return run_colhist4_u8<256>(p, B, s, "k_colhist4_u8<256>");
+        case 13: return run_colhist4_u8<32>(p, B, s, "k_colhist4_u8<32>");
         case 0: return run_colhist_u8_ts<128, 1>(p, B, s, "k_colhist_u8<128,1>");
         case 2: return run_colhist_u8_ts<128, 2>(p, B, s, "k_colhist_u8<128,2>");
         case 3: return run_colhist_u8_ts<256, 1>(p, B, s, "k_colhist_u8<256,1>");
