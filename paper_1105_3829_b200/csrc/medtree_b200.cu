@@ -226,17 +226,15 @@ static int run_colhist_u8_gm(SlabParams p, int B, cudaStream_t s, const char *na
     return launch(kern, grid, T, smem, s, p, name);
 }
 
+// n is odd, so the tail n mod G is odd for G > 1 and 0 for G = 1
 template <int T, int S, int G>
 static int run_colhist_u8_g(SlabParams p, int B, cudaStream_t s, const char *name) {
     switch ((2 * p.radius + 1) % G) {
-        case 0: return run_colhist_u8_gm<T, S, G, 0>(p, B, s, name);
         case 1: return run_colhist_u8_gm<T, S, G, (G > 1 ? 1 : 0)>(p, B, s, name);
-        case 2: return run_colhist_u8_gm<T, S, G, (G > 2 ? 2 : 0)>(p, B, s, name);
         case 3: return run_colhist_u8_gm<T, S, G, (G > 3 ? 3 : 0)>(p, B, s, name);
-        case 4: return run_colhist_u8_gm<T, S, G, (G > 4 ? 4 : 0)>(p, B, s, name);
         case 5: return run_colhist_u8_gm<T, S, G, (G > 5 ? 5 : 0)>(p, B, s, name);
-        case 6: return run_colhist_u8_gm<T, S, G, (G > 6 ? 6 : 0)>(p, B, s, name);
-        default: return run_colhist_u8_gm<T, S, G, (G > 7 ? 7 : 0)>(p, B, s, name);
+        case 7: return run_colhist_u8_gm<T, S, G, (G > 7 ? 7 : 0)>(p, B, s, name);
+        default: return run_colhist_u8_gm<T, S, G, 0>(p, B, s, name);
     }
 }
 
@@ -267,14 +265,11 @@ static int run_colhist4_u8_gm(SlabParams p, int B, cudaStream_t s, const char *n
 template <int T, int G>
 static int run_colhist4_u8_g(SlabParams p, int B, cudaStream_t s, const char *name) {
     switch ((2 * p.radius + 1) % G) {
-        case 0: return run_colhist4_u8_gm<T, G, 0>(p, B, s, name);
         case 1: return run_colhist4_u8_gm<T, G, (G > 1 ? 1 : 0)>(p, B, s, name);
-        case 2: return run_colhist4_u8_gm<T, G, (G > 2 ? 2 : 0)>(p, B, s, name);
         case 3: return run_colhist4_u8_gm<T, G, (G > 3 ? 3 : 0)>(p, B, s, name);
-        case 4: return run_colhist4_u8_gm<T, G, (G > 4 ? 4 : 0)>(p, B, s, name);
         case 5: return run_colhist4_u8_gm<T, G, (G > 5 ? 5 : 0)>(p, B, s, name);
-        case 6: return run_colhist4_u8_gm<T, G, (G > 6 ? 6 : 0)>(p, B, s, name);
-        default: return run_colhist4_u8_gm<T, G, (G > 7 ? 7 : 0)>(p, B, s, name);
+        case 7: return run_colhist4_u8_gm<T, G, (G > 7 ? 7 : 0)>(p, B, s, name);
+        default: return run_colhist4_u8_gm<T, G, 0>(p, B, s, name);
     }
 }
 
@@ -287,17 +282,16 @@ static int run_colhist4_u8(SlabParams p, int B, cudaStream_t s, const char *name
     return run_colhist4_u8_g<T, 1>(p, B, s, name);
 }
 
+// 8-bit column-histogram gather kernels; the variant by radius (tools/probe.py
+// sweep on config 2): 16-bin records, one pixel per thread for
+// r <= 5, two for r <= 13; radix-4 records above.  MTB_CH_VAR forces one.
 static int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
-    switch (env_int("MTB_CH_VAR", 1)) {
-        case 10: return run_colhist4_u8<64>(p, B, s, "k_colhist4_u8<64>");
-        case 11: return run_colhist4_u8<128>(p, B, s, "k_colhist4_u8<128>");
-        case 12: return run_colhist4_u8<256>(p, B, s, "k_colhist4_u8<256>");
-        case 13: return run_colhist4_u8<32>(p, B, s, "k_colhist4_u8<32>");
+    int var = env_int("MTB_CH_VAR", -1);
+    if (var < 0) var = p.radius <= 5 ? 0 : (p.radius <= 13 ? 2 : 12);
+    switch (var) {
         case 0: return run_colhist_u8_ts<128, 1>(p, B, s, "k_colhist_u8<128,1>");
         case 2: return run_colhist_u8_ts<128, 2>(p, B, s, "k_colhist_u8<128,2>");
-        case 3: return run_colhist_u8_ts<256, 1>(p, B, s, "k_colhist_u8<256,1>");
-        case 4: return run_colhist_u8_ts<64, 1>(p, B, s, "k_colhist_u8<64,1>");
-        default: return run_colhist_u8_ts<64, 2>(p, B, s, "k_colhist_u8<64,2>");
+        default: return run_colhist4_u8<256>(p, B, s, "k_colhist4_u8<256>");
     }
 }
 
@@ -394,15 +388,18 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     const bool wide = n * n > 65535;
     const std::string force = forced_kernel();
     // Kernel choice (measured on B200, tools/probe.py):
-    //   median, n <= 7          -> selection networks (any bit depth)
-    //   8-bit, 14 <= r <= 127   -> column-histogram CTMF (O(1) in r)
-    //   otherwise               -> per-column vertical histograms (any r/rank)
-    if ((force.empty() || force == "sortnet") && sortnet_applies<P>(p)) return run_sortnet<P>(p, B, s);
+    //   median, n <= 5 (8-bit), n <= 7 (16-bit)  -> selection networks
+    //   8-bit, r <= 40 (any rank)                 -> column-histogram gather
+    //   8-bit, 41 <= r <= 127                     -> CTMF tiles (O(1) in r)
+    //   otherwise                                 -> per-column vertical histograms
+    if ((force.empty() || force == "sortnet") && sortnet_applies<P>(p) &&
+        (sizeof(P) == 2 || p.radius <= 2 || force == "sortnet"))
+        return run_sortnet<P>(p, B, s);
     if (sizeof(P) == 1 && p.radius <= 63 && force == "lob") return run_lob_u8_l<32>(p, B, s);
-    if (sizeof(P) == 1 && n <= 255 && force == "colhist") return run_colhist_u8(p, B, s);
-    if (sizeof(P) == 1 && !wide &&
-        (force == "ctmf" || (force.empty() && p.radius >= env_int("MTB_CT_MIN_R", 14))))
-        return run_ctmf_u8(p, B, s);
+    if (sizeof(P) == 1 && n <= 255 &&
+        (force == "colhist" || (force.empty() && p.radius <= env_int("MTB_CH_MAX_R", 40))))
+        return run_colhist_u8(p, B, s);
+    if (sizeof(P) == 1 && !wide && (force == "ctmf" || force.empty())) return run_ctmf_u8(p, B, s);
     if (sizeof(P) == 1 && !wide && force != "vert" && (n * n <= 255 || force == "vert2")) {
         constexpr int T = 128;
         const int bx = (p.W + T - 1) / T;

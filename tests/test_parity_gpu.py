@@ -275,7 +275,7 @@ def _cfg4():
 _FAMILY_CASES = [c for c in G.small_cases() if c[0]["rank"] is None and c[0]["percentile"] is None]
 
 
-@pytest.mark.parametrize("family", ["vert", "vert2", "ctmf", "lob", "sortnet"])
+@pytest.mark.parametrize("family", ["vert", "vert2", "ctmf", "lob", "sortnet", "colhist"])
 def test_each_kernel_family_is_exact(family, monkeypatch):
     """MTB_KERNEL forces one family; families that do not apply to a case
     (ctmf/lob: 8-bit only; sortnet: median of n <= 7) fall through to the
@@ -299,7 +299,7 @@ def test_each_kernel_family_is_exact(family, monkeypatch):
         out16 = mtb.rank_filter(torch.from_numpy(px16).cuda(), min(r, 34)).cpu().numpy()
         assert np.array_equal(out16, O.iot_filter(px16, 2 * min(r, 34) + 1)), (family, r)
     expect = {"vert": "k_vert_u8", "vert2": "k_vert2_u16", "ctmf": "k_ctmf_u8", "lob": "k_lob_u8",
-              "sortnet": "k_sortnet"}[family]
+              "sortnet": "k_sortnet", "colhist": "k_colhist_u8"}[family]
     assert expect in seen, seen
 
 
@@ -322,3 +322,24 @@ def test_vert2_u16_ranks_and_counter_widths(r, monkeypatch):
             expect = "k_vert_u16" if r == 130 else "k_vert2_u16"
             assert _lib.last_kernel().startswith(expect), _lib.last_kernel()
             assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (r, rank)
+
+
+@pytest.mark.parametrize("var,name", [(0, "k_colhist_u8<128,1>"), (2, "k_colhist_u8<128,2>"),
+                                      (12, "k_colhist4_u8<256>")])
+def test_colhist_variants_all_group_tails(var, name, monkeypatch):
+    """Each column-histogram variant at radii covering every carry-free group
+    size G (8/4/2/1) and tail n mod G, ragged tiles (W not a multiple of the
+    tile) and min / max / off-centre ranks."""
+    from paper_1105_3829_b200 import _lib
+
+    monkeypatch.setenv("MTB_KERNEL", "colhist")
+    monkeypatch.setenv("MTB_CH_VAR", str(var))
+    rng = np.random.default_rng(90 + var)
+    px = workloads.cfg2_blur_sp_u8(160, 601, seed=90 + var)
+    noise = rng.integers(0, 256, px.shape).astype(np.uint8)
+    for r in (1, 2, 3, 4, 5, 6, 7, 8, 11, 13, 15, 16, 20, 31, 32, 45, 63, 64, 100, 127):
+        n = 2 * r + 1
+        for img, rank in ((px, None), (noise, 1), (noise, n * n), (px, (n * n) // 5 + 1)):
+            out = mtb.rank_filter(torch.from_numpy(img).cuda(), r, rank=rank).cpu().numpy()
+            assert _lib.last_kernel() == name, _lib.last_kernel()
+            assert np.array_equal(out, O.iot_filter(img, n, rank=rank)), (var, r, rank)
