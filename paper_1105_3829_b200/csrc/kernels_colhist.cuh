@@ -294,14 +294,99 @@ __device__ __forceinline__ void ch4_bump(uint8_t *recb, int NCOL, int c, unsigne
     recb[((21 + (v >> 2)) * NCOL + c) * 4 + (v & 3)] += d;
 }
 
+// the 4-level selection of the rank-k element (k updated to the rank within
+// the selected value) from the records of the window starting at rp (= record
+// row 0, thread column applied)
+template <int G, int M>
+__device__ __forceinline__ unsigned ch4_select(const uint32_t *rp, int NCOL, int n, uint32_t &k) {
+    uint32_t w0, w1;
+    ch4_gather<G, M>(rp, n, w0, w1);
+    const int d3 = ch4_descend(w0, w1, k);
+    ch4_gather<G, M>(rp + (1 + d3) * NCOL, n, w0, w1);
+    const int d2 = ch4_descend(w0, w1, k);
+    const int p2 = d3 * 4 + d2;
+    ch4_gather<G, M>(rp + (5 + p2) * NCOL, n, w0, w1);
+    const int d1 = ch4_descend(w0, w1, k);
+    const int p3 = p2 * 4 + d1;
+    ch4_gather<G, M>(rp + (21 + p3) * NCOL, n, w0, w1);
+    const int d0 = ch4_descend(w0, w1, k);
+    return (unsigned)(p3 * 4 + d0);
+}
+
+// One downward sweep of a CTA stripe over rows [ya, yb]: the column records
+// are built for row ya from the (clamped) spans, then moved down a row at a
+// time; `key(v)` maps a pixel to its 8-bit record key (or -1: not counted),
+// `pixel(y)` runs after each row's records are final.  Next-row pixels are
+// prefetched a row ahead so their latency hides behind the gathers.
+template <int T, typename P, typename Key, typename Pixel>
+__device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uint32_t *rec, int NCOL, int X0,
+                                          int ya, int yb, Key key, Pixel pixel) {
+    const int tid = threadIdx.x;
+    const int r = p.radius, H = p.H, W = p.W;
+    uint8_t *recb = reinterpret_cast<uint8_t *>(rec);
+    auto bump2 = [&](int c, unsigned vo, unsigned vi) {
+        const int ko = key(vo), ki = key(vi);
+        if (ko == ki) return;
+        if (ko >= 0) ch4_bump(recb, NCOL, c, (unsigned)ko, -1);
+        if (ki >= 0) ch4_bump(recb, NCOL, c, (unsigned)ki, 1);
+    };
+    __syncthreads();  // previous users of rec are done
+    for (int i = tid; i < CH4_RECS * NCOL; i += T) rec[i] = 0;
+    __syncthreads();
+    for (int c = tid; c < NCOL; c += T) {
+        const int gx = clampi(X0 - r + c, 0, W - 1);
+        for (int j = -r; j <= r; ++j) {
+            const int kv = key(src_row(p, src, clampi(ya + j, 0, H - 1))[gx]);
+            if (kv >= 0) ch4_bump(recb, NCOL, c, (unsigned)kv, 1);
+        }
+    }
+    __syncthreads();
+    constexpr int CH_PF = 2;
+    int gxs[CH_PF];
+#pragma unroll
+    for (int u = 0; u < CH_PF; ++u) gxs[u] = clampi(X0 - r + min(tid + u * T, NCOL - 1), 0, W - 1);
+    unsigned pvo[CH_PF], pvi[CH_PF];
+    auto prefetch = [&](int yn) {
+        const P *ro = src_row(p, src, clampi(yn - r - 1, 0, H - 1));
+        const P *ri = src_row(p, src, clampi(yn + r, 0, H - 1));
+#pragma unroll
+        for (int u = 0; u < CH_PF; ++u) {
+            pvo[u] = __ldg(ro + gxs[u]);
+            pvi[u] = __ldg(ri + gxs[u]);
+        }
+    };
+    if (ya < yb) prefetch(ya + 1);
+    for (int y = ya; y <= yb; ++y) {
+        if (y > ya) {
+            __syncthreads();  // previous row's gathers done
+#pragma unroll
+            for (int u = 0; u < CH_PF; ++u) {
+                const int c = tid + u * T;
+                if (c < NCOL && pvo[u] != pvi[u]) bump2(c, pvo[u], pvi[u]);
+            }
+            if (NCOL > CH_PF * T) {  // narrow CTA, wide halo: the rest without prefetch
+                const P *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
+                const P *ri = src_row(p, src, clampi(y + r, 0, H - 1));
+                for (int c = tid + CH_PF * T; c < NCOL; c += T) {
+                    const int gx = clampi(X0 - r + c, 0, W - 1);
+                    const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
+                    if (vo != vi) bump2(c, vo, vi);
+                }
+            }
+            if (y < yb) prefetch(y + 1);
+            __syncthreads();
+        }
+        pixel(y);
+    }
+}
+
 template <int T, int G, int M>
 __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
-    const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
+    const int r = p.radius, W = p.W, n = 2 * r + 1;
     const int NCOL = T + 2 * r;
     uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCOL]
-    uint8_t *recb = smem_raw;
     const int X0 = blockIdx.x * T;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
     if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
@@ -309,73 +394,84 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
     const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
     uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
-    const uint32_t rank = p.rank;
-
-    for (int i = tid; i < CH4_RECS * NCOL; i += T) rec[i] = 0;
-    __syncthreads();
-    for (int c = tid; c < NCOL; c += T) {
-        const int gx = clampi(X0 - r + c, 0, W - 1);
-        for (int j = -r; j <= r; ++j) ch4_bump(recb, NCOL, c, __ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx), 1);
-    }
-    __syncthreads();
-
     const int x = X0 + tid;
-    // the (<= CH_PF) stripe columns this thread moves down each row, and their
-    // leaving / entering pixels for the NEXT row, loaded a row ahead so the
-    // global-load latency hides behind the gathers
-    constexpr int CH_PF = 2;
-    int gxs[CH_PF];
-#pragma unroll
-    for (int u = 0; u < CH_PF; ++u) gxs[u] = clampi(X0 - r + min(tid + u * T, NCOL - 1), 0, W - 1);
-    unsigned pvo[CH_PF], pvi[CH_PF];
-    auto prefetch = [&](int yn) {
-        const uint8_t *ro = src_row(p, src, clampi(yn - r - 1, 0, H - 1));
-        const uint8_t *ri = src_row(p, src, clampi(yn + r, 0, H - 1));
-#pragma unroll
-        for (int u = 0; u < CH_PF; ++u) {
-            pvo[u] = __ldg(ro + gxs[u]);
-            pvi[u] = __ldg(ri + gxs[u]);
-        }
-    };
-    if (y0 + 1 < y1) prefetch(y0 + 1);
-    for (int y = y0; y < y1; ++y) {
-        if (y > y0) {
-            __syncthreads();  // previous row's gathers done
-#pragma unroll
-            for (int u = 0; u < CH_PF; ++u) {
-                const int c = tid + u * T;
-                if (c < NCOL && pvo[u] != pvi[u]) {
-                    ch4_bump(recb, NCOL, c, pvo[u], -1);
-                    ch4_bump(recb, NCOL, c, pvi[u], 1);
-                }
+    ch4_sweep<T, uint8_t>(
+        p, src, rec, NCOL, X0, y0, y1 - 1, [](unsigned v) { return (int)v; },
+        [&](int y) {
+            uint32_t k = p.rank;
+            const unsigned v = ch4_select<G, M>(rec + tid, NCOL, n, k);
+            if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
+        });
+}
+
+// ---------------------------------------------------------------------------
+// 16-bit images whose median high bytes are locally few (compact data, e.g.
+// config 4): two phases over the CTA's tile, each a ch4_sweep.
+//   A: records keyed by the high byte -> every pixel's high byte H and its
+//      rank k within H (H to a u8 scratch plane, k to dst); the set of H
+//      values used by the tile and their first / last row are collected.
+//   B: once per H used (ascending): records keyed by the low byte of the
+//      pixels whose high byte is H, swept over that H's row range; pixels
+//      with this H select their low byte with rank k.
+// Exact for any image; the cost grows with the number of distinct H per
+// tile, so the host only picks it when the sampled high-byte spread is small.
+template <int T, int G, int M>
+__global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__restrict__ hplane) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x;
+    const int r = p.radius, W = p.W, n = 2 * r + 1;
+    const int NCOL = T + 2 * r;
+    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCOL]
+    int *hfirst = reinterpret_cast<int *>(rec + CH4_RECS * NCOL);  // [256]
+    int *hlast = hfirst + 256;                                      // [256]
+    const int X0 = blockIdx.x * T;
+    const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
+    if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
+    const int y1 = min(y0 + p.rows_per_cta, p.row_end);
+    const uint16_t *src = static_cast<const uint16_t *>(p.src) + blockIdx.z * p.src_img_stride;
+    uint16_t *dst = static_cast<uint16_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
+    const uint16_t *lut = static_cast<const uint16_t *>(p.lut);
+    const int64_t hp_img = (int64_t)(p.row_end - p.row_begin) * p.W;
+    uint8_t *hpl = hplane + blockIdx.z * hp_img;
+    const int x = X0 + tid;
+    for (int i = tid; i < 256; i += T) {
+        hfirst[i] = 1 << 30;
+        hlast[i] = -1;
+    }
+    // phase A: high byte and rank within it
+    ch4_sweep<T, uint16_t>(
+        p, src, rec, NCOL, X0, y0, y1 - 1, [](unsigned v) { return (int)(v >> 8); },
+        [&](int y) {
+            uint32_t k = p.rank;
+            const unsigned hb = ch4_select<G, M>(rec + tid, NCOL, n, k);
+            if (x < W) {
+                const int64_t o = (int64_t)(y - p.row_begin) * W + x;
+                hpl[o] = (uint8_t)hb;
+                dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = (uint16_t)k;
+                // rows ascend and every writer of a row stores the same y:
+                // plain stores (no atomics) are race-free in effect
+                if (hfirst[hb] > y) hfirst[hb] = y;
+                hlast[hb] = y;
             }
-            if (NCOL > CH_PF * T) {  // narrow CTA, wide halo: the rest without prefetch
-                const uint8_t *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
-                const uint8_t *ri = src_row(p, src, clampi(y + r, 0, H - 1));
-                for (int c = tid + CH_PF * T; c < NCOL; c += T) {
-                    const int gx = clampi(X0 - r + c, 0, W - 1);
-                    const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
-                    if (vo == vi) continue;
-                    ch4_bump(recb, NCOL, c, vo, -1);
-                    ch4_bump(recb, NCOL, c, vi, 1);
-                }
-            }
-            if (y + 1 < y1) prefetch(y + 1);
-            __syncthreads();
-        }
-        uint32_t k = rank, w0, w1;
-        ch4_gather<G, M>(rec + tid, n, w0, w1);
-        const int d3 = ch4_descend(w0, w1, k);
-        ch4_gather<G, M>(rec + (1 + d3) * NCOL + tid, n, w0, w1);
-        const int d2 = ch4_descend(w0, w1, k);
-        const int p2 = d3 * 4 + d2;
-        ch4_gather<G, M>(rec + (5 + p2) * NCOL + tid, n, w0, w1);
-        const int d1 = ch4_descend(w0, w1, k);
-        const int p3 = p2 * 4 + d1;
-        ch4_gather<G, M>(rec + (21 + p3) * NCOL + tid, n, w0, w1);
-        const int d0 = ch4_descend(w0, w1, k);
-        unsigned v = (unsigned)(p3 * 4 + d0);
-        if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
+        });
+    __syncthreads();
+    // phase B: one sweep per high byte used by the tile
+    for (int hb = 0; hb < 256; ++hb) {
+        const int ya = hfirst[hb], yb = hlast[hb];  // CTA-uniform
+        if (yb < 0) continue;
+        ch4_sweep<T, uint16_t>(
+            p, src, rec, NCOL, X0, ya, yb,
+            [hb](unsigned v) { return (int)(v >> 8) == hb ? (int)(v & 255) : -1; },
+            [&](int y) {
+                if (x >= W) return;
+                const int64_t o = (int64_t)(y - p.row_begin) * W + x;
+                if (hpl[o] != hb) return;
+                uint16_t *d = dst + (int64_t)(y - p.row_begin) * p.dst_pitch + x;
+                uint32_t k = *d;
+                const unsigned lo = ch4_select<G, M>(rec + tid, NCOL, n, k);
+                const unsigned v = ((unsigned)hb << 8) | lo;
+                *d = lut ? __ldg(lut + v) : (uint16_t)v;
+            });
     }
 }
 

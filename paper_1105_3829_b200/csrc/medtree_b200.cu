@@ -282,6 +282,52 @@ static int run_colhist4_u8(SlabParams p, int B, cudaStream_t s, const char *name
     return run_colhist4_u8_g<T, 1>(p, B, s, name);
 }
 
+template <int T, int G, int M>
+static int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s) {
+    const size_t smem = (size_t)colhist4_bytes(T, p.radius) + 2 * 256 * sizeof(int);
+    auto kern = k_colhist16_u16<T, G, M>;
+    if (int rc = set_smem(kern, smem)) return rc;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int bx = (p.W + T - 1) / T;
+    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm);
+    dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
+    // per-pixel high-byte plane (stream-ordered pool allocation, kept cached)
+    uint8_t *hplane = nullptr;
+    keep_pool_memory();
+    const size_t hbytes = (size_t)(p.row_end - p.row_begin) * p.W * B;
+    if (cudaMallocAsync(reinterpret_cast<void **>(&hplane), hbytes, s) != cudaSuccess)
+        return fail(MTB_E_CUDA, "k_colhist16_u16: scratch allocation failed");
+    if (int rc = set_smem(kern, smem)) return rc;
+    kern<<<grid, T, smem, s>>>(p, hplane);
+    cudaError_t e = cudaGetLastError();
+    cudaFreeAsync(hplane, s);
+    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_colhist16_u16: ") + cudaGetErrorString(e));
+    g_kernel = "k_colhist16_u16";
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return MTB_OK;
+}
+
+template <int T, int G>
+static int run_colhist16_u16_g(SlabParams p, int B, cudaStream_t s) {
+    switch ((2 * p.radius + 1) % G) {
+        case 1: return run_colhist16_u16_gm<T, G, (G > 1 ? 1 : 0)>(p, B, s);
+        case 3: return run_colhist16_u16_gm<T, G, (G > 3 ? 3 : 0)>(p, B, s);
+        case 5: return run_colhist16_u16_gm<T, G, (G > 5 ? 5 : 0)>(p, B, s);
+        case 7: return run_colhist16_u16_gm<T, G, (G > 7 ? 7 : 0)>(p, B, s);
+        default: return run_colhist16_u16_gm<T, G, 0>(p, B, s);
+    }
+}
+
+static int run_colhist16_u16(SlabParams p, int B, cudaStream_t s) {
+    const int n = 2 * p.radius + 1;
+    if (8 * n <= 255) return run_colhist16_u16_g<256, 8>(p, B, s);
+    if (4 * n <= 255) return run_colhist16_u16_g<256, 4>(p, B, s);
+    if (2 * n <= 255) return run_colhist16_u16_g<256, 2>(p, B, s);
+    return run_colhist16_u16_g<256, 1>(p, B, s);
+}
+
 // 8-bit column-histogram gather kernels; the variant by radius (tools/probe.py
 // sweep on config 2): 16-bin records, one pixel per thread for
 // r <= 5, two for r <= 13; radix-4 records above.  MTB_CH_VAR forces one.
@@ -400,6 +446,16 @@ static int run(SlabParams p, int B, cudaStream_t s) {
         (force == "colhist" || (force.empty() && p.radius <= env_int("MTB_CH_MAX_R", 40))))
         return run_colhist_u8(p, B, s);
     if (sizeof(P) == 1 && !wide && (force == "ctmf" || force.empty())) return run_ctmf_u8(p, B, s);
+    // 16-bit: compact high bytes (sampled spread <= MTB_U16_SPREAD) -> the
+    // two-phase column-histogram kernel; widely spread -> sorted-column
+    // kernel for r <= MTB_U16_V2_MAX_R, the two-phase kernel above it
+    bool spread = false;
+    if (sizeof(P) == 2 && force.empty()) {
+        spread = wide_spread_u16(p, s);
+        if (n <= 255 && (!spread || p.radius > env_int("MTB_U16_V2_MAX_R", 15)))
+            return run_colhist16_u16(p, B, s);
+    }
+    if (sizeof(P) == 2 && n <= 255 && force == "colhist") return run_colhist16_u16(p, B, s);
     if (sizeof(P) == 1 && !wide && force != "vert" && (n * n <= 255 || force == "vert2")) {
         constexpr int T = 128;
         const int bx = (p.W + T - 1) / T;
@@ -419,7 +475,7 @@ static int run(SlabParams p, int B, cudaStream_t s) {
         dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
         return wide ? launch(k_vert_u8<uint32_t, T>, grid, T, smem, s, p, "k_vert_u8<u32>")
                     : launch(k_vert_u8<uint16_t, T>, grid, T, smem, s, p, "k_vert_u8<u16>");
-    } else if (!wide && force != "vert" && (force == "vert2" || wide_spread_u16(p, s))) {
+    } else if (!wide && (force == "vert2" || (force.empty() && spread))) {
         constexpr int T = 64;
         const int n16 = (int)n;
         const size_t smem = (size_t)(16 + 256 + 16) * T * 2 + (size_t)(T + 2 * p.radius) * n16 * 2 +

@@ -343,3 +343,45 @@ def test_colhist_variants_all_group_tails(var, name, monkeypatch):
             out = mtb.rank_filter(torch.from_numpy(img).cuda(), r, rank=rank).cpu().numpy()
             assert _lib.last_kernel() == name, _lib.last_kernel()
             assert np.array_equal(out, O.iot_filter(img, n, rank=rank)), (var, r, rank)
+
+
+@pytest.mark.parametrize("kind", ["compact", "uniform"])
+def test_colhist16_u16_two_phase(kind, monkeypatch):
+    """k_colhist16_u16 (high byte by column records, then one low-byte sweep
+    per high byte used by the tile) at radii covering every group size/tail,
+    ragged tiles, min / max / off-centre ranks; the uniform image makes many
+    high bytes per tile (many low-byte sweeps)."""
+    from paper_1105_3829_b200 import _lib
+
+    monkeypatch.setenv("MTB_KERNEL", "colhist")
+    rng = np.random.default_rng(123 if kind == "compact" else 321)
+    h, w = 150, 300
+    if kind == "compact":
+        px = (20000 + rng.normal(0, 250, (h, w))).clip(0, 65535).astype(np.uint16)
+    else:
+        px = rng.integers(0, 65536, (h, w)).astype(np.uint16)
+    for r in (1, 2, 3, 4, 5, 7, 8, 15, 16, 31, 32, 63, 64, 127):
+        n = 2 * r + 1
+        for rank in (None, 1, n * n, (n * n) // 3 + 1):
+            out = mtb.rank_filter(torch.from_numpy(px).cuda(), r, rank=rank).cpu().numpy()
+            assert _lib.last_kernel() == "k_colhist16_u16", _lib.last_kernel()
+            assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (kind, r, rank)
+
+
+def test_colhist16_u16_batch_slab_and_lut(monkeypatch):
+    """Two-phase 16-bit kernel through the batch entry (per-image scratch
+    planes), a row slab with a pitched output, and a value map."""
+    monkeypatch.setenv("MTB_KERNEL", "colhist")
+    rng = np.random.default_rng(5)
+    imgs = (30000 + rng.normal(0, 400, (3, 90, 130))).clip(0, 65535).astype(np.uint16)
+    out = mtb.rank_filter(torch.from_numpy(imgs).cuda(), 6).cpu().numpy()
+    for i in range(3):
+        assert np.array_equal(out[i], O.iot_filter(imgs[i], 13)), i
+    px = imgs[0]
+    ref = O.iot_filter(px, 13)
+    big = torch.zeros((90, 160), dtype=torch.uint16, device="cuda")
+    sl = mtb.rank_filter(torch.from_numpy(px).cuda(), 6, rows=(20, 70), out=big[20:70, :130])
+    assert np.array_equal(sl.cpu().numpy(), ref[20:70])
+    lut = torch.from_numpy((np.arange(65536) & ~np.uint32(15)).astype(np.uint16)).cuda()
+    q = mtb.rank_filter(torch.from_numpy(px).cuda(), 6, lut=lut).cpu().numpy()
+    assert np.array_equal(q, ref & ~np.uint16(15))
