@@ -3,7 +3,9 @@
 // The host side only validates, picks a kernel variant and a grid, and
 // launches; there is no CPU compute path and no fallback: a missing device
 // or a launch failure is reported as an error.
+#include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -527,6 +529,133 @@ static SlabParams make_params(const void *src, int64_t src_pitch, int32_t src_ro
 
 using namespace mtb;
 
+// ---------------------------------------------------------------------------
+// Host-buffer path (mtb_filter_host): the frame is cut into row bands; band
+// i's source rows go host->device on a copy stream, its filter launch waits
+// only for the rows it reads (band + r halo rows), and its result rows go
+// device->host on a second copy stream -- so the copies of one band overlap
+// the filtering of its neighbours.  Device buffers and streams are kept per
+// device between calls (the pool grows, never shrinks).
+struct HostCtx {
+    int dev = -1;
+    void *dsrc = nullptr, *ddst = nullptr, *dlut = nullptr;
+    size_t cap = 0;
+    cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
+    static constexpr int KMAX = 16;
+    cudaEvent_t eh[KMAX], ec[KMAX];
+};
+
+static std::mutex g_host_mu;
+static HostCtx g_host[64];
+
+static int host_ctx(HostCtx *&ctx, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return fail(MTB_E_CUDA, "device index out of range");
+    ctx = &g_host[dev];
+    auto ok = [](cudaError_t e, const char *what) {
+        if (e != cudaSuccess) {
+            fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+            return false;
+        }
+        return true;
+    };
+    if (ctx->dev < 0) {
+        if (!ok(cudaStreamCreateWithFlags(&ctx->sh, cudaStreamNonBlocking), "cudaStreamCreate") ||
+            !ok(cudaStreamCreateWithFlags(&ctx->sc, cudaStreamNonBlocking), "cudaStreamCreate") ||
+            !ok(cudaStreamCreateWithFlags(&ctx->sd, cudaStreamNonBlocking), "cudaStreamCreate") ||
+            !ok(cudaMalloc(&ctx->dlut, 65536 * 2), "cudaMalloc"))
+            return MTB_E_CUDA;
+        for (int i = 0; i < HostCtx::KMAX; ++i)
+            if (!ok(cudaEventCreateWithFlags(&ctx->eh[i], cudaEventDisableTiming), "cudaEventCreate") ||
+                !ok(cudaEventCreateWithFlags(&ctx->ec[i], cudaEventDisableTiming), "cudaEventCreate"))
+                return MTB_E_CUDA;
+        ctx->dev = dev;
+    }
+    if (ctx->cap < bytes) {
+        cudaDeviceSynchronize();
+        if (ctx->dsrc) cudaFree(ctx->dsrc);
+        if (ctx->ddst) cudaFree(ctx->ddst);
+        ctx->dsrc = ctx->ddst = nullptr;
+        ctx->cap = 0;
+        if (!ok(cudaMalloc(&ctx->dsrc, bytes), "cudaMalloc") || !ok(cudaMalloc(&ctx->ddst, bytes), "cudaMalloc"))
+            return MTB_E_CUDA;
+        ctx->cap = bytes;
+    }
+    return MTB_OK;
+}
+
+static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W, int radius, int64_t rank,
+                         const void *lut, uint32_t flags) {
+    std::lock_guard<std::mutex> lock(g_host_mu);
+    const size_t es = bit_depth == 8 ? 1 : 2;
+    const size_t row = (size_t)W * es;
+    HostCtx *ctx = nullptr;
+    if (int rc = host_ctx(ctx, (size_t)H * row)) return rc;
+    // bands: enough rows that per-band launch and halo overheads stay small
+    // (measured on config 2, tools/e2e_probe.py: 4 bands of 1024 rows for
+    // r <= 31, 2 for r = 63 -- shorter bands re-pay the n-row column build)
+    const int min_rows = std::max(1024, 32 * radius);
+    int K = env_int("MTB_HOST_BANDS", std::min(8, std::max(1, H / min_rows)));
+    K = std::max(1, std::min(K, std::min(HostCtx::KMAX, H)));
+    auto cuda_ok = [](cudaError_t e, const char *what) {
+        return e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    if (lut) {
+        if (int rc = cuda_ok(cudaMemcpyAsync(ctx->dlut, lut, ((size_t)1 << bit_depth) * es, cudaMemcpyHostToDevice,
+                                             ctx->sh), "H2D lut"))
+            return rc;
+    }
+    const char *s8 = static_cast<const char *>(src);
+    char *d8 = static_cast<char *>(dst);
+    char *ds = static_cast<char *>(ctx->dsrc);
+    char *dd = static_cast<char *>(ctx->ddst);
+    int copied = 0;  // source rows [0, copied) enqueued host->device
+    int rc = MTB_OK;
+    auto band = [&](int i, int &a, int &b) {
+        a = (int)((int64_t)H * i / K);
+        b = (int)((int64_t)H * (i + 1) / K);
+    };
+    // result rows of band i back to the host (enqueued one band late: with
+    // pageable host memory the call blocks until the copy is done, and by
+    // then the next band's filter is already queued behind it)
+    auto d2h = [&](int i) {
+        int a, b;
+        band(i, a, b);
+        cudaStreamWaitEvent(ctx->sd, ctx->ec[i], 0);
+        return cuda_ok(cudaMemcpyAsync(d8 + (size_t)a * row, dd + (size_t)a * row, (size_t)(b - a) * row,
+                                       cudaMemcpyDeviceToHost, ctx->sd), "D2H");
+    };
+    int done = 0;
+    for (int i = 0; i < K && rc == MTB_OK; ++i) {
+        int a, b;
+        band(i, a, b);
+        const int need = std::min(H, b + radius);
+        if (need > copied) {
+            rc = cuda_ok(cudaMemcpyAsync(ds + copied * row, s8 + copied * row, (size_t)(need - copied) * row,
+                                         cudaMemcpyHostToDevice, ctx->sh), "H2D");
+            copied = need;
+        }
+        if (rc) break;
+        cudaEventRecord(ctx->eh[i], ctx->sh);
+        cudaStreamWaitEvent(ctx->sc, ctx->eh[i], 0);
+        rc = bit_depth == 8
+                 ? mtb_median_u8((const uint8_t *)ds, W, 0, H, (uint8_t *)(dd + (size_t)a * row), W, H, W, a, b,
+                                 radius, rank, lut ? (const uint8_t *)ctx->dlut : nullptr, flags, ctx->sc)
+                 : mtb_median_u16((const uint16_t *)ds, W, 0, H, (uint16_t *)(dd + (size_t)a * row), W, H, W, a,
+                                  b, radius, rank, lut ? (const uint16_t *)ctx->dlut : nullptr, flags, ctx->sc);
+        if (rc) break;
+        cudaEventRecord(ctx->ec[i], ctx->sc);
+        if (i >= 1) rc = d2h(i - 1);
+        done = i;
+    }
+    if (rc == MTB_OK) rc = d2h(done);
+    const int rs = cuda_ok(cudaStreamSynchronize(ctx->sd), "cudaStreamSynchronize");
+    cudaStreamSynchronize(ctx->sc);
+    cudaStreamSynchronize(ctx->sh);
+    return rc ? rc : rs;
+}
+
 extern "C" {
 
 int mtb_median_u8(const uint8_t *src, int64_t src_pitch, int32_t src_row0, int32_t src_rows,
@@ -577,38 +706,7 @@ int mtb_filter_host(const void *src, void *dst, int32_t bit_depth, int32_t H, in
         return fail(MTB_E_INVAL, "bit_depth must be 8 or 16, got " + std::to_string(bit_depth));
     if (!src || !dst) return fail(MTB_E_INVAL, "null src/dst pointer");
     if (H < 1 || W < 1) return fail(MTB_E_INVAL, "pixels must be a non-empty 2D array");
-    const size_t es = bit_depth == 8 ? 1 : 2;
-    const size_t bytes = (size_t)H * (size_t)W * es;
-    const size_t lut_bytes = ((size_t)1 << bit_depth) * es;
-    void *dsrc = nullptr, *ddst = nullptr, *dlut = nullptr;
-    cudaStream_t s = nullptr;
-    int rc = MTB_OK;
-    auto check = [&](cudaError_t e, const char *what) {
-        if (e != cudaSuccess && rc == MTB_OK)
-            rc = fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-        return e == cudaSuccess;
-    };
-    if (check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate") &&
-        check(cudaMallocAsync(&dsrc, bytes, s), "cudaMallocAsync") &&
-        check(cudaMallocAsync(&ddst, bytes, s), "cudaMallocAsync") &&
-        (!lut || check(cudaMallocAsync(&dlut, lut_bytes, s), "cudaMallocAsync")) &&
-        check(cudaMemcpyAsync(dsrc, src, bytes, cudaMemcpyHostToDevice, s), "H2D") &&
-        (!lut || check(cudaMemcpyAsync(dlut, lut, lut_bytes, cudaMemcpyHostToDevice, s), "H2D"))) {
-        rc = bit_depth == 8
-                 ? mtb_median_u8((const uint8_t *)dsrc, W, 0, H, (uint8_t *)ddst, W, H, W, 0, H,
-                                 radius, rank, (const uint8_t *)dlut, flags, s)
-                 : mtb_median_u16((const uint16_t *)dsrc, W, 0, H, (uint16_t *)ddst, W, H, W, 0,
-                                  H, radius, rank, (const uint16_t *)dlut, flags, s);
-        if (rc == MTB_OK) check(cudaMemcpyAsync(dst, ddst, bytes, cudaMemcpyDeviceToHost, s), "D2H");
-    }
-    if (s) {
-        if (dsrc) cudaFreeAsync(dsrc, s);
-        if (ddst) cudaFreeAsync(ddst, s);
-        if (dlut) cudaFreeAsync(dlut, s);
-        check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-        cudaStreamDestroy(s);
-    }
-    return rc;
+    return host_pipeline(src, dst, bit_depth, H, W, radius, rank, lut, flags);
 }
 
 uint64_t mtb_launch_count(void) { return g_launches.load(); }

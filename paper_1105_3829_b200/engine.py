@@ -242,18 +242,30 @@ def median_filter(image, radius: int, bit_depth: int | None = None, adaptive: bo
 
 
 def filter_host_buffer(src: np.ndarray, radius: int, rank: int | None = None,
-                       lut: np.ndarray | None = None, adaptive: bool = False) -> np.ndarray:
+                       lut: np.ndarray | None = None, adaptive: bool = False,
+                       out: np.ndarray | None = None) -> np.ndarray:
     """Whole-frame call through the C ABI's HOST-buffer entry
-    (mtb_filter_host): what a ctypes binding in the reference would use."""
+    (mtb_filter_host): what a ctypes binding in the reference would use.
+    The library pipelines row bands (copy in / filter / copy out overlap);
+    page-locked ``src`` / ``out`` buffers (e.g. numpy views of pinned torch
+    tensors) make the copies asynchronous.  ``out``: optional C-contiguous
+    destination of src's shape and dtype."""
     src = np.ascontiguousarray(src)
     bits = 8 if src.dtype == np.uint8 else 16
     if src.dtype not in (np.uint8, np.uint16):
         raise ValueError("src must be uint8 or uint16")
+    if src.ndim != 2:
+        raise ValueError("src must be a 2-D array")
     H, W = src.shape
     n = 2 * int(radius) + 1
     if rank is None:
         rank = (n * n + 1) // 2
-    dst = np.empty_like(src)
+    if out is None:
+        dst = np.empty_like(src)
+    else:
+        if out.shape != src.shape or out.dtype != src.dtype or not out.flags.c_contiguous:
+            raise ValueError("out must be C-contiguous with src's shape and dtype")
+        dst = out
     lut_ptr = None
     if lut is not None:
         lut = np.ascontiguousarray(lut, dtype=src.dtype)

@@ -202,6 +202,33 @@ def test_host_buffer_entry_point(rng):
                           O.iot_filter(px16, 7, max_error=16))
 
 
+@pytest.mark.parametrize("bits,r,bands", [(8, 2, None), (8, 9, "3"), (8, 40, None), (16, 5, None),
+                                          (16, 20, "5"), (8, 3, "16")])
+def test_host_pipeline_bands(bits, r, bands, monkeypatch):
+    """mtb_filter_host cuts the frame into row bands whose copies overlap the
+    filtering; results must not depend on the band count (pinned and
+    pageable buffers, caller-provided out)."""
+    if bands:
+        monkeypatch.setenv("MTB_HOST_BANDS", bands)
+    rng = np.random.default_rng(bits * 100 + r)
+    H, W = 1300, 333
+    if bits == 8:
+        px = workloads.cfg2_blur_sp_u8(H, W, seed=r)
+    else:
+        px = (25000 + rng.normal(0, 500, (H, W))).clip(0, 65535).astype(np.uint16)
+    tdt = torch.uint8 if bits == 8 else torch.uint16
+    pin_src = torch.empty((H, W), dtype=tdt).pin_memory().numpy()
+    pin_src[...] = px
+    pin_out = torch.empty((H, W), dtype=tdt).pin_memory().numpy()
+    got = mtb.filter_host_buffer(pin_src, r, out=pin_out)
+    assert got is pin_out
+    ref = O.iot_filter(px, 2 * r + 1)
+    assert np.array_equal(pin_out, ref)
+    assert np.array_equal(mtb.filter_host_buffer(px, r), ref)
+    with pytest.raises(ValueError):
+        mtb.filter_host_buffer(px, r, out=np.empty((H, W + 1), px.dtype))
+
+
 # ------------------------------------------------ full-size BASELINE configs
 
 def _check_bands(px, out, n, samples, mode="uniform"):
