@@ -143,15 +143,11 @@ def _run(px: np.ndarray, bits: int, radius: int, rank: int, lut: np.ndarray | No
         devices = [torch.cuda.current_device()]
     devices = [torch.device("cuda", d) if isinstance(d, int) else torch.device(d) for d in devices]
     if len(devices) == 1:
-        dev = devices[0]
-        with torch.cuda.device(dev):
-            src = host.to(dev)
-            dlut = torch.from_numpy(lut).to(dev) if lut is not None else None
-            out = torch.empty((H, W), dtype=tdt, device=dev)
-            for a, b in _band_edges(H, bands):
-                rank_filter(src, radius, rank, out=out[a:b], lut=dlut, adaptive=adaptive,
-                            rows=(a, b), height=H)
-            return out.cpu().numpy()
+        # one device: the library's host-buffer entry, which pipelines row
+        # bands (copy in / filter / copy out overlap); `bands` does not change
+        # results and the library picks its own band count
+        with torch.cuda.device(devices[0]):
+            return filter_host_buffer(px, radius, rank, lut=lut, adaptive=adaptive)
     # several GPUs: one slab per device (each may still be cut into bands)
     pinned = host.pin_memory()
     result = torch.empty((H, W), dtype=tdt).pin_memory()
