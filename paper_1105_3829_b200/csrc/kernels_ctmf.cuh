@@ -292,7 +292,7 @@ __device__ __forceinline__ bool ct_rows_aligned16(const void *src, int64_t pitch
 
 template <int S>
 __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int tiles_x, int tiles_y,
-                                                        uint8_t *__restrict__ snap) {
+                                                        uint8_t *__restrict__ snap, int snap_two_scans) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -330,51 +330,63 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
     __syncwarp();
 
     // ---- per-tile snapshot of every column's initial span (rows clamp(Y0-r ..
-    // Y0+r)): its full 256-bin histogram and its cumulative coarse counts,
-    // built once in a global workspace; every pass then initialises its
-    // column histograms from it in O(columns) instead of rescanning n rows.
-    // Layout per resident warp (reused for each of its tiles, so the live
-    // set stays L2-resident): cu[NCP] (16 B: count below 16*b, bytes),
-    // off[NCP] (u16), then a heap of 16-B fine chunks -- per column only
-    // the bins present in its span, ascending, starting at chunk off[c].
+    // Y0+r)) in a global workspace; every pass then initialises its column
+    // histograms from it in O(columns) instead of rescanning n rows.
+    // Layout per resident warp (reused for each of its tiles): cu[NCP] (16 B:
+    // count below 16*b, bytes), off[NCP] (u16), then a heap of 16-B fine
+    // chunks.  Two scans of the spans: before the coarse pass only cu; after
+    // it, the fine chunks of the bins the fine passes will need (coarse bins
+    // of the tile's outputs that are present in the column), packed per
+    // column from chunk off[c] -- a live set small enough to stay in L2.
     const size_t heap_off = ((size_t)g.NCP * 18 + 15) & ~(size_t)15;
     const size_t snap_stride = heap_off + (size_t)g.NCP * 256;
     uint4 *snap_cu = nullptr, *snap_heap = nullptr;
     uint16_t *snap_off = nullptr;
-    if (snap) {
-        const size_t slot = ((size_t)blockIdx.z * gridDim.x + blockIdx.x) * CT_WARPS + warp;
-        uint8_t *rec = snap + slot * snap_stride;
-        snap_cu = reinterpret_cast<uint4 *>(rec);
-        snap_off = reinterpret_cast<uint16_t *>(rec + (size_t)g.NCP * 16);
-        snap_heap = reinterpret_cast<uint4 *>(rec + heap_off);
+    uint32_t needb[4] = {0, 0, 0, 0};  // byte masks of the needed bins
+    auto snap_scan = [&](bool cu_too, bool chunks, uint32_t need) {
         uint8_t *scr = reinterpret_cast<uint8_t *>(colA) + lane * 260;  // lane-private column
         int heap_top = 0;
         for (int g0 = 0; g0 < g.NC; g0 += 32) {
             const int c = g0 + lane;
             const int gx = clampi(X0 - r + min(c, g.NC - 1), 0, W - 1);
             for (int i = 0; i < 65; ++i) reinterpret_cast<uint32_t *>(scr)[i] = 0;
+            // 16 loads in flight per lane: the spans come from L2 and this
+            // scan is latency-bound otherwise
             int j = -r;
+            for (; j + 15 <= r; j += 16) {
+                unsigned v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) v[u] = __ldg(src_row(p, src, clampi(Y0 + j + u, 0, H - 1)) + gx);
+#pragma unroll
+                for (int u = 0; u < 16; ++u) scr[v[u]] += 1;
+            }
             for (; j + 3 <= r; j += 4) {
-                const unsigned v0 = __ldg(src_row(p, src, clampi(Y0 + j, 0, H - 1)) + gx);
-                const unsigned v1 = __ldg(src_row(p, src, clampi(Y0 + j + 1, 0, H - 1)) + gx);
-                const unsigned v2 = __ldg(src_row(p, src, clampi(Y0 + j + 2, 0, H - 1)) + gx);
-                const unsigned v3 = __ldg(src_row(p, src, clampi(Y0 + j + 3, 0, H - 1)) + gx);
-                scr[v0] += 1;
-                scr[v1] += 1;
-                scr[v2] += 1;
-                scr[v3] += 1;
+                unsigned v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = __ldg(src_row(p, src, clampi(Y0 + j + u, 0, H - 1)) + gx);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) scr[v[u]] += 1;
             }
             for (; j <= r; ++j) scr[__ldg(src_row(p, src, clampi(Y0 + j, 0, H - 1)) + gx)] += 1;
             const uint32_t *w = reinterpret_cast<const uint32_t *>(scr);
-            uint32_t acc = 0, pres = 0, cw[4] = {0, 0, 0, 0};
+            if (cu_too) {
+                uint32_t acc = 0, cw[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    cw[q >> 2] |= acc << (8 * (q & 3));
+                    acc += __vsadu4(w[4 * q], 0) + __vsadu4(w[4 * q + 1], 0) + __vsadu4(w[4 * q + 2], 0) +
+                           __vsadu4(w[4 * q + 3], 0);
+                }
+                if (c < g.NC) snap_cu[c] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+                if (!chunks) continue;
+            }
+            uint32_t pres = 0;
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-                cw[q >> 2] |= acc << (8 * (q & 3));
-                const uint32_t cb = __vsadu4(w[4 * q], 0) + __vsadu4(w[4 * q + 1], 0) +
-                                    __vsadu4(w[4 * q + 2], 0) + __vsadu4(w[4 * q + 3], 0);
+                const uint32_t cb = w[4 * q] | w[4 * q + 1] | w[4 * q + 2] | w[4 * q + 3];
                 pres |= (cb ? 1u : 0u) << q;
-                acc += cb;
             }
+            pres &= need;
             // warp exclusive scan of the chunk counts -> heap positions
             const int K = c < g.NC ? __popc(pres) : 0;
             int incl = K;
@@ -386,7 +398,6 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
             const int off = heap_top + incl - K;
             heap_top += __shfl_sync(0xffffffffu, incl, 31);
             if (c < g.NC) {
-                snap_cu[c] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
                 snap_off[c] = (uint16_t)off;
                 int k = off;
                 for (uint32_t m = pres; m; m &= m - 1) {
@@ -396,6 +407,20 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
             }
         }
         __syncwarp();
+    };
+    if (snap) {
+        const size_t slot = ((size_t)blockIdx.z * gridDim.x + blockIdx.x) * CT_WARPS + warp;
+        uint8_t *rec = snap + slot * snap_stride;
+        snap_cu = reinterpret_cast<uint4 *>(rec);
+        snap_off = reinterpret_cast<uint16_t *>(rec + (size_t)g.NCP * 16);
+        snap_heap = reinterpret_cast<uint4 *>(rec + heap_off);
+        // snap_two_scans: cu first, chunks of the needed bins after the coarse
+        // pass (small live set); else one scan storing every present bin
+        snap_scan(true, !snap_two_scans, 0xffffu);
+        if (!snap_two_scans) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) needb[i] = 0xffffffffu;
+        }
     }
     const uint32_t nspan = (uint32_t)(2 * r + 1);
 
@@ -410,6 +435,16 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
     for (int pass = 0;; ++pass) {
         if (pass > 0) {
             if (tile_mask == 0) break;
+            if (pass == 1 && snap && snap_two_scans) {
+                __syncwarp();
+                snap_scan(false, true, tile_mask);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t nb = (tile_mask >> (4 * i)) & 15u;
+                    needb[i] = ((nb & 1u) ? 0xffu : 0u) | ((nb & 2u) ? 0xff00u : 0u) |
+                               ((nb & 4u) ? 0xff0000u : 0u) | ((nb & 8u) ? 0xff000000u : 0u);
+                }
+            }
             // descending: a pixel finalised by pass beta holds a value >= 16*beta,
             // which can never be mistaken for a lower coarse bin still pending
             beta = 31 - __clz(tile_mask);
@@ -464,7 +499,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
                             for (int i = 0; i < 4; ++i) {
                                 const int nb = min(max(beta - 4 * i, 0), 4);
                                 const uint32_t sel = nb >= 4 ? 0xffffffffu : ((1u << (8 * nb)) - 1u);
-                                k += __popc(__vcmpne4(d[i], 0) & sel) >> 3;
+                                k += __popc(__vcmpne4(d[i], 0) & sel & needb[i]) >> 3;
                             }
                             const uint4 f = __ldcg(snap_heap + k);
                             cnt[0] = f.x; cnt[1] = f.y; cnt[2] = f.z; cnt[3] = f.w;

@@ -204,7 +204,7 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
             snap = nullptr;  // fall back to rescanning the spans
         }
     }
-    kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y, snap);
+    kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y, snap, env_int("MTB_CT_SCAN2", 1));
     cudaError_t e = cudaGetLastError();
     if (snap) cudaFreeAsync(snap, s);
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_ctmf_u8: ") + cudaGetErrorString(e));
