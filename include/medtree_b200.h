@@ -89,6 +89,16 @@ int mtb_median_batch_u16(const uint16_t *src, int64_t src_image_stride, int64_t 
 int mtb_filter_host(const void *src, void *dst, int32_t bit_depth, int32_t H, int32_t W,
                     int32_t radius, int64_t rank, const void *lut, uint32_t flags);
 
+/* Independent exact selection on DEVICE buffers: per pixel, the bits of the
+ * rank-th smallest window value are decided from the top by counting passes
+ * over the n x n replicate-clamped window (O(d * n^2) per pixel).  Shares no
+ * code with the fast kernels; it is the package's GPU stand-in for the
+ * reference's oracle filters (oracles.py:36-66, used by `cli compare` and
+ * `bench --oracle`).  bit_depth 8 or 16; src/dst uint8/uint16 [H][pitch]. */
+int mtb_rank_bruteforce(const void *src, int64_t src_pitch, void *dst, int64_t dst_pitch,
+                        int32_t bit_depth, int32_t H, int32_t W, int32_t radius, int64_t rank,
+                        void *stream);
+
 /* Kernel launches issued by this library since load (evidence counter). */
 uint64_t mtb_launch_count(void);
 

@@ -17,6 +17,7 @@
 #include "kernels_lob.cuh"
 #include "kernels_sortnet.cuh"
 #include "kernels_colhist.cuh"
+#include "kernels_select.cuh"
 #include <cstdlib>
 
 namespace mtb {
@@ -707,6 +708,31 @@ int mtb_filter_host(const void *src, void *dst, int32_t bit_depth, int32_t H, in
     if (!src || !dst) return fail(MTB_E_INVAL, "null src/dst pointer");
     if (H < 1 || W < 1) return fail(MTB_E_INVAL, "pixels must be a non-empty 2D array");
     return host_pipeline(src, dst, bit_depth, H, W, radius, rank, lut, flags);
+}
+
+int mtb_rank_bruteforce(const void *src, int64_t src_pitch, void *dst, int64_t dst_pitch, int32_t bit_depth,
+                        int32_t H, int32_t W, int32_t radius, int64_t rank, void *stream) {
+    if (bit_depth != 8 && bit_depth != 16)
+        return fail(MTB_E_INVAL, "bit_depth must be 8 or 16, got " + std::to_string(bit_depth));
+    if (!src || !dst) return fail(MTB_E_INVAL, "null src/dst pointer");
+    if (H < 1 || W < 1) return fail(MTB_E_INVAL, "pixels must be a non-empty 2D array");
+    if (radius < 0) return fail(MTB_E_INVAL, "radius must be >= 0");
+    const int64_t n = 2 * (int64_t)radius + 1;
+    if (rank < 1 || rank > n * n) return fail(MTB_E_INVAL, "rank must be in [1, n*n]");
+    if (src_pitch < W || dst_pitch < W) return fail(MTB_E_INVAL, "pitch must be >= W");
+    dim3 block(32, 8), grid((W + 31) / 32, (H + 7) / 8);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (bit_depth == 8)
+        k_select_brute<uint8_t, 8><<<grid, block, 0, s>>>((const uint8_t *)src, src_pitch, (uint8_t *)dst, dst_pitch,
+                                                          H, W, radius, (uint32_t)rank);
+    else
+        k_select_brute<uint16_t, 16><<<grid, block, 0, s>>>((const uint16_t *)src, src_pitch, (uint16_t *)dst,
+                                                            dst_pitch, H, W, radius, (uint32_t)rank);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_select_brute: ") + cudaGetErrorString(e));
+    g_kernel = "k_select_brute";
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return MTB_OK;
 }
 
 uint64_t mtb_launch_count(void) { return g_launches.load(); }
