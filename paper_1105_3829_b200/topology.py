@@ -198,22 +198,21 @@ def uniform_levels(bit_depth: int, max_error: int) -> int:
     return max(0, min(bit_depth, levels))
 
 
-def value_map(topology: TreeTopology, max_error: int) -> np.ndarray | None:
-    """Output value as a function of the exact rank value, or None for the
-    identity.  Uniform: v & ~(w-1), w = 2^(d-levels) (_kernels.py:229-253).
-    Adaptive: lower bound of the first node on v's root-to-leaf path that
-    is no wider than max_error, or whose child is a leaf (_kernels.py:256-289)."""
+def descent_intervals(topology: TreeTopology, max_error: int) -> tuple[np.ndarray, np.ndarray]:
+    """(lo, width) of the interval where the reference's rank descent stops,
+    for every exact rank value v (int64 arrays of 2^d entries).  Uniform:
+    lo = v & ~(w-1), width w = 2^(d-levels) (_kernels.py:229-253).  Adaptive:
+    the first node on v's root-to-leaf path no wider than max_error, or
+    whose child is a leaf, or whose right part is within the leaf precision
+    (_kernels.py:256-289)."""
     d = topology.bit_depth
-    dtype = np.uint8 if d <= 8 else np.uint16
     nv = 1 << d
+    v = np.arange(nv, dtype=np.int64)
     if topology.mode == "uniform":
         w = 1 << (d - uniform_levels(d, max_error))
-        if w == 1:
-            return None
-        return (np.arange(nv, dtype=np.int64) & ~(w - 1)).astype(dtype)
+        return v & ~(w - 1), np.full(nv, w, dtype=np.int64)
     up, leaf, span = topology.up, topology.leaf.astype(bool), topology.span
     prec = topology.leaf_precision
-    v = np.arange(nv, dtype=np.int64)
     lo = np.zeros(nv, dtype=np.int64)
     hi = np.full(nv, nv, dtype=np.int64)
     pos = np.ones(nv, dtype=np.int64)
@@ -234,6 +233,13 @@ def value_map(topology: TreeTopology, max_error: int) -> np.ndarray | None:
         live[ri[stop_r]] = False
         still = np.nonzero(live)[0]
         live[still] = hi[still] - lo[still] > max_error
-    if np.array_equal(lo, v):
+    return lo, hi - lo
+
+
+def value_map(topology: TreeTopology, max_error: int) -> np.ndarray | None:
+    """Output value as a function of the exact rank value (the lower bound
+    of descent_intervals), or None for the identity."""
+    lo, _ = descent_intervals(topology, max_error)
+    if np.array_equal(lo, np.arange(lo.size, dtype=np.int64)):
         return None
-    return lo.astype(dtype)
+    return lo.astype(np.uint8 if topology.bit_depth <= 8 else np.uint16)

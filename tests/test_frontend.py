@@ -176,3 +176,41 @@ def test_bruteforce_oracle_matches_c_oracle(bits):
         assert np.array_equal(got, ref)
         out, adds = mtb.huang_filter(px, n, rank)
         assert np.array_equal(out.pixels, ref) and adds == 45 * (n * n + 51 * 2 * n)
+
+
+def test_window_engine_host_checks():
+    img = mtb.gen_image("normal_noise", 9, 7, 8, 1)
+    with pytest.raises(ValueError, match="topology is 16-bit, image is 8-bit"):
+        mtb.WindowEngine(img, 3, mtb.uniform_topology(16))
+    with pytest.raises(ValueError):
+        mtb.WindowEngine(img, 4, mtb.uniform_topology(8))
+
+
+def test_descent_intervals_agree_with_recorded_steps():
+    """(value, bound) is a function of the exact value: every recorded step
+    of the reference must be descent_intervals() of some value (CPU check
+    of the interval tables themselves)."""
+    for c in G["window_engine"]:
+        im = mtb.gen_image(c["kind"], 9, 7, c["depth"], c["seed"])
+        topo = mtb.resolve_topology(im, c["n"], c["mode"])
+        lo, width = mtb.descent_intervals(topo, c["max_error"])
+        pairs = set(zip(lo.tolist(), width.tolist()))
+        assert all(tuple(s) in pairs for s in c["steps"])
+
+
+@pytest.mark.gpu
+def test_window_engine_steps_match_reference():
+    for c in G["window_engine"]:
+        im = mtb.gen_image(c["kind"], 9, 7, c["depth"], c["seed"])
+        topo = mtb.resolve_topology(im, c["n"], c["mode"])
+        eng = mtb.WindowEngine(im, c["n"], topo, rank=c["rank"], max_error=c["max_error"])
+        assert eng.position == (0, 0)
+        steps = [list(s) for s in eng]
+        assert steps == c["steps"], (c["mode"], c["max_error"])
+        assert eng.position == (0, 7) and eng.counters.pixels == 63
+        with pytest.raises(StopIteration):
+            eng.step()
+        with pytest.raises(RuntimeError, match="fresh engine"):
+            eng.run()
+        eng2 = mtb.WindowEngine(im, c["n"], topo, rank=c["rank"], max_error=c["max_error"])
+        assert eng2.run().tolist() == c["run"]
