@@ -28,6 +28,7 @@
 #pragma once
 #include "common.cuh"
 #include "kernels_ctmf.cuh"  // ct_descend
+#include "kernels_vert.cuh"  // lower_bound_multi
 
 namespace mtb {
 
@@ -472,6 +473,150 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
                 const unsigned v = ((unsigned)hb << 8) | lo;
                 *d = lut ? __ldg(lut + v) : (uint16_t)v;
             });
+    }
+}
+
+}  // namespace mtb
+
+namespace mtb {
+
+// ---------------------------------------------------------------------------
+// 16-bit, widely spread data (e.g. uniform noise): one sweep.  The high byte
+// H and the rank k within it come from radix-4 column records keyed by the
+// high byte (as in phase A of k_colhist16_u16, gathered per pixel); the low
+// byte from per-column SORTED arrays of the stripe kept in the same shared
+// memory (one delete + one insert per column and row): the window values
+// with high byte H are one run per window column, starting at
+// lower_bound(256H) (2r+1 interleaved branchless searches), counted per
+// bits 4..7 and then per bits 0..3 of the selected 16-value sub-run.
+// Replaces the per-thread high-byte counters of k_vert2_u16 (544 B per
+// thread) by shared records (340 B per column): more resident threads and
+// no read-modify-write chains in the high-byte step.
+template <int T, int G, int M>
+__global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x;
+    const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
+    const int NCOL = T + 2 * r;
+    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);                  // [85][NCOL]
+    uint16_t *sc = reinterpret_cast<uint16_t *>(rec + CH4_RECS * NCOL);      // [16][T]
+    uint8_t *rpos = reinterpret_cast<uint8_t *>(sc + 16 * T);                // [n][T]
+    uint16_t *scol = reinterpret_cast<uint16_t *>(rpos + ((n * T + 15) & ~15));  // [NCOL][n]
+    uint8_t *recb = reinterpret_cast<uint8_t *>(rec);
+    const int X0 = blockIdx.x * T;
+    const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
+    if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
+    const int y1 = min(y0 + p.rows_per_cta, p.row_end);
+    const uint16_t *src = static_cast<const uint16_t *>(p.src) + blockIdx.z * p.src_img_stride;
+    uint16_t *dst = static_cast<uint16_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
+    const uint16_t *lut = static_cast<const uint16_t *>(p.lut);
+    const int x = X0 + tid;
+    const uint16_t *wcol = scol + tid * n;  // window column j of this thread = stripe column tid + j
+
+    // records and sorted columns for row y0
+    for (int i = tid; i < CH4_RECS * NCOL; i += T) rec[i] = 0;
+    __syncthreads();
+    for (int c = tid; c < NCOL; c += T) {
+        const int gx = clampi(X0 - r + c, 0, W - 1);
+        uint16_t *a = scol + c * n;
+        for (int j = 0; j < n; ++j) {
+            const uint16_t v = __ldg(src_row(p, src, clampi(y0 - r + j, 0, H - 1)) + gx);
+            ch4_bump(recb, NCOL, c, v >> 8, 1);
+            int i = j;
+            while (i > 0 && a[i - 1] > v) {
+                a[i] = a[i - 1];
+                --i;
+            }
+            a[i] = v;
+        }
+    }
+    __syncthreads();
+    for (int y = y0; y < y1; ++y) {
+        if (y > y0) {
+            const int yo = clampi(y - r - 1, 0, H - 1), yi = clampi(y + r, 0, H - 1);
+            if (yo != yi) {
+                __syncthreads();  // previous row's reads done
+                const uint16_t *ro = src_row(p, src, yo), *ri = src_row(p, src, yi);
+                for (int c = tid; c < NCOL; c += T) {
+                    const int gx = clampi(X0 - r + c, 0, W - 1);
+                    const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
+                    if (vo == vi) continue;
+                    if ((vo >> 8) != (vi >> 8)) {
+                        ch4_bump(recb, NCOL, c, vo >> 8, -1);
+                        ch4_bump(recb, NCOL, c, vi >> 8, 1);
+                    }
+                    uint16_t *a = scol + c * n;
+                    const uint16_t *const aa[2] = {a, a};
+                    const unsigned vv[2] = {vo, vi};
+                    int pos[2];
+                    lower_bound_multi<2>(aa, n, vv, pos);
+                    const int io = pos[0], ii = pos[1];  // a[io] == vo
+                    if (ii > io) {
+                        for (int q = io; q < ii - 1; ++q) a[q] = a[q + 1];
+                        a[ii - 1] = (uint16_t)vi;
+                    } else {
+                        for (int q = io; q > ii; --q) a[q] = a[q - 1];
+                        a[ii] = (uint16_t)vi;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // high byte and rank within it
+        uint32_t k = p.rank;
+        const unsigned hb = ch4_select<G, M>(rec + tid, NCOL, n, k);
+        // low byte: runs of [256H, 256H+256) in the window columns
+        const unsigned vb = hb << 8, ve = vb + 256;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) sc[q * T + tid] = 0;
+        for (int j0 = 0; j0 < n; j0 += 8) {
+            const uint16_t *aa[8];
+            unsigned vv[8];
+            int e0[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                aa[u] = wcol + min(j0 + u, n - 1) * n;
+                vv[u] = vb;
+            }
+            lower_bound_multi<8>(aa, n, vv, e0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (j0 + u >= n) break;
+                rpos[(j0 + u) * T + tid] = (uint8_t)e0[u];
+                const uint16_t *a = aa[u];
+                for (int e = e0[u]; e < n; ++e) {
+                    const unsigned v = a[e];
+                    if (v >= ve) break;
+                    sc[((v >> 4) & 15) * T + tid] += 1;
+                }
+            }
+        }
+        uint32_t acc = 0;
+        int lb = 0;
+        for (; lb < 15; ++lb) {
+            const uint32_t c = sc[lb * T + tid];
+            if (acc + c >= k) break;
+            acc += c;
+        }
+        const unsigned vs = vb + 16u * (unsigned)lb, vse = vs + 16;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) sc[q * T + tid] = 0;
+        for (int j = 0; j < n; ++j) {
+            const uint16_t *a = wcol + j * n;
+            for (int e = rpos[j * T + tid]; e < n; ++e) {
+                const unsigned v = a[e];
+                if (v >= vse) break;
+                if (v >= vs) sc[(v & 15) * T + tid] += 1;
+            }
+        }
+        int lo = lb * 16;
+        for (const int e = lo + 15; lo < e; ++lo) {
+            const uint32_t c = sc[(lo & 15) * T + tid];
+            if (acc + c >= k) break;
+            acc += c;
+        }
+        const unsigned v = vb | (unsigned)lo;
+        if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint16_t)v;
     }
 }
 

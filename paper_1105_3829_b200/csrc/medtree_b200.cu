@@ -331,6 +331,46 @@ static int run_colhist16_u16(SlabParams p, int B, cudaStream_t s) {
     return run_colhist16_u16_g<256, 1>(p, B, s);
 }
 
+static int run_colhist16_u16(SlabParams p, int B, cudaStream_t s);
+
+template <int T, int G, int M>
+static int run_colhist16s_u16_gm(SlabParams p, int B, cudaStream_t s) {
+    const int n = 2 * p.radius + 1, NCOL = T + 2 * p.radius;
+    const size_t smem = (size_t)colhist4_bytes(T, p.radius) + 16 * T * 2 + ((size_t)(n * T + 15) & ~(size_t)15) +
+                        (size_t)NCOL * n * 2;
+    if (smem > 220 * 1024) return run_colhist16_u16(p, B, s);  // sorted columns too large: two-phase kernel
+    auto kern = k_colhist16s_u16<T, G, M>;
+    if (int rc = set_smem(kern, smem)) return rc;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int bx = (p.W + T - 1) / T;
+    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm);
+    if (p.rows_per_cta < 2 * n) p.rows_per_cta = std::min(2 * n, p.row_end - p.row_begin);
+    dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
+    return launch(kern, grid, T, smem, s, p, "k_colhist16s_u16");
+}
+
+template <int T, int G>
+static int run_colhist16s_u16_g(SlabParams p, int B, cudaStream_t s) {
+    switch ((2 * p.radius + 1) % G) {
+        case 1: return run_colhist16s_u16_gm<T, G, (G > 1 ? 1 : 0)>(p, B, s);
+        case 3: return run_colhist16s_u16_gm<T, G, (G > 3 ? 3 : 0)>(p, B, s);
+        case 5: return run_colhist16s_u16_gm<T, G, (G > 5 ? 5 : 0)>(p, B, s);
+        case 7: return run_colhist16s_u16_gm<T, G, (G > 7 ? 7 : 0)>(p, B, s);
+        default: return run_colhist16s_u16_gm<T, G, 0>(p, B, s);
+    }
+}
+
+// widely spread 16-bit data; sorted columns need n <= 255 (u8 run starts)
+static int run_colhist16s_u16(SlabParams p, int B, cudaStream_t s) {
+    const int n = 2 * p.radius + 1;
+    if (8 * n <= 255) return run_colhist16s_u16_g<128, 8>(p, B, s);
+    if (4 * n <= 255) return run_colhist16s_u16_g<128, 4>(p, B, s);
+    if (2 * n <= 255) return run_colhist16s_u16_g<128, 2>(p, B, s);
+    return run_colhist16s_u16_g<128, 1>(p, B, s);
+}
+
 // 8-bit column-histogram gather kernels; the variant by radius (tools/probe.py
 // sweep on config 2): 16-bin records, one pixel per thread for
 // r <= 5, two for r <= 13; radix-4 records above.  MTB_CH_VAR forces one.
@@ -450,15 +490,16 @@ static int run(SlabParams p, int B, cudaStream_t s) {
         return run_colhist_u8(p, B, s);
     if (sizeof(P) == 1 && !wide && (force == "ctmf" || force.empty())) return run_ctmf_u8(p, B, s);
     // 16-bit: compact high bytes (sampled spread <= MTB_U16_SPREAD) -> the
-    // two-phase column-histogram kernel; widely spread -> sorted-column
-    // kernel for r <= MTB_U16_V2_MAX_R, the two-phase kernel above it
+    // two-phase column-histogram kernel; widely spread -> high-byte records +
+    // sorted columns for r <= MTB_U16_S_MAX_R, the two-phase kernel above it
     bool spread = false;
     if (sizeof(P) == 2 && force.empty()) {
         spread = wide_spread_u16(p, s);
-        if (n <= 255 && (!spread || p.radius > env_int("MTB_U16_V2_MAX_R", 15)))
-            return run_colhist16_u16(p, B, s);
+        if (n <= 255 && spread && p.radius <= env_int("MTB_U16_S_MAX_R", 16)) return run_colhist16s_u16(p, B, s);
+        if (n <= 255) return run_colhist16_u16(p, B, s);
     }
     if (sizeof(P) == 2 && n <= 255 && force == "colhist") return run_colhist16_u16(p, B, s);
+    if (sizeof(P) == 2 && n <= 255 && force == "colhist16s") return run_colhist16s_u16(p, B, s);
     if (sizeof(P) == 1 && !wide && force != "vert" && (n * n <= 255 || force == "vert2")) {
         constexpr int T = 128;
         const int bx = (p.W + T - 1) / T;

@@ -412,3 +412,27 @@ def test_colhist16_u16_batch_slab_and_lut(monkeypatch):
     lut = torch.from_numpy((np.arange(65536) & ~np.uint32(15)).astype(np.uint16)).cuda()
     q = mtb.rank_filter(torch.from_numpy(px).cuda(), 6, lut=lut).cpu().numpy()
     assert np.array_equal(q, ref & ~np.uint16(15))
+
+
+@pytest.mark.parametrize("kind", ["compact", "uniform"])
+def test_colhist16s_u16_sorted_columns(kind, monkeypatch):
+    """k_colhist16s_u16 (high byte from column records, low byte from sorted
+    columns) at radii covering every group size/tail, ragged tiles and
+    min / max / off-centre ranks; r=127 exceeds shared memory and must fall
+    back to the two-phase kernel, still exact."""
+    from paper_1105_3829_b200 import _lib
+
+    monkeypatch.setenv("MTB_KERNEL", "colhist16s")
+    rng = np.random.default_rng(77 if kind == "compact" else 78)
+    h, w = 150, 300
+    if kind == "compact":
+        px = (20000 + rng.normal(0, 250, (h, w))).clip(0, 65535).astype(np.uint16)
+    else:
+        px = rng.integers(0, 65536, (h, w)).astype(np.uint16)
+    for r in (1, 2, 3, 4, 7, 8, 15, 16, 31, 32, 63, 64, 127):
+        n = 2 * r + 1
+        for rank in (None, 1, n * n, (n * n) // 3 + 1):
+            out = mtb.rank_filter(torch.from_numpy(px).cuda(), r, rank=rank).cpu().numpy()
+            expect = "k_colhist16_u16" if r == 127 else "k_colhist16s_u16"
+            assert _lib.last_kernel() == expect, _lib.last_kernel()
+            assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (kind, r, rank)
