@@ -22,6 +22,14 @@ struct SlabParams {
     uint32_t rank;            // 1-based
     const void *lut;          // optional value map (2^d entries) or nullptr
     int32_t rows_per_cta;     // slab height handled by one CTA row
+    // streaming mode (host-buffer path, mtb_filter_host): the source rows
+    // arrive in chunks while the kernel runs and results leave in chunks.
+    // in_rows: number of global rows [0, *in_rows) already copied in;
+    // out_px[c]: output pixels of rows [c*out_chunk, (c+1)*out_chunk) done.
+    // Both nullptr outside streaming mode.
+    const unsigned int *in_rows;
+    unsigned int *out_px;
+    int32_t out_chunk;
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) {
@@ -31,6 +39,48 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) {
 template <typename P>
 __device__ __forceinline__ const P *src_row(const SlabParams &p, const P *base, int g) {
     return base + (int64_t)(g - p.src_row0) * p.src_pitch;
+}
+
+// ---- streaming mode helpers (no-ops unless p.in_rows / p.out_px are set)
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int *a) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+
+// spin (one thread) until source rows [0, need) have arrived
+__device__ __forceinline__ void stream_wait_rows_1(const SlabParams &p, int need) {
+    if (!p.in_rows) return;
+    need = min(need, p.H);
+    while ((int)ld_acquire(p.in_rows) < need) __nanosleep(256);
+}
+
+__device__ __forceinline__ void stream_wait_rows(const SlabParams &p, int need) {
+    if (!p.in_rows) return;
+    if (threadIdx.x == 0 && threadIdx.y == 0) stream_wait_rows_1(p, need);
+    __syncthreads();
+}
+
+// one thread reports output rows [y0, y1) x columns [x0, x1) as written
+__device__ __forceinline__ void stream_signal_1(const SlabParams &p, int y0, int y1, int x0, int x1) {
+    if (!p.out_px) return;
+    x1 = min(x1, p.W);
+    y1 = min(y1, p.row_end);
+    if (x1 <= x0 || y1 <= y0) return;
+    __threadfence();
+    const int C = p.out_chunk;
+    for (int c = (y0 - p.row_begin) / C; c * C + p.row_begin < y1; ++c) {
+        const int a = max(y0, p.row_begin + c * C), b = min(y1, p.row_begin + (c + 1) * C);
+        atomicAdd(p.out_px + c, (unsigned int)((b - a) * (x1 - x0)));
+    }
+}
+
+// CTA-wide: all threads' stores are done, then one thread signals
+__device__ __forceinline__ void stream_signal(const SlabParams &p, int y0, int y1, int x0, int x1) {
+    if (!p.out_px) return;
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) stream_signal_1(p, y0, y1, x0, x1);
 }
 
 }  // namespace mtb

@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
     if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
     const int y1 = min(y0 + p.rows_per_cta, p.row_end);
+    stream_wait_rows(p, y1 + r);
     const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
     uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
@@ -232,6 +233,7 @@ __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
             }
         }
     }
+    stream_signal(p, y0, y1, X0, X0 + g.TW);
 }
 
 }  // namespace mtb
@@ -396,6 +398,7 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
     uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
     const int x = X0 + tid;
+    stream_wait_rows(p, y1 + r);
     ch4_sweep<T, uint8_t>(
         p, src, rec, NCOL, X0, y0, y1 - 1, [](unsigned v) { return (int)v; },
         [&](int y) {
@@ -403,6 +406,7 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
             const unsigned v = ch4_select<G, M>(rec + tid, NCOL, n, k);
             if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
         });
+    stream_signal(p, y0, y1, X0, X0 + T);
 }
 
 // ---------------------------------------------------------------------------
@@ -435,6 +439,7 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
     const int64_t hp_img = (int64_t)(p.row_end - p.row_begin) * p.W;
     uint8_t *hpl = hplane + blockIdx.z * hp_img;
     const int x = X0 + tid;
+    stream_wait_rows(p, y1 + r);
     for (int i = tid; i < 256; i += T) {
         hfirst[i] = 1 << 30;
         hlast[i] = -1;
@@ -474,6 +479,7 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
                 *d = lut ? __ldg(lut + v) : (uint16_t)v;
             });
     }
+    stream_signal(p, y0, y1, X0, X0 + T);
 }
 
 }  // namespace mtb
@@ -512,6 +518,7 @@ __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
     const uint16_t *lut = static_cast<const uint16_t *>(p.lut);
     const int x = X0 + tid;
     const uint16_t *wcol = scol + tid * n;  // window column j of this thread = stripe column tid + j
+    stream_wait_rows(p, y1 + r);
 
     // records and sorted columns for row y0
     for (int i = tid; i < CH4_RECS * NCOL; i += T) rec[i] = 0;
@@ -618,6 +625,7 @@ __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
         const unsigned v = vb | (unsigned)lo;
         if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint16_t)v;
     }
+    stream_signal(p, y0, y1, X0, X0 + T);
 }
 
 }  // namespace mtb

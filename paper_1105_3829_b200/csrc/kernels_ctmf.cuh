@@ -327,6 +327,9 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
     const int A = ct_span_base(sx0);
     const bool aligned = ct_rows_aligned16(src, p.src_pitch);
     const int SPB = g.SPB;
+    if (p.in_rows) {  // streaming: this tile's source rows have arrived
+        if (lane == 0) stream_wait_rows_1(p, Y1 + r);
+    }
     __syncwarp();
 
     // ---- per-tile snapshot of every column's initial span (rows clamp(Y0-r ..
@@ -693,6 +696,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
         __syncwarp();
     }
     __syncwarp();
+    if (p.out_px && lane == 0) stream_signal_1(p, Y0, Y1, X0, X0 + g.TW);
     }  // tiles
 }
 

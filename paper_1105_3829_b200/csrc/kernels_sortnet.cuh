@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(128) k_sortnet(SlabParams p) {
     P *dst = static_cast<P *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const P *lut = static_cast<const P *>(p.lut);
     const int tid = threadIdx.x + 32 * threadIdx.y;
+    stream_wait_rows(p, Y0 + TY + R);
 
     // stage rows Y0-R .. Y0+TY+R-1, columns X0-R .. X0+TX+R-1 (clamped)
     for (int idx = tid; idx < SH * SW; idx += 128) {
@@ -202,6 +203,7 @@ __global__ void __launch_bounds__(128) k_sortnet(SlabParams p) {
             }
         }
     }
+    stream_signal(p, Y0, Y0 + TY, X0, X0 + TX);
 }
 
 }  // namespace mtb

@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(T) k_vert_u8(SlabParams p) {
     uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
     const int r = p.radius, H = p.H, W = p.W;
+    stream_wait_rows_1(p, y1 + r);
 
     for (int b = 0; b < 16; ++b) hc[b * T + tid] = 0;
     for (int b = 0; b < 256; ++b) hf[b * T + tid] = 0;
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(T) k_vert_u8(SlabParams p) {
         Lb = L;
         dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
     }
+    stream_signal_1(p, y0, y1, x, x + 1);
 }
 
 // 8-bit general path, v2: each warp stages the rows it needs (its 32
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
     if (y0 >= p.row_end || xw >= W) return;                       // warp-uniform
     const int y1 = min(y0 + p.rows_per_cta, p.row_end);
+    stream_wait_rows_1(p, y1 + r);
     const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
     uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
@@ -210,6 +213,7 @@ __global__ void __launch_bounds__(T) k_vert2_u8(SlabParams p) {
         Lb = L;
         if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
     }
+    stream_signal_1(p, y0, y1, x, x + 1);
 }
 
 // 16-bit: three-level hierarchy.  Levels 1+2 are the 8-bit hierarchy over
@@ -234,6 +238,7 @@ __global__ void __launch_bounds__(T) k_vert_u16(SlabParams p) {
     uint16_t *dst = static_cast<uint16_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint16_t *lut = static_cast<const uint16_t *>(p.lut);
     const int r = p.radius, H = p.H, W = p.W;
+    stream_wait_rows_1(p, y1 + r);
 
     for (int b = 0; b < 16; ++b) tc[b * T + tid] = 0;
     for (int b = 0; b < 256; ++b) tf[b * T + tid] = 0;
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(T) k_vert_u16(SlabParams p) {
         const unsigned v = ((unsigned)hb << 8) | (unsigned)lo;
         dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint16_t)v;
     }
+    stream_signal_1(p, y0, y1, x, x + 1);
 }
 
 }  // namespace mtb
@@ -373,6 +379,7 @@ __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
     if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
     const int y1 = min(y0 + p.rows_per_cta, p.row_end);
+    stream_wait_rows(p, y1 + r);
     const uint16_t *src = static_cast<const uint16_t *>(p.src) + blockIdx.z * p.src_img_stride;
     uint16_t *dst = static_cast<uint16_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint16_t *lut = static_cast<const uint16_t *>(p.lut);
@@ -514,6 +521,7 @@ __global__ void __launch_bounds__(T) k_vert2_u16(SlabParams p) {
         const unsigned v = ((unsigned)hb << 8) | (unsigned)lo;
         if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint16_t)v;
     }
+    stream_signal(p, y0, y1, X0, X0 + T);
 }
 
 }  // namespace mtb

@@ -25,8 +25,8 @@ namespace mtb {
 // Spread of the 16-bit value distribution: number of distinct high bytes
 // among a strided sample of the source rows.  Selects the 16-bit kernel:
 // a wide spread (high byte of the median changes often) favours the
-// sorted-column rebuild of k_vert2_u16; a compact one (changes rare)
-// favours the leaner k_vert_u16.  Both are exact.
+// sorted-column low byte of k_colhist16s_u16; a compact one the two-phase
+// k_colhist16_u16.  Both are exact.
 __global__ void k_highbyte_spread(const uint16_t *src, int64_t pitch, int rows, int W, int *out) {
     __shared__ int seen[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) seen[i] = 0;
@@ -450,7 +450,23 @@ static int run_sortnet(SlabParams p, int B, cudaStream_t s) {
 }
 
 // true when the 16-bit image's high bytes are widely spread (see k_highbyte_spread)
+// host-side decision supplied by the streaming host path (-1: none)
+static thread_local int g_spread_hint = -1;
+
+static int spread_distinct_host(const uint16_t *src, int64_t pitch, int rows, int W) {
+    bool seen[256] = {};
+    for (int i = 0; i < (1 << 14); ++i) {
+        const int y = (int)(((int64_t)i * 7919) % rows);
+        const int x = (int)(((int64_t)i * 104729) % W);
+        seen[src[(int64_t)y * pitch + x] >> 8] = true;
+    }
+    int d = 0;
+    for (int b = 0; b < 256; ++b) d += seen[b] ? 1 : 0;
+    return d;
+}
+
 static bool wide_spread_u16(const SlabParams &p, cudaStream_t s) {
+    if (g_spread_hint >= 0) return g_spread_hint > env_int("MTB_U16_SPREAD", 24);
     static int *d_out = nullptr;
     static int h_dev = -1;
     int dev = 0;
@@ -581,6 +597,7 @@ using namespace mtb;
 struct HostCtx {
     int dev = -1;
     void *dsrc = nullptr, *ddst = nullptr, *dlut = nullptr;
+    unsigned int *dflags = nullptr;  // [0] rows arrived, [1..] output pixels per chunk
     size_t cap = 0;
     cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
     static constexpr int KMAX = 16;
@@ -606,7 +623,8 @@ static int host_ctx(HostCtx *&ctx, size_t bytes) {
         if (!ok(cudaStreamCreateWithFlags(&ctx->sh, cudaStreamNonBlocking), "cudaStreamCreate") ||
             !ok(cudaStreamCreateWithFlags(&ctx->sc, cudaStreamNonBlocking), "cudaStreamCreate") ||
             !ok(cudaStreamCreateWithFlags(&ctx->sd, cudaStreamNonBlocking), "cudaStreamCreate") ||
-            !ok(cudaMalloc(&ctx->dlut, 65536 * 2), "cudaMalloc"))
+            !ok(cudaMalloc(&ctx->dlut, 65536 * 2), "cudaMalloc") ||
+            !ok(cudaMalloc(&ctx->dflags, 64 * sizeof(unsigned int)), "cudaMalloc"))
             return MTB_E_CUDA;
         for (int i = 0; i < HostCtx::KMAX; ++i)
             if (!ok(cudaEventCreateWithFlags(&ctx->eh[i], cudaEventDisableTiming), "cudaEventCreate") ||
@@ -627,6 +645,99 @@ static int host_ctx(HostCtx *&ctx, size_t bytes) {
     return MTB_OK;
 }
 
+// ---- streaming host path: ONE launch over the whole frame while the copies
+// run.  Source rows go host->device in chunks on the copy stream, each
+// followed by a stream memory write of "rows arrived" (executed by the copy
+// engine, after the data); CTAs spin on that counter before reading their
+// rows.  Each CTA/tile adds the pixels it finished to its output chunk's
+// counter; the device->host stream waits (stream memory wait) for a chunk's
+// full count and copies it out.  Copies in, filtering and copies out
+// overlap with no per-band relaunch cost.  Chunk copies end on 128-byte
+// line boundaries, so no L1 line ever mixes arrived and pending rows.
+typedef int (*write32_fn)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+
+static int host_stream(HostCtx *ctx, const void *src, void *dst, int bit_depth, int H, int W, int radius,
+                       int64_t rank, const void *lut, uint32_t flags) {
+    static write32_fn write32 = nullptr, wait32 = nullptr;
+    static int resolved = 0;
+    if (!resolved) {
+        void *fw = nullptr, *fwt = nullptr;
+        cudaDriverEntryPointQueryResult q1, q2;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fw, cudaEnableDefault, &q1) == cudaSuccess &&
+            cudaGetDriverEntryPoint("cuStreamWaitValue32", &fwt, cudaEnableDefault, &q2) == cudaSuccess &&
+            q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && fw && fwt) {
+            write32 = reinterpret_cast<write32_fn>(fw);
+            wait32 = reinterpret_cast<write32_fn>(fwt);
+            resolved = 1;
+        } else {
+            cudaGetLastError();
+            resolved = -1;
+        }
+    }
+    if (resolved < 0) return 1;  // caller falls back to the banded path
+    const size_t es = bit_depth == 8 ? 1 : 2;
+    const size_t row = (size_t)W * es, total = (size_t)H * row;
+    const int K = std::max(1, std::min(env_int("MTB_HOST_IN_CHUNKS", 4), H / 128));    // input chunks
+    const int KO = std::max(1, std::min(env_int("MTB_HOST_OUT_CHUNKS", 8), std::min(63, H / 128)));  // output
+    const int C = (H + KO - 1) / KO;                                  // rows per output chunk
+    const int nout = (H + C - 1) / C;
+    auto ok = [](cudaError_t e, const char *what) {
+        return e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    int rc = ok(cudaMemsetAsync(ctx->dflags, 0, (1 + nout) * sizeof(unsigned int), ctx->sh), "memset");
+    if (!rc && lut)
+        rc = ok(cudaMemcpyAsync(ctx->dlut, lut, ((size_t)1 << bit_depth) * es, cudaMemcpyHostToDevice, ctx->sh),
+                "H2D lut");
+    if (rc) return rc;
+    cudaEventRecord(ctx->eh[0], ctx->sh);
+    cudaStreamWaitEvent(ctx->sc, ctx->eh[0], 0);
+    cudaStreamWaitEvent(ctx->sd, ctx->eh[0], 0);
+    SlabParams p = make_params(ctx->dsrc, W, 0, H, ctx->ddst, W, H, W, 0, H, radius, rank,
+                               lut ? ctx->dlut : nullptr);
+    p.in_rows = ctx->dflags;
+    p.out_px = ctx->dflags + 1;
+    p.out_chunk = C;
+    if (bit_depth == 16)
+        g_spread_hint = spread_distinct_host(static_cast<const uint16_t *>(src), W, H, W);
+    (void)flags;
+    rc = bit_depth == 8 ? run<uint8_t>(p, 1, ctx->sc) : run<uint16_t>(p, 1, ctx->sc);
+    g_spread_hint = -1;
+    if (rc) {
+        // nothing waits on the flags yet: release any spinning CTAs, then fail
+        write32(ctx->sh, (unsigned long long)ctx->dflags, (unsigned int)H, 0);
+        cudaStreamSynchronize(ctx->sc);
+        cudaStreamSynchronize(ctx->sh);
+        return rc;
+    }
+    const char *s8 = static_cast<const char *>(src);
+    size_t b = 0;
+    for (int i = 0; i < K && !rc; ++i) {
+        const int R = (int)((int64_t)H * (i + 1) / K);
+        const size_t e = i == K - 1 ? total : std::min(total, ((size_t)R * row + 127) & ~(size_t)127);
+        if (e > b) {
+            rc = ok(cudaMemcpyAsync(static_cast<char *>(ctx->dsrc) + b, s8 + b, e - b, cudaMemcpyHostToDevice, ctx->sh),
+                    "H2D");
+            b = e;
+        }
+        if (!rc && write32(ctx->sh, (unsigned long long)ctx->dflags, (unsigned int)R, 0) != 0)
+            rc = fail(MTB_E_CUDA, "cuStreamWriteValue32 failed");
+    }
+    char *d8 = static_cast<char *>(dst);
+    for (int c = 0; c < nout && !rc; ++c) {
+        const int a = c * C, e = std::min(H, a + C);
+        if (wait32(ctx->sd, (unsigned long long)(ctx->dflags + 1 + c), (unsigned int)((e - a) * W), 0) != 0)
+            rc = fail(MTB_E_CUDA, "cuStreamWaitValue32 failed");
+        else
+            rc = ok(cudaMemcpyAsync(d8 + (size_t)a * row, static_cast<char *>(ctx->ddst) + (size_t)a * row,
+                                    (size_t)(e - a) * row, cudaMemcpyDeviceToHost, ctx->sd), "D2H");
+    }
+    if (rc) write32(ctx->sh, (unsigned long long)ctx->dflags, (unsigned int)H, 0);  // never leave CTAs spinning
+    const int r1 = ok(cudaStreamSynchronize(ctx->sd), "cudaStreamSynchronize");
+    const int r2 = ok(cudaStreamSynchronize(ctx->sc), "cudaStreamSynchronize");
+    const int r3 = ok(cudaStreamSynchronize(ctx->sh), "cudaStreamSynchronize");
+    return rc ? rc : (r1 ? r1 : (r2 ? r2 : r3));
+}
+
 static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W, int radius, int64_t rank,
                          const void *lut, uint32_t flags) {
     std::lock_guard<std::mutex> lock(g_host_mu);
@@ -634,6 +745,16 @@ static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W
     const size_t row = (size_t)W * es;
     HostCtx *ctx = nullptr;
     if (int rc = host_ctx(ctx, (size_t)H * row)) return rc;
+    // streaming (one launch, copies overlapped) for compute-heavy radii;
+    // row bands below, where the stream-op latencies outweigh the overlap
+    // (tools/e2e_probe.py: equal at r = 15, streaming -12% at r = 31, +10%
+    // at r <= 3).  MTB_HOST_STREAM=0/1 forces; lob has no streaming support.
+    const int stream_mode = env_int("MTB_HOST_STREAM", -1);
+    const bool want_stream = stream_mode < 0 ? radius >= 12 : stream_mode != 0;
+    if (want_stream && std::string(forced_kernel()) != "lob") {
+        const int rs = host_stream(ctx, src, dst, bit_depth, H, W, radius, rank, lut, flags);
+        if (rs != 1) return rs;
+    }
     // bands: enough rows that per-band launch and halo overheads stay small
     // (measured on config 2, tools/e2e_probe.py: 4 bands of 1024 rows for
     // r <= 31, 2 for r = 63 -- shorter bands re-pay the n-row column build)

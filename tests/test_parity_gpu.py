@@ -202,14 +202,19 @@ def test_host_buffer_entry_point(rng):
                           O.iot_filter(px16, 7, max_error=16))
 
 
-@pytest.mark.parametrize("bits,r,bands", [(8, 2, None), (8, 9, "3"), (8, 40, None), (16, 5, None),
-                                          (16, 20, "5"), (8, 3, "16")])
-def test_host_pipeline_bands(bits, r, bands, monkeypatch):
-    """mtb_filter_host cuts the frame into row bands whose copies overlap the
-    filtering; results must not depend on the band count (pinned and
+@pytest.mark.parametrize("bits,r,bands,stream", [(8, 2, None, None), (8, 9, "3", None), (8, 40, None, None),
+                                                 (16, 5, None, None), (16, 20, "5", None), (8, 3, "16", None),
+                                                 (8, 2, None, "1"), (8, 40, None, "0"), (8, 70, None, "1"),
+                                                 (16, 3, None, "1"), (16, 6, None, "1"), (8, 1, None, "1")])
+def test_host_pipeline_bands(bits, r, bands, stream, monkeypatch):
+    """mtb_filter_host overlaps copies with filtering -- row bands, or one
+    streaming launch whose CTAs wait for their rows (stream memory ops);
+    results must not depend on the mode or the band count (pinned and
     pageable buffers, caller-provided out)."""
     if bands:
         monkeypatch.setenv("MTB_HOST_BANDS", bands)
+    if stream:
+        monkeypatch.setenv("MTB_HOST_STREAM", stream)
     rng = np.random.default_rng(bits * 100 + r)
     H, W = 1300, 333
     if bits == 8:
