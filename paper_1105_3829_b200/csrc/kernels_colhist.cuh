@@ -383,7 +383,9 @@ __device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uin
     }
 }
 
-template <int T, int G, int M>
+// STREAM: the streaming host path's instantiation (row waits / chunk
+// signals); the plain one has no hooks (they cost ~2% here when inlined).
+template <int T, int G, int M, bool STREAM>
 __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
@@ -398,7 +400,7 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
     uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
     const int x = X0 + tid;
-    stream_wait_rows(p, y1 + r);
+    if (STREAM) stream_wait_rows(p, y1 + r);
     ch4_sweep<T, uint8_t>(
         p, src, rec, NCOL, X0, y0, y1 - 1, [](unsigned v) { return (int)v; },
         [&](int y) {
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
             const unsigned v = ch4_select<G, M>(rec + tid, NCOL, n, k);
             if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
         });
-    stream_signal(p, y0, y1, X0, X0 + T);
+    if (STREAM) stream_signal(p, y0, y1, X0, X0 + T);
 }
 
 // ---------------------------------------------------------------------------

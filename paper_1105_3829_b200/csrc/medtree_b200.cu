@@ -254,7 +254,7 @@ static int run_colhist_u8_ts(SlabParams p, int B, cudaStream_t s, const char *na
 template <int T, int G, int M>
 static int run_colhist4_u8_gm(SlabParams p, int B, cudaStream_t s, const char *name) {
     const size_t smem = (size_t)colhist4_bytes(T, p.radius);
-    auto kern = k_colhist4_u8<T, G, M>;
+    auto kern = p.in_rows ? k_colhist4_u8<T, G, M, true> : k_colhist4_u8<T, G, M, false>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
