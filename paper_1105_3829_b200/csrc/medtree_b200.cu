@@ -10,13 +10,9 @@
 #include <cstring>
 #include <string>
 
-#include "../../include/medtree_b200.h"
-#include "common.cuh"
+#include "host.h"
 #include "kernels_vert.cuh"
-#include "kernels_ctmf.cuh"
-#include "kernels_lob.cuh"
 #include "kernels_sortnet.cuh"
-#include "kernels_colhist.cuh"
 #include "kernels_select.cuh"
 #include <cstdlib>
 
@@ -45,16 +41,16 @@ __global__ void k_highbyte_spread(const uint16_t *src, int64_t pitch, int rows, 
     }
 }
 
-static thread_local std::string g_err;
-static thread_local const char *g_kernel = "";
-static std::atomic<uint64_t> g_launches{0};
+thread_local std::string g_err;
+thread_local const char *g_kernel = "";
+std::atomic<uint64_t> g_launches{0};
 
-static int fail(int code, const std::string &msg) {
+int fail(int code, const std::string &msg) {
     g_err = msg;
     return code;
 }
 
-static int sm_count() {
+int sm_count() {
     static int cached[64] = {0};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 148;
@@ -98,28 +94,7 @@ static int validate(const SlabParams &p, int B) {
     return MTB_OK;
 }
 
-// Opt in to the dynamic shared memory a launch needs (static __shared__
-// of the kernel counts against the default 48 KB too, so always set it).
-template <typename K>
-static int set_smem(K kernel, size_t smem) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    return MTB_OK;
-}
-
-template <typename K>
-static int launch(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                  const SlabParams &p, const char *name) {
-    if (int rc = set_smem(kernel, smem)) return rc;
-    kernel<<<grid, block, smem, s>>>(p);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
-    g_kernel = name;
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return MTB_OK;
-}
-
-static int rows_per_cta(const SlabParams &p, int blocks_x, int B, int ctas_per_sm) {
+int rows_per_cta(const SlabParams &p, int blocks_x, int B, int ctas_per_sm) {
     const int rows = p.row_end - p.row_begin;
     const int64_t target = (int64_t)sm_count() * ctas_per_sm * 2;
     int64_t slabs = (target + (int64_t)blocks_x * B - 1) / ((int64_t)blocks_x * B);
@@ -133,20 +108,20 @@ static int rows_per_cta(const SlabParams &p, int blocks_x, int B, int ctas_per_s
     return rpc < 1 ? 1 : rpc;
 }
 
-static int env_int(const char *name, int dflt) {
+int env_int(const char *name, int dflt) {
     const char *v = getenv(name);
     return (v && *v) ? atoi(v) : dflt;
 }
 
 // kernel choice: MTB_KERNEL=vert|ctmf forces a family (testing/tuning)
-static const char *forced_kernel() {
+const char *forced_kernel() {
     const char *v = getenv("MTB_KERNEL");
     return v ? v : "";
 }
 
 // keep freed stream-ordered allocations in the device's default pool so the
 // per-launch workspace does not go back to the driver at every sync
-static void keep_pool_memory() {
+void keep_pool_memory() {
     static int done[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -159,262 +134,10 @@ static void keep_pool_memory() {
     done[dev] = 1;
 }
 
-template <int S>
-static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
-    const CtmfGeom g = ctmf_geom(S, p.radius);
-    const int rows = p.row_end - p.row_begin;
-    const int tiles_x = (p.W + g.TW - 1) / g.TW;
-    const size_t smem = (size_t)g.warp_bytes * CT_WARPS;
-    auto kern = k_ctmf_u8<S>;
-    if (int rc = set_smem(kern, smem)) return rc;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CT_WARPS * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-    // Tile height: near max(24, n/3) rows, adjusted so that the tiles divide
-    // evenly over the resident warps (k full rounds, no ragged last round).
-    const int n = 2 * p.radius + 1;
-    const int64_t warps = (int64_t)sm_count() * per_sm * CT_WARPS;
-    const double per_stripe = (double)warps / ((double)tiles_x * B);  // warps per column stripe
-    const int target = env_int("MTB_CT_MIN_TH", n / 3 > 24 ? n / 3 : 24);
-    int th;
-    if (per_stripe >= 1.0) {
-        int k = (int)((double)rows / (target * per_stripe) + 0.5);
-        if (k < 1) k = 1;
-        th = (int)((rows + (int64_t)(k * per_stripe) - 1) / (int64_t)(k * per_stripe));
-    } else {
-        th = target;
-    }
-    th = env_int("MTB_CT_TH", th);
-    if (th < 8) th = 8 < rows ? 8 : rows;
-    if (th > rows) th = rows;
-    p.rows_per_cta = th;
-    const int tiles_y = (rows + th - 1) / th;
-    const int tiles = tiles_x * tiles_y;
-    // persistent grid: as many CTAs as are resident at once (per image)
-    int ctas = (tiles + CT_WARPS - 1) / CT_WARPS;
-    const int resident = (int)((sm_count() * per_sm + B - 1) / B);
-    if (env_int("MTB_CT_PERSIST", 1) && ctas > resident) ctas = resident > 0 ? resident : 1;
-    dim3 grid(ctas, 1, B);
-    // per-tile column snapshots (stream-ordered pool allocation, kept cached)
-    uint8_t *snap = nullptr;
-    const size_t snap_bytes = (size_t)ctas * CT_WARPS * B * ((((size_t)g.NCP * 18 + 15) & ~(size_t)15) + (size_t)g.NCP * 256);
-    if (env_int("MTB_CT_SNAP", 1)) {
-        keep_pool_memory();
-        if (cudaMallocAsync(reinterpret_cast<void **>(&snap), snap_bytes, s) != cudaSuccess) {
-            cudaGetLastError();
-            snap = nullptr;  // fall back to rescanning the spans
-        }
-    }
-    kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y, snap, env_int("MTB_CT_SCAN2", 1));
-    cudaError_t e = cudaGetLastError();
-    if (snap) cudaFreeAsync(snap, s);
-    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_ctmf_u8: ") + cudaGetErrorString(e));
-    g_kernel = S == 8 ? "k_ctmf_u8<8>" : "k_ctmf_u8<16>";
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return MTB_OK;
-}
 
-template <int T, int S, int G, int M>
-static int run_colhist_u8_gm(SlabParams p, int B, cudaStream_t s, const char *name) {
-    const ColhistGeom g = colhist_geom(T, S, p.radius);
-    const size_t smem = (size_t)g.bytes;
-    auto kern = k_colhist_u8<T, S, G, M>;
-    if (int rc = set_smem(kern, smem)) return rc;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int bx = (p.W + g.TW - 1) / g.TW;
-    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm);
-    dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
-    return launch(kern, grid, T, smem, s, p, name);
-}
 
-// n is odd, so the tail n mod G is odd for G > 1 and 0 for G = 1
-template <int T, int S, int G>
-static int run_colhist_u8_g(SlabParams p, int B, cudaStream_t s, const char *name) {
-    switch ((2 * p.radius + 1) % G) {
-        case 1: return run_colhist_u8_gm<T, S, G, (G > 1 ? 1 : 0)>(p, B, s, name);
-        case 3: return run_colhist_u8_gm<T, S, G, (G > 3 ? 3 : 0)>(p, B, s, name);
-        case 5: return run_colhist_u8_gm<T, S, G, (G > 5 ? 5 : 0)>(p, B, s, name);
-        case 7: return run_colhist_u8_gm<T, S, G, (G > 7 ? 7 : 0)>(p, B, s, name);
-        default: return run_colhist_u8_gm<T, S, G, 0>(p, B, s, name);
-    }
-}
 
-// carry-free group size: G columns of counts <= n sum to <= 255 per u8 lane
-template <int T, int S>
-static int run_colhist_u8_ts(SlabParams p, int B, cudaStream_t s, const char *name) {
-    const int n = 2 * p.radius + 1;
-    if (8 * n <= 255) return run_colhist_u8_g<T, S, 8>(p, B, s, name);
-    if (4 * n <= 255) return run_colhist_u8_g<T, S, 4>(p, B, s, name);
-    if (2 * n <= 255) return run_colhist_u8_g<T, S, 2>(p, B, s, name);
-    return run_colhist_u8_g<T, S, 1>(p, B, s, name);
-}
 
-template <int T, int G, int M>
-static int run_colhist4_u8_gm(SlabParams p, int B, cudaStream_t s, const char *name) {
-    const size_t smem = (size_t)colhist4_bytes(T, p.radius);
-    auto kern = p.in_rows ? k_colhist4_u8<T, G, M, true> : k_colhist4_u8<T, G, M, false>;
-    if (int rc = set_smem(kern, smem)) return rc;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int bx = (p.W + T - 1) / T;
-    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm);
-    dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
-    return launch(kern, grid, T, smem, s, p, name);
-}
-
-template <int T, int G>
-static int run_colhist4_u8_g(SlabParams p, int B, cudaStream_t s, const char *name) {
-    switch ((2 * p.radius + 1) % G) {
-        case 1: return run_colhist4_u8_gm<T, G, (G > 1 ? 1 : 0)>(p, B, s, name);
-        case 3: return run_colhist4_u8_gm<T, G, (G > 3 ? 3 : 0)>(p, B, s, name);
-        case 5: return run_colhist4_u8_gm<T, G, (G > 5 ? 5 : 0)>(p, B, s, name);
-        case 7: return run_colhist4_u8_gm<T, G, (G > 7 ? 7 : 0)>(p, B, s, name);
-        default: return run_colhist4_u8_gm<T, G, 0>(p, B, s, name);
-    }
-}
-
-template <int T>
-static int run_colhist4_u8(SlabParams p, int B, cudaStream_t s, const char *name) {
-    const int n = 2 * p.radius + 1;
-    if (8 * n <= 255) return run_colhist4_u8_g<T, 8>(p, B, s, name);
-    if (4 * n <= 255) return run_colhist4_u8_g<T, 4>(p, B, s, name);
-    if (2 * n <= 255) return run_colhist4_u8_g<T, 2>(p, B, s, name);
-    return run_colhist4_u8_g<T, 1>(p, B, s, name);
-}
-
-template <int T, int G, int M>
-static int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s) {
-    const size_t smem = (size_t)colhist4_bytes(T, p.radius) + 2 * 256 * sizeof(int);
-    auto kern = k_colhist16_u16<T, G, M>;
-    if (int rc = set_smem(kern, smem)) return rc;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int bx = (p.W + T - 1) / T;
-    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm);
-    dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
-    // per-pixel high-byte plane (stream-ordered pool allocation, kept cached)
-    uint8_t *hplane = nullptr;
-    keep_pool_memory();
-    const size_t hbytes = (size_t)(p.row_end - p.row_begin) * p.W * B;
-    if (cudaMallocAsync(reinterpret_cast<void **>(&hplane), hbytes, s) != cudaSuccess)
-        return fail(MTB_E_CUDA, "k_colhist16_u16: scratch allocation failed");
-    if (int rc = set_smem(kern, smem)) return rc;
-    kern<<<grid, T, smem, s>>>(p, hplane);
-    cudaError_t e = cudaGetLastError();
-    cudaFreeAsync(hplane, s);
-    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_colhist16_u16: ") + cudaGetErrorString(e));
-    g_kernel = "k_colhist16_u16";
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return MTB_OK;
-}
-
-template <int T, int G>
-static int run_colhist16_u16_g(SlabParams p, int B, cudaStream_t s) {
-    switch ((2 * p.radius + 1) % G) {
-        case 1: return run_colhist16_u16_gm<T, G, (G > 1 ? 1 : 0)>(p, B, s);
-        case 3: return run_colhist16_u16_gm<T, G, (G > 3 ? 3 : 0)>(p, B, s);
-        case 5: return run_colhist16_u16_gm<T, G, (G > 5 ? 5 : 0)>(p, B, s);
-        case 7: return run_colhist16_u16_gm<T, G, (G > 7 ? 7 : 0)>(p, B, s);
-        default: return run_colhist16_u16_gm<T, G, 0>(p, B, s);
-    }
-}
-
-static int run_colhist16_u16(SlabParams p, int B, cudaStream_t s) {
-    const int n = 2 * p.radius + 1;
-    if (8 * n <= 255) return run_colhist16_u16_g<256, 8>(p, B, s);
-    if (4 * n <= 255) return run_colhist16_u16_g<256, 4>(p, B, s);
-    if (2 * n <= 255) return run_colhist16_u16_g<256, 2>(p, B, s);
-    return run_colhist16_u16_g<256, 1>(p, B, s);
-}
-
-static int run_colhist16_u16(SlabParams p, int B, cudaStream_t s);
-
-template <int T, int G, int M>
-static int run_colhist16s_u16_gm(SlabParams p, int B, cudaStream_t s) {
-    const int n = 2 * p.radius + 1, NCOL = T + 2 * p.radius;
-    const size_t smem = (size_t)colhist4_bytes(T, p.radius) + 16 * T * 2 + ((size_t)(n * T + 15) & ~(size_t)15) +
-                        (size_t)NCOL * n * 2;
-    if (smem > 220 * 1024) return run_colhist16_u16(p, B, s);  // sorted columns too large: two-phase kernel
-    auto kern = k_colhist16s_u16<T, G, M>;
-    if (int rc = set_smem(kern, smem)) return rc;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int bx = (p.W + T - 1) / T;
-    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm);
-    if (p.rows_per_cta < 2 * n) p.rows_per_cta = std::min(2 * n, p.row_end - p.row_begin);
-    dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
-    return launch(kern, grid, T, smem, s, p, "k_colhist16s_u16");
-}
-
-template <int T, int G>
-static int run_colhist16s_u16_g(SlabParams p, int B, cudaStream_t s) {
-    switch ((2 * p.radius + 1) % G) {
-        case 1: return run_colhist16s_u16_gm<T, G, (G > 1 ? 1 : 0)>(p, B, s);
-        case 3: return run_colhist16s_u16_gm<T, G, (G > 3 ? 3 : 0)>(p, B, s);
-        case 5: return run_colhist16s_u16_gm<T, G, (G > 5 ? 5 : 0)>(p, B, s);
-        case 7: return run_colhist16s_u16_gm<T, G, (G > 7 ? 7 : 0)>(p, B, s);
-        default: return run_colhist16s_u16_gm<T, G, 0>(p, B, s);
-    }
-}
-
-// widely spread 16-bit data; sorted columns need n <= 255 (u8 run starts)
-static int run_colhist16s_u16(SlabParams p, int B, cudaStream_t s) {
-    const int n = 2 * p.radius + 1;
-    if (8 * n <= 255) return run_colhist16s_u16_g<128, 8>(p, B, s);
-    if (4 * n <= 255) return run_colhist16s_u16_g<128, 4>(p, B, s);
-    if (2 * n <= 255) return run_colhist16s_u16_g<128, 2>(p, B, s);
-    return run_colhist16s_u16_g<128, 1>(p, B, s);
-}
-
-// 8-bit column-histogram gather kernels; the variant by radius (tools/probe.py
-// sweep on config 2): 16-bin records, one pixel per thread for
-// r <= 5, two for r <= 13; radix-4 records above.  MTB_CH_VAR forces one.
-static int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
-    int var = env_int("MTB_CH_VAR", -1);
-    if (var < 0) var = p.radius <= 5 ? 0 : (p.radius <= 13 ? 2 : 12);
-    switch (var) {
-        case 0: return run_colhist_u8_ts<128, 1>(p, B, s, "k_colhist_u8<128,1>");
-        case 2: return run_colhist_u8_ts<128, 2>(p, B, s, "k_colhist_u8<128,2>");
-        default: return run_colhist4_u8<256>(p, B, s, "k_colhist4_u8<256>");
-    }
-}
-
-static int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
-    return env_int("MTB_CT_S", 8) == 8 ? run_ctmf_u8_s<8>(p, B, s) : run_ctmf_u8_s<16>(p, B, s);
-}
-
-template <int L>
-static int run_lob_u8_l(SlabParams p, int B, cudaStream_t s) {
-    const LobGeom g = lob_geom(L, p.radius);
-    const int rows = p.row_end - p.row_begin;
-    const int tiles_x = (p.W + g.TW - 1) / g.TW;
-    const int per_sm = (220 * 1024) / g.warp_bytes;
-    const int want = sm_count() * (per_sm < 1 ? 1 : per_sm) * 3;
-    int ty = (want + tiles_x * B - 1) / (tiles_x * B);
-    int th = (rows + ty - 1) / ty;
-    const int min_th = env_int("MTB_LOB_MIN_TH", 32);
-    if (th < min_th) th = min_th;
-    th = env_int("MTB_LOB_TH", th);
-    if (th > rows) th = rows;
-    if (th < 1) th = 1;
-    p.rows_per_cta = th;
-    const int tiles_y = (rows + th - 1) / th;
-    dim3 grid(tiles_x * tiles_y, 1, B);
-    const size_t smem = (size_t)g.warp_bytes;
-    auto kern = k_lob_u8<L>;
-    if (int rc = set_smem(kern, smem)) return rc;
-    kern<<<grid, 32, smem, s>>>(p, tiles_x, tiles_y);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_lob_u8: ") + cudaGetErrorString(e));
-    g_kernel = L == 32 ? "k_lob_u8<32>" : "k_lob_u8<64>";
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return MTB_OK;
-}
 
 template <int N, int K, int RT, typename P>
 static int run_sortnet_n(SlabParams p, int B, cudaStream_t s, const char *name) {
@@ -500,7 +223,7 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     if ((force.empty() || force == "sortnet") && sortnet_applies<P>(p) &&
         (sizeof(P) == 2 || p.radius <= 2 || force == "sortnet"))
         return run_sortnet<P>(p, B, s);
-    if (sizeof(P) == 1 && p.radius <= 63 && force == "lob") return run_lob_u8_l<32>(p, B, s);
+    if (sizeof(P) == 1 && p.radius <= 63 && force == "lob") return run_lob_u8_32(p, B, s);
     if (sizeof(P) == 1 && n <= 255 &&
         (force == "colhist" || (force.empty() && p.radius <= env_int("MTB_CH_MAX_R", 40))))
         return run_colhist_u8(p, B, s);

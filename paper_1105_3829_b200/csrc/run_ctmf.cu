@@ -1,0 +1,98 @@
+// run_ctmf.cu -- launchers of the CTMF tile kernel (kernels_ctmf.cuh) and of
+// the rejected lanes-own-bins kernel (kernels_lob.cuh).
+#include "host.h"
+#include "kernels_ctmf.cuh"
+#include "kernels_lob.cuh"
+
+namespace mtb {
+
+template <int S>
+static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
+    const CtmfGeom g = ctmf_geom(S, p.radius);
+    const int rows = p.row_end - p.row_begin;
+    const int tiles_x = (p.W + g.TW - 1) / g.TW;
+    const size_t smem = (size_t)g.warp_bytes * CT_WARPS;
+    auto kern = k_ctmf_u8<S>;
+    if (int rc = set_smem(kern, smem)) return rc;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CT_WARPS * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    // Tile height: near max(24, n/3) rows, adjusted so that the tiles divide
+    // evenly over the resident warps (k full rounds, no ragged last round).
+    const int n = 2 * p.radius + 1;
+    const int64_t warps = (int64_t)sm_count() * per_sm * CT_WARPS;
+    const double per_stripe = (double)warps / ((double)tiles_x * B);  // warps per column stripe
+    const int target = env_int("MTB_CT_MIN_TH", n / 3 > 24 ? n / 3 : 24);
+    int th;
+    if (per_stripe >= 1.0) {
+        int k = (int)((double)rows / (target * per_stripe) + 0.5);
+        if (k < 1) k = 1;
+        th = (int)((rows + (int64_t)(k * per_stripe) - 1) / (int64_t)(k * per_stripe));
+    } else {
+        th = target;
+    }
+    th = env_int("MTB_CT_TH", th);
+    if (th < 8) th = 8 < rows ? 8 : rows;
+    if (th > rows) th = rows;
+    p.rows_per_cta = th;
+    const int tiles_y = (rows + th - 1) / th;
+    const int tiles = tiles_x * tiles_y;
+    // persistent grid: as many CTAs as are resident at once (per image)
+    int ctas = (tiles + CT_WARPS - 1) / CT_WARPS;
+    const int resident = (int)((sm_count() * per_sm + B - 1) / B);
+    if (env_int("MTB_CT_PERSIST", 1) && ctas > resident) ctas = resident > 0 ? resident : 1;
+    dim3 grid(ctas, 1, B);
+    // per-tile column snapshots (stream-ordered pool allocation, kept cached)
+    uint8_t *snap = nullptr;
+    const size_t snap_bytes = (size_t)ctas * CT_WARPS * B * ((((size_t)g.NCP * 18 + 15) & ~(size_t)15) + (size_t)g.NCP * 256);
+    if (env_int("MTB_CT_SNAP", 1)) {
+        keep_pool_memory();
+        if (cudaMallocAsync(reinterpret_cast<void **>(&snap), snap_bytes, s) != cudaSuccess) {
+            cudaGetLastError();
+            snap = nullptr;  // fall back to rescanning the spans
+        }
+    }
+    kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y, snap, env_int("MTB_CT_SCAN2", 1));
+    cudaError_t e = cudaGetLastError();
+    if (snap) cudaFreeAsync(snap, s);
+    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_ctmf_u8: ") + cudaGetErrorString(e));
+    g_kernel = S == 8 ? "k_ctmf_u8<8>" : "k_ctmf_u8<16>";
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return MTB_OK;
+}
+
+int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
+    return env_int("MTB_CT_S", 8) == 8 ? run_ctmf_u8_s<8>(p, B, s) : run_ctmf_u8_s<16>(p, B, s);
+}
+
+template <int L>
+static int run_lob_u8_l(SlabParams p, int B, cudaStream_t s) {
+    const LobGeom g = lob_geom(L, p.radius);
+    const int rows = p.row_end - p.row_begin;
+    const int tiles_x = (p.W + g.TW - 1) / g.TW;
+    const int per_sm = (220 * 1024) / g.warp_bytes;
+    const int want = sm_count() * (per_sm < 1 ? 1 : per_sm) * 3;
+    int ty = (want + tiles_x * B - 1) / (tiles_x * B);
+    int th = (rows + ty - 1) / ty;
+    const int min_th = env_int("MTB_LOB_MIN_TH", 32);
+    if (th < min_th) th = min_th;
+    th = env_int("MTB_LOB_TH", th);
+    if (th > rows) th = rows;
+    if (th < 1) th = 1;
+    p.rows_per_cta = th;
+    const int tiles_y = (rows + th - 1) / th;
+    dim3 grid(tiles_x * tiles_y, 1, B);
+    const size_t smem = (size_t)g.warp_bytes;
+    auto kern = k_lob_u8<L>;
+    if (int rc = set_smem(kern, smem)) return rc;
+    kern<<<grid, 32, smem, s>>>(p, tiles_x, tiles_y);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_lob_u8: ") + cudaGetErrorString(e));
+    g_kernel = L == 32 ? "k_lob_u8<32>" : "k_lob_u8<64>";
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return MTB_OK;
+}
+
+int run_lob_u8_32(SlabParams p, int B, cudaStream_t s) { return run_lob_u8_l<32>(p, B, s); }
+
+}  // namespace mtb
