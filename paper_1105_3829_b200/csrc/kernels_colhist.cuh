@@ -631,3 +631,168 @@ __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
 }
 
 }  // namespace mtb
+
+namespace mtb {
+
+// ---------------------------------------------------------------------------
+// Radix-4 records with PAIR records for the upper levels (8-bit, mid r).
+// The gathers of k_colhist4_u8 are bound by shared-memory wavefronts (one
+// word per window column and level).  Here the CTA also keeps, for levels
+// 0-2 (21 record rows), the sums of column pairs (2k, 2k+1): a window of n
+// (odd) columns is (n-1)/2 pairs plus one single column -- the single is
+// the first column when the window starts odd, the last when it starts
+// even, so the pair run always starts at (s+1)/2 -- about half the words
+// for those levels (2.5n words per pixel instead of 4n).  Pair counts are
+// at most 2n, so G/2 pairs per carry-free group.  Row updates add the
+// pair changes with shared-memory atomics (adjacent columns belong to
+// adjacent threads); counts never go below zero, so a per-byte decrement
+// never borrows across bytes.
+// PL = number of levels with pair records (3: levels 0-2, 21 record rows;
+// 2: levels 0-1, 5 rows) -- fewer when shared memory would otherwise drop
+// the CTA below two per SM.
+__host__ __device__ constexpr int ch4p_recs(int PL) { return PL >= 3 ? 21 : (PL == 2 ? 5 : 1); }
+
+__host__ __device__ inline int colhist4p_ncolp(int T, int r) { return (T + 2 * r + 1) & ~1; }
+__host__ __device__ inline int colhist4p_bytes(int T, int r, int PL) {
+    const int ncp = colhist4p_ncolp(T, r);
+    return (CH4_RECS * ncp + ch4p_recs(PL) * (ncp / 2)) * 4;
+}
+
+// window of one level from pair records (np = (n-1)/2 pairs from kp) plus
+// the single column cs; GP pairs per carry-free group, runtime tail
+template <int GP>
+__device__ __forceinline__ void ch4p_gather(const uint32_t *pr, const uint32_t *sr, int kp, int cs, int np,
+                                            uint32_t &w0, uint32_t &w1) {
+    const uint32_t sv = sr[cs];
+    w0 = __byte_perm(sv, 0, 0x4140);
+    w1 = __byte_perm(sv, 0, 0x4342);
+    const uint32_t *rp = pr + kp;
+    const int full = np - np % GP;
+    int j = 0;
+    for (; j < full; j += GP) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int q = 0; q < GP; q += 2) t += rp[j + q] + (q + 1 < GP ? rp[j + q + 1] : 0u);
+        w0 += __byte_perm(t, 0, 0x4140);
+        w1 += __byte_perm(t, 0, 0x4342);
+    }
+    if (j < np) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int q = 0; q < GP - 1; ++q)
+            if (j + q < np) t += rp[j + q];
+        w0 += __byte_perm(t, 0, 0x4140);
+        w1 += __byte_perm(t, 0, 0x4342);
+    }
+}
+
+template <int T, int G, int M, int PL, bool STREAM>
+__global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
+    constexpr int GP = G / 2;
+    constexpr int PR = ch4p_recs(PL);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x;
+    const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
+    const int NCOL = T + 2 * r, NCP = colhist4p_ncolp(T, r), NPR = NCP / 2;
+    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCP] singles
+    uint32_t *prs = rec + CH4_RECS * NCP;                     // [PR][NPR] pairs
+    uint8_t *recb = smem_raw;
+    const int X0 = blockIdx.x * T;
+    const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
+    if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
+    const int y1 = min(y0 + p.rows_per_cta, p.row_end);
+    if (STREAM) stream_wait_rows(p, y1 + r);
+    const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
+    uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
+    const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
+    const int x = X0 + tid;
+
+    for (int i = tid; i < CH4_RECS * NCP; i += T) rec[i] = 0;
+    __syncthreads();
+    for (int c = tid; c < NCOL; c += T) {
+        const int gx = clampi(X0 - r + c, 0, W - 1);
+        for (int j = -r; j <= r; ++j) ch4_bump(recb, NCP, c, __ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx), 1);
+    }
+    __syncthreads();
+    for (int i = tid; i < PR * NPR; i += T) {
+        const int row = i / NPR, k = i - row * NPR;
+        prs[i] = rec[row * NCP + 2 * k] + rec[row * NCP + 2 * k + 1];
+    }
+    // pair updates: levels 0-2 of value v, +-1 in the byte of the next digit
+    auto pbump = [&](int c, unsigned v, int d) {
+        const int k = c >> 1;
+        const unsigned one = (unsigned)d;  // +1 or 0xffffffff (-1)
+        atomicAdd(prs + 0 * NPR + k, one << (8 * (v >> 6)));
+        if (PL >= 2) atomicAdd(prs + (1 + (v >> 6)) * NPR + k, one << (8 * ((v >> 4) & 3)));
+        if (PL >= 3) atomicAdd(prs + (5 + (v >> 4)) * NPR + k, one << (8 * ((v >> 2) & 3)));
+    };
+    constexpr int CH_PF = 2;
+    int gxs[CH_PF];
+#pragma unroll
+    for (int u = 0; u < CH_PF; ++u) gxs[u] = clampi(X0 - r + min(tid + u * T, NCOL - 1), 0, W - 1);
+    unsigned pvo[CH_PF], pvi[CH_PF];
+    auto prefetch = [&](int yn) {
+        const uint8_t *ro = src_row(p, src, clampi(yn - r - 1, 0, H - 1));
+        const uint8_t *ri = src_row(p, src, clampi(yn + r, 0, H - 1));
+#pragma unroll
+        for (int u = 0; u < CH_PF; ++u) {
+            pvo[u] = __ldg(ro + gxs[u]);
+            pvi[u] = __ldg(ri + gxs[u]);
+        }
+    };
+    if (y0 + 1 < y1) prefetch(y0 + 1);
+    // the thread's window: stripe columns tid .. tid+n-1
+    const int kp = (tid + 1) >> 1, cs = (tid & 1) ? tid : tid + n - 1, np = (n - 1) >> 1;
+    for (int y = y0; y < y1; ++y) {
+        if (y > y0) {
+            __syncthreads();  // previous row's gathers done (also orders the pair init)
+#pragma unroll
+            for (int u = 0; u < CH_PF; ++u) {
+                const int c = tid + u * T;
+                if (c < NCOL && pvo[u] != pvi[u]) {
+                    ch4_bump(recb, NCP, c, pvo[u], -1);
+                    ch4_bump(recb, NCP, c, pvi[u], 1);
+                    pbump(c, pvo[u], -1);
+                    pbump(c, pvi[u], 1);
+                }
+            }
+            if (NCOL > CH_PF * T) {
+                const uint8_t *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
+                const uint8_t *ri = src_row(p, src, clampi(y + r, 0, H - 1));
+                for (int c = tid + CH_PF * T; c < NCOL; c += T) {
+                    const int gx = clampi(X0 - r + c, 0, W - 1);
+                    const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
+                    if (vo == vi) continue;
+                    ch4_bump(recb, NCP, c, vo, -1);
+                    ch4_bump(recb, NCP, c, vi, 1);
+                    pbump(c, vo, -1);
+                    pbump(c, vi, 1);
+                }
+            }
+            if (y + 1 < y1) prefetch(y + 1);
+        }
+        __syncthreads();
+        uint32_t k = p.rank, w0, w1;
+        ch4p_gather<GP>(prs, rec, kp, cs, np, w0, w1);
+        const int d3 = ch4_descend(w0, w1, k);
+        if (PL >= 2)
+            ch4p_gather<GP>(prs + (1 + d3) * NPR, rec + (1 + d3) * NCP, kp, cs, np, w0, w1);
+        else
+            ch4_gather<G, M>(rec + (1 + d3) * NCP + tid, n, w0, w1);
+        const int d2 = ch4_descend(w0, w1, k);
+        const int p2 = d3 * 4 + d2;
+        if (PL >= 3)
+            ch4p_gather<GP>(prs + (5 + p2) * NPR, rec + (5 + p2) * NCP, kp, cs, np, w0, w1);
+        else
+            ch4_gather<G, M>(rec + (5 + p2) * NCP + tid, n, w0, w1);
+        const int d1 = ch4_descend(w0, w1, k);
+        const int p3 = p2 * 4 + d1;
+        ch4_gather<G, M>(rec + (21 + p3) * NCP + tid, n, w0, w1);
+        const int d0 = ch4_descend(w0, w1, k);
+        const unsigned v = (unsigned)(p3 * 4 + d0);
+        if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
+    }
+    if (STREAM) stream_signal(p, y0, y1, X0, X0 + T);
+}
+
+}  // namespace mtb
