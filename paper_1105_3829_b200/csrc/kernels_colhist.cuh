@@ -297,9 +297,89 @@ __device__ __forceinline__ void ch4_bump(uint8_t *recb, int NCOL, int c, unsigne
     recb[((21 + (v >> 2)) * NCOL + c) * 4 + (v & 3)] += d;
 }
 
+// PL = number of levels with pair records (3: levels 0-2, 21 record rows;
+// 2: levels 0-1, 5 rows) -- fewer when shared memory would otherwise drop
+// the CTA below two per SM.
+__host__ __device__ constexpr int ch4p_recs(int PL) { return PL >= 3 ? 21 : (PL == 2 ? 5 : 1); }
+
+__host__ __device__ inline int colhist4p_ncolp(int T, int r) { return (T + 2 * r + 1) & ~1; }
+__host__ __device__ inline int colhist4p_bytes(int T, int r, int PL) {
+    const int ncp = colhist4p_ncolp(T, r);
+    return (CH4_RECS * ncp + ch4p_recs(PL) * (ncp / 2)) * 4;
+}
+
+// window of one level from pair records (np = (n-1)/2 pairs from kp) plus
+// the single column cs; GP pairs per carry-free group, runtime tail
+template <int GP>
+__device__ __forceinline__ void ch4p_gather(const uint32_t *pr, const uint32_t *sr, int kp, int cs, int np,
+                                            uint32_t &w0, uint32_t &w1) {
+    const uint32_t sv = sr[cs];
+    w0 = __byte_perm(sv, 0, 0x4140);
+    w1 = __byte_perm(sv, 0, 0x4342);
+    const uint32_t *rp = pr + kp;
+    const int full = np - np % GP;
+    int j = 0;
+    for (; j < full; j += GP) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int q = 0; q < GP; q += 2) t += rp[j + q] + (q + 1 < GP ? rp[j + q + 1] : 0u);
+        w0 += __byte_perm(t, 0, 0x4140);
+        w1 += __byte_perm(t, 0, 0x4342);
+    }
+    if (j < np) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int q = 0; q < GP - 1; ++q)
+            if (j + q < np) t += rp[j + q];
+        w0 += __byte_perm(t, 0, 0x4140);
+        w1 += __byte_perm(t, 0, 0x4342);
+    }
+}
+
 // the 4-level selection of the rank-k element (k updated to the rank within
 // the selected value) from the records of the window starting at rp (= record
 // row 0, thread column applied)
+// the same with pair records for the upper PL levels (prs: [PR][NPR]);
+// the thread's window is stripe columns tid .. tid+n-1
+template <int G, int M, int PL>
+__device__ __forceinline__ unsigned ch4_select_p(const uint32_t *rec, const uint32_t *prs, int NCP, int NPR, int tid,
+                                                 int n, uint32_t &k) {
+    if (PL == 0) {
+        uint32_t w0, w1;
+        ch4_gather<G, M>(rec + tid, n, w0, w1);
+        const int d3 = ch4_descend(w0, w1, k);
+        ch4_gather<G, M>(rec + (1 + d3) * NCP + tid, n, w0, w1);
+        const int d2 = ch4_descend(w0, w1, k);
+        const int p2 = d3 * 4 + d2;
+        ch4_gather<G, M>(rec + (5 + p2) * NCP + tid, n, w0, w1);
+        const int d1 = ch4_descend(w0, w1, k);
+        const int p3 = p2 * 4 + d1;
+        ch4_gather<G, M>(rec + (21 + p3) * NCP + tid, n, w0, w1);
+        const int d0 = ch4_descend(w0, w1, k);
+        return (unsigned)(p3 * 4 + d0);
+    }
+    constexpr int GP = G / 2;
+    const int kp = (tid + 1) >> 1, cs = (tid & 1) ? tid : tid + n - 1, np = (n - 1) >> 1;
+    uint32_t w0, w1;
+    ch4p_gather<GP>(prs, rec, kp, cs, np, w0, w1);
+    const int d3 = ch4_descend(w0, w1, k);
+    if (PL >= 2)
+        ch4p_gather<GP>(prs + (1 + d3) * NPR, rec + (1 + d3) * NCP, kp, cs, np, w0, w1);
+    else
+        ch4_gather<G, M>(rec + (1 + d3) * NCP + tid, n, w0, w1);
+    const int d2 = ch4_descend(w0, w1, k);
+    const int p2 = d3 * 4 + d2;
+    if (PL >= 3)
+        ch4p_gather<GP>(prs + (5 + p2) * NPR, rec + (5 + p2) * NCP, kp, cs, np, w0, w1);
+    else
+        ch4_gather<G, M>(rec + (5 + p2) * NCP + tid, n, w0, w1);
+    const int d1 = ch4_descend(w0, w1, k);
+    const int p3 = p2 * 4 + d1;
+    ch4_gather<G, M>(rec + (21 + p3) * NCP + tid, n, w0, w1);
+    const int d0 = ch4_descend(w0, w1, k);
+    return (unsigned)(p3 * 4 + d0);
+}
+
 template <int G, int M>
 __device__ __forceinline__ unsigned ch4_select(const uint32_t *rp, int NCOL, int n, uint32_t &k) {
     uint32_t w0, w1;
@@ -321,29 +401,55 @@ __device__ __forceinline__ unsigned ch4_select(const uint32_t *rp, int NCOL, int
 // time; `key(v)` maps a pixel to its 8-bit record key (or -1: not counted),
 // `pixel(y)` runs after each row's records are final.  Next-row pixels are
 // prefetched a row ahead so their latency hides behind the gathers.
-template <int T, typename P, typename Key, typename Pixel>
+// PL > 0: also pair records prs [ch4p_recs(PL)][NCP/2] for the upper PL
+// levels (rec row stride NCP even, pad column zero); updated with
+// shared-memory atomics.
+template <int T, int PL = 0, typename P, typename Key, typename Pixel>
 __device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uint32_t *rec, int NCOL, int X0,
-                                          int ya, int yb, Key key, Pixel pixel) {
+                                          int ya, int yb, Key key, Pixel pixel, uint32_t *prs = nullptr,
+                                          int NCP = 0) {
     const int tid = threadIdx.x;
     const int r = p.radius, H = p.H, W = p.W;
+    const int RS = PL > 0 ? NCP : NCOL;  // record row stride
+    const int NPR = RS / 2;
     uint8_t *recb = reinterpret_cast<uint8_t *>(rec);
+    auto pbump = [&](int c, unsigned v, int d) {
+        const int kk = c >> 1;
+        const unsigned one = (unsigned)d;
+        atomicAdd(prs + kk, one << (8 * (v >> 6)));
+        if (PL >= 2) atomicAdd(prs + (1 + (v >> 6)) * NPR + kk, one << (8 * ((v >> 4) & 3)));
+        if (PL >= 3) atomicAdd(prs + (5 + (v >> 4)) * NPR + kk, one << (8 * ((v >> 2) & 3)));
+    };
     auto bump2 = [&](int c, unsigned vo, unsigned vi) {
         const int ko = key(vo), ki = key(vi);
         if (ko == ki) return;
-        if (ko >= 0) ch4_bump(recb, NCOL, c, (unsigned)ko, -1);
-        if (ki >= 0) ch4_bump(recb, NCOL, c, (unsigned)ki, 1);
+        if (ko >= 0) {
+            ch4_bump(recb, RS, c, (unsigned)ko, -1);
+            if (PL > 0) pbump(c, (unsigned)ko, -1);
+        }
+        if (ki >= 0) {
+            ch4_bump(recb, RS, c, (unsigned)ki, 1);
+            if (PL > 0) pbump(c, (unsigned)ki, 1);
+        }
     };
     __syncthreads();  // previous users of rec are done
-    for (int i = tid; i < CH4_RECS * NCOL; i += T) rec[i] = 0;
+    for (int i = tid; i < CH4_RECS * RS; i += T) rec[i] = 0;
     __syncthreads();
     for (int c = tid; c < NCOL; c += T) {
         const int gx = clampi(X0 - r + c, 0, W - 1);
         for (int j = -r; j <= r; ++j) {
             const int kv = key(src_row(p, src, clampi(ya + j, 0, H - 1))[gx]);
-            if (kv >= 0) ch4_bump(recb, NCOL, c, (unsigned)kv, 1);
+            if (kv >= 0) ch4_bump(recb, RS, c, (unsigned)kv, 1);
         }
     }
     __syncthreads();
+    if (PL > 0) {
+        for (int i = tid; i < ch4p_recs(PL) * NPR; i += T) {
+            const int row = i / NPR, kk = i - row * NPR;
+            prs[i] = rec[row * RS + 2 * kk] + rec[row * RS + 2 * kk + 1];
+        }
+        __syncthreads();
+    }
     constexpr int CH_PF = 2;
     int gxs[CH_PF];
 #pragma unroll
@@ -401,7 +507,7 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
     const int x = X0 + tid;
     if (STREAM) stream_wait_rows(p, y1 + r);
-    ch4_sweep<T, uint8_t>(
+    ch4_sweep<T, 0, uint8_t>(
         p, src, rec, NCOL, X0, y0, y1 - 1, [](unsigned v) { return (int)v; },
         [&](int y) {
             uint32_t k = p.rank;
@@ -422,14 +528,17 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
 //      with this H select their low byte with rank k.
 // Exact for any image; the cost grows with the number of distinct H per
 // tile, so the host only picks it when the sampled high-byte spread is small.
-template <int T, int G, int M>
+template <int T, int G, int M, int PL>
 __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__restrict__ hplane) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int r = p.radius, W = p.W, n = 2 * r + 1;
     const int NCOL = T + 2 * r;
-    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCOL]
-    int *hfirst = reinterpret_cast<int *>(rec + CH4_RECS * NCOL);  // [256]
+    const int NCP = PL > 0 ? colhist4p_ncolp(T, r) : NCOL;  // record row stride
+    const int NPR = NCP / 2;
+    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCP]
+    uint32_t *prs = rec + CH4_RECS * NCP;                     // [PR][NPR] (PL > 0)
+    int *hfirst = reinterpret_cast<int *>(prs + (PL > 0 ? ch4p_recs(PL) * NPR : 0));  // [256]
     int *hlast = hfirst + 256;                                      // [256]
     const int X0 = blockIdx.x * T;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
@@ -447,11 +556,11 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
         hlast[i] = -1;
     }
     // phase A: high byte and rank within it
-    ch4_sweep<T, uint16_t>(
+    ch4_sweep<T, PL, uint16_t>(
         p, src, rec, NCOL, X0, y0, y1 - 1, [](unsigned v) { return (int)(v >> 8); },
         [&](int y) {
             uint32_t k = p.rank;
-            const unsigned hb = ch4_select<G, M>(rec + tid, NCOL, n, k);
+            const unsigned hb = ch4_select_p<G, M, PL>(rec, prs, NCP, NPR, tid, n, k);
             if (x < W) {
                 const int64_t o = (int64_t)(y - p.row_begin) * W + x;
                 hpl[o] = (uint8_t)hb;
@@ -461,13 +570,14 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
                 if (hfirst[hb] > y) hfirst[hb] = y;
                 hlast[hb] = y;
             }
-        });
+        },
+        prs, NCP);
     __syncthreads();
     // phase B: one sweep per high byte used by the tile
     for (int hb = 0; hb < 256; ++hb) {
         const int ya = hfirst[hb], yb = hlast[hb];  // CTA-uniform
         if (yb < 0) continue;
-        ch4_sweep<T, uint16_t>(
+        ch4_sweep<T, PL, uint16_t>(
             p, src, rec, NCOL, X0, ya, yb,
             [hb](unsigned v) { return (int)(v >> 8) == hb ? (int)(v & 255) : -1; },
             [&](int y) {
@@ -476,10 +586,11 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
                 if (hpl[o] != hb) return;
                 uint16_t *d = dst + (int64_t)(y - p.row_begin) * p.dst_pitch + x;
                 uint32_t k = *d;
-                const unsigned lo = ch4_select<G, M>(rec + tid, NCOL, n, k);
+                const unsigned lo = ch4_select_p<G, M, PL>(rec, prs, NCP, NPR, tid, n, k);
                 const unsigned v = ((unsigned)hb << 8) | lo;
                 *d = lut ? __ldg(lut + v) : (uint16_t)v;
-            });
+            },
+            prs, NCP);
     }
     stream_signal(p, y0, y1, X0, X0 + T);
 }
@@ -647,45 +758,6 @@ namespace mtb {
 // pair changes with shared-memory atomics (adjacent columns belong to
 // adjacent threads); counts never go below zero, so a per-byte decrement
 // never borrows across bytes.
-// PL = number of levels with pair records (3: levels 0-2, 21 record rows;
-// 2: levels 0-1, 5 rows) -- fewer when shared memory would otherwise drop
-// the CTA below two per SM.
-__host__ __device__ constexpr int ch4p_recs(int PL) { return PL >= 3 ? 21 : (PL == 2 ? 5 : 1); }
-
-__host__ __device__ inline int colhist4p_ncolp(int T, int r) { return (T + 2 * r + 1) & ~1; }
-__host__ __device__ inline int colhist4p_bytes(int T, int r, int PL) {
-    const int ncp = colhist4p_ncolp(T, r);
-    return (CH4_RECS * ncp + ch4p_recs(PL) * (ncp / 2)) * 4;
-}
-
-// window of one level from pair records (np = (n-1)/2 pairs from kp) plus
-// the single column cs; GP pairs per carry-free group, runtime tail
-template <int GP>
-__device__ __forceinline__ void ch4p_gather(const uint32_t *pr, const uint32_t *sr, int kp, int cs, int np,
-                                            uint32_t &w0, uint32_t &w1) {
-    const uint32_t sv = sr[cs];
-    w0 = __byte_perm(sv, 0, 0x4140);
-    w1 = __byte_perm(sv, 0, 0x4342);
-    const uint32_t *rp = pr + kp;
-    const int full = np - np % GP;
-    int j = 0;
-    for (; j < full; j += GP) {
-        uint32_t t = 0;
-#pragma unroll
-        for (int q = 0; q < GP; q += 2) t += rp[j + q] + (q + 1 < GP ? rp[j + q + 1] : 0u);
-        w0 += __byte_perm(t, 0, 0x4140);
-        w1 += __byte_perm(t, 0, 0x4342);
-    }
-    if (j < np) {
-        uint32_t t = 0;
-#pragma unroll
-        for (int q = 0; q < GP - 1; ++q)
-            if (j + q < np) t += rp[j + q];
-        w0 += __byte_perm(t, 0, 0x4140);
-        w1 += __byte_perm(t, 0, 0x4342);
-    }
-}
-
 template <int T, int G, int M, int PL, bool STREAM>
 __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
     constexpr int GP = G / 2;

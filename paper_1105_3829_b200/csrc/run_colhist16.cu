@@ -7,10 +7,11 @@
 
 namespace mtb {
 
-template <int T, int G, int M>
+template <int T, int G, int M, int PL>
 static int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s) {
-    const size_t smem = (size_t)colhist4_bytes(T, p.radius) + 2 * 256 * sizeof(int);
-    auto kern = k_colhist16_u16<T, G, M>;
+    const size_t smem = (PL > 0 ? (size_t)colhist4p_bytes(T, p.radius, PL) : (size_t)colhist4_bytes(T, p.radius)) +
+                        2 * 256 * sizeof(int);
+    auto kern = k_colhist16_u16<T, G, M, PL>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
@@ -34,23 +35,31 @@ static int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s) {
     return MTB_OK;
 }
 
-template <int T, int G>
+template <int T, int G, int PL>
 static int run_colhist16_u16_g(SlabParams p, int B, cudaStream_t s) {
     switch ((2 * p.radius + 1) % G) {
-        case 1: return run_colhist16_u16_gm<T, G, (G > 1 ? 1 : 0)>(p, B, s);
-        case 3: return run_colhist16_u16_gm<T, G, (G > 3 ? 3 : 0)>(p, B, s);
-        case 5: return run_colhist16_u16_gm<T, G, (G > 5 ? 5 : 0)>(p, B, s);
-        case 7: return run_colhist16_u16_gm<T, G, (G > 7 ? 7 : 0)>(p, B, s);
-        default: return run_colhist16_u16_gm<T, G, 0>(p, B, s);
+        case 1: return run_colhist16_u16_gm<T, G, (G > 1 ? 1 : 0), PL>(p, B, s);
+        case 3: return run_colhist16_u16_gm<T, G, (G > 3 ? 3 : 0), PL>(p, B, s);
+        case 5: return run_colhist16_u16_gm<T, G, (G > 5 ? 5 : 0), PL>(p, B, s);
+        case 7: return run_colhist16_u16_gm<T, G, (G > 7 ? 7 : 0), PL>(p, B, s);
+        default: return run_colhist16_u16_gm<T, G, 0, PL>(p, B, s);
     }
 }
 
 int run_colhist16_u16(SlabParams p, int B, cudaStream_t s) {
     const int n = 2 * p.radius + 1;
-    if (8 * n <= 255) return run_colhist16_u16_g<256, 8>(p, B, s);
-    if (4 * n <= 255) return run_colhist16_u16_g<256, 4>(p, B, s);
-    if (2 * n <= 255) return run_colhist16_u16_g<256, 2>(p, B, s);
-    return run_colhist16_u16_g<256, 1>(p, B, s);
+    // pair records (upper levels) where two 256-thread CTAs per SM still fit
+    const int lim = 113 * 1024 - 2 * 256 * (int)sizeof(int);
+    const int pl = env_int("MTB_CH16_PL", colhist4p_bytes(256, p.radius, 3) <= lim ? 3
+                                          : colhist4p_bytes(256, p.radius, 2) <= lim ? 2 : 0);
+    if (8 * n <= 255) {
+        if (pl == 3) return run_colhist16_u16_g<256, 8, 3>(p, B, s);
+        if (pl == 2) return run_colhist16_u16_g<256, 8, 2>(p, B, s);
+        return run_colhist16_u16_g<256, 8, 0>(p, B, s);
+    }
+    if (4 * n <= 255) return pl >= 2 ? run_colhist16_u16_g<256, 4, 2>(p, B, s) : run_colhist16_u16_g<256, 4, 0>(p, B, s);
+    if (2 * n <= 255) return run_colhist16_u16_g<256, 2, 0>(p, B, s);
+    return run_colhist16_u16_g<256, 1, 0>(p, B, s);
 }
 
 
