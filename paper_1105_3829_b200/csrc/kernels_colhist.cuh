@@ -251,7 +251,11 @@ namespace mtb {
 // loads are 32 consecutive words.
 constexpr int CH4_RECS = 85;
 
-__host__ __device__ inline int colhist4_bytes(int T, int r) { return CH4_RECS * (T + 2 * r) * 4; }
+// record row stride: a multiple of 32 words, so a warp's per-column byte
+// updates (column c -> bank c mod 32, whatever the record row) never
+// conflict
+__host__ __device__ inline int ch4_stride(int ncol) { return (ncol + 31) & ~31; }
+__host__ __device__ inline int colhist4_bytes(int T, int r) { return CH4_RECS * ch4_stride(T + 2 * r) * 4; }
 
 // 4 bins (packed u16 pairs w0 = {b0, b1}, w1 = {b2, b3}): smallest digit d
 // with cumsum(bins[0..d]) >= k; leaves the rank within bin d in k
@@ -302,10 +306,46 @@ __device__ __forceinline__ void ch4_bump(uint8_t *recb, int NCOL, int c, unsigne
 // the CTA below two per SM.
 __host__ __device__ constexpr int ch4p_recs(int PL) { return PL >= 3 ? 21 : (PL == 2 ? 5 : 1); }
 
-__host__ __device__ inline int colhist4p_ncolp(int T, int r) { return (T + 2 * r + 1) & ~1; }
-__host__ __device__ inline int colhist4p_bytes(int T, int r, int PL) {
+// record rows padded to a multiple of 32 columns (conflict-free updates;
+// pair and quad alignment)
+__host__ __device__ inline int colhist4p_ncolp(int T, int r) { return (T + 2 * r + 31) & ~31; }
+__host__ __device__ inline int colhist4p_bytes(int T, int r, int PL, int QL = 0) {
     const int ncp = colhist4p_ncolp(T, r);
-    return (CH4_RECS * ncp + ch4p_recs(PL) * (ncp / 2)) * 4;
+    return (CH4_RECS * ncp + ch4p_recs(PL) * (ncp / 2) + ch4p_recs(QL) * (ncp / 4) * (QL > 0)) * 4;
+}
+
+// window of one level from QUAD records (columns 4q..4q+3) for the aligned
+// middle of [a, a+n), pair and single records for the 0-3 columns at
+// either end (predicated loads: the head/tail shape differs per lane).
+// Quad counts are <= 4n: GQ quads per carry-free group.
+template <int GQ>
+__device__ __forceinline__ void ch4q_gather(const uint32_t *qr, const uint32_t *pr, const uint32_t *sr, int a, int n,
+                                            uint32_t &w0, uint32_t &w1) {
+    const int b = a + n;
+    const int a4 = (a + 3) & ~3, b4 = b & ~3;
+    const int h = a4 - a, t = b - b4;
+    const uint32_t hv = ((h & 1) ? sr[a] : 0u) + ((h & 2) ? pr[(a + (h & 1)) >> 1] : 0u);
+    const uint32_t tv = ((t & 2) ? pr[b4 >> 1] : 0u) + ((t & 1) ? sr[b4 + (t & 2)] : 0u);
+    w0 = __byte_perm(hv, 0, 0x4140) + __byte_perm(tv, 0, 0x4140);
+    w1 = __byte_perm(hv, 0, 0x4342) + __byte_perm(tv, 0, 0x4342);
+    const uint32_t *rp = qr + (a4 >> 2);
+    const int nq = (b4 - a4) >> 2;
+    int j = 0;
+    for (; j + GQ <= nq; j += GQ) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int q = 0; q < GQ; ++q) v += rp[j + q];
+        w0 += __byte_perm(v, 0, 0x4140);
+        w1 += __byte_perm(v, 0, 0x4342);
+    }
+    if (GQ > 1 && j < nq) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int q = 0; q < GQ - 1; ++q)
+            if (j + q < nq) v += rp[j + q];
+        w0 += __byte_perm(v, 0, 0x4140);
+        w1 += __byte_perm(v, 0, 0x4342);
+    }
 }
 
 // window of one level from pair records (np = (n-1)/2 pairs from kp) plus
@@ -410,7 +450,7 @@ __device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uin
                                           int NCP = 0) {
     const int tid = threadIdx.x;
     const int r = p.radius, H = p.H, W = p.W;
-    const int RS = PL > 0 ? NCP : NCOL;  // record row stride
+    const int RS = PL > 0 ? NCP : ch4_stride(NCOL);  // record row stride
     const int NPR = RS / 2;
     uint8_t *recb = reinterpret_cast<uint8_t *>(rec);
     auto pbump = [&](int c, unsigned v, int d) {
@@ -496,8 +536,8 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int r = p.radius, W = p.W, n = 2 * r + 1;
-    const int NCOL = T + 2 * r;
-    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCOL]
+    const int NCOL = T + 2 * r, RS = ch4_stride(NCOL);
+    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][RS]
     const int X0 = blockIdx.x * T;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
     if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
@@ -511,7 +551,7 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
         p, src, rec, NCOL, X0, y0, y1 - 1, [](unsigned v) { return (int)v; },
         [&](int y) {
             uint32_t k = p.rank;
-            const unsigned v = ch4_select<G, M>(rec + tid, NCOL, n, k);
+            const unsigned v = ch4_select<G, M>(rec + tid, RS, n, k);
             if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
         });
     if (STREAM) stream_signal(p, y0, y1, X0, X0 + T);
@@ -534,7 +574,7 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
     const int tid = threadIdx.x;
     const int r = p.radius, W = p.W, n = 2 * r + 1;
     const int NCOL = T + 2 * r;
-    const int NCP = PL > 0 ? colhist4p_ncolp(T, r) : NCOL;  // record row stride
+    const int NCP = PL > 0 ? colhist4p_ncolp(T, r) : ch4_stride(NCOL);  // record row stride
     const int NPR = NCP / 2;
     uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCP]
     uint32_t *prs = rec + CH4_RECS * NCP;                     // [PR][NPR] (PL > 0)
@@ -616,9 +656,9 @@ __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
-    const int NCOL = T + 2 * r;
-    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);                  // [85][NCOL]
-    uint16_t *sc = reinterpret_cast<uint16_t *>(rec + CH4_RECS * NCOL);      // [16][T]
+    const int NCOL = T + 2 * r, RS = ch4_stride(NCOL);
+    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);                  // [85][RS]
+    uint16_t *sc = reinterpret_cast<uint16_t *>(rec + CH4_RECS * RS);        // [16][T]
     uint8_t *rpos = reinterpret_cast<uint8_t *>(sc + 16 * T);                // [n][T]
     uint16_t *scol = reinterpret_cast<uint16_t *>(rpos + ((n * T + 15) & ~15));  // [NCOL][n]
     uint8_t *recb = reinterpret_cast<uint8_t *>(rec);
@@ -634,14 +674,14 @@ __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
     stream_wait_rows(p, y1 + r);
 
     // records and sorted columns for row y0
-    for (int i = tid; i < CH4_RECS * NCOL; i += T) rec[i] = 0;
+    for (int i = tid; i < CH4_RECS * RS; i += T) rec[i] = 0;
     __syncthreads();
     for (int c = tid; c < NCOL; c += T) {
         const int gx = clampi(X0 - r + c, 0, W - 1);
         uint16_t *a = scol + c * n;
         for (int j = 0; j < n; ++j) {
             const uint16_t v = __ldg(src_row(p, src, clampi(y0 - r + j, 0, H - 1)) + gx);
-            ch4_bump(recb, NCOL, c, v >> 8, 1);
+            ch4_bump(recb, RS, c, v >> 8, 1);
             int i = j;
             while (i > 0 && a[i - 1] > v) {
                 a[i] = a[i - 1];
@@ -662,8 +702,8 @@ __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
                     const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
                     if (vo == vi) continue;
                     if ((vo >> 8) != (vi >> 8)) {
-                        ch4_bump(recb, NCOL, c, vo >> 8, -1);
-                        ch4_bump(recb, NCOL, c, vi >> 8, 1);
+                        ch4_bump(recb, RS, c, vo >> 8, -1);
+                        ch4_bump(recb, RS, c, vi >> 8, 1);
                     }
                     uint16_t *a = scol + c * n;
                     const uint16_t *const aa[2] = {a, a};
@@ -684,7 +724,7 @@ __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
         }
         // high byte and rank within it
         uint32_t k = p.rank;
-        const unsigned hb = ch4_select<G, M>(rec + tid, NCOL, n, k);
+        const unsigned hb = ch4_select<G, M>(rec + tid, RS, n, k);
         // low byte: runs of [256H, 256H+256) in the window columns
         const unsigned vb = hb << 8, ve = vb + 256;
 #pragma unroll
@@ -758,16 +798,21 @@ namespace mtb {
 // pair changes with shared-memory atomics (adjacent columns belong to
 // adjacent threads); counts never go below zero, so a per-byte decrement
 // never borrows across bytes.
-template <int T, int G, int M, int PL, bool STREAM>
+template <int T, int G, int M, int PL, int QL, bool STREAM>
 __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
+    static_assert(QL <= PL && QL <= 2 && (QL == 0 || G >= 4), "quad levels need pairs and 4n <= 255");
     constexpr int GP = G / 2;
+    constexpr int GQ = G >= 4 ? G / 4 : 1;
     constexpr int PR = ch4p_recs(PL);
+    constexpr int QR = QL > 0 ? ch4p_recs(QL) : 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
     const int NCOL = T + 2 * r, NCP = colhist4p_ncolp(T, r), NPR = NCP / 2;
     uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCP] singles
     uint32_t *prs = rec + CH4_RECS * NCP;                     // [PR][NPR] pairs
+    const int NQ = NCP / 4;
+    uint32_t *qrs = prs + PR * NPR;                            // [QR][NQ] quads
     uint8_t *recb = smem_raw;
     const int X0 = blockIdx.x * T;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
@@ -790,6 +835,11 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         const int row = i / NPR, k = i - row * NPR;
         prs[i] = rec[row * NCP + 2 * k] + rec[row * NCP + 2 * k + 1];
     }
+    for (int i = tid; i < QR * NQ; i += T) {
+        const int row = i / NQ, q = i - row * NQ;
+        const uint32_t *sr = rec + row * NCP + 4 * q;
+        qrs[i] = sr[0] + sr[1] + sr[2] + sr[3];
+    }
     // pair updates: levels 0-2 of value v, +-1 in the byte of the next digit
     auto pbump = [&](int c, unsigned v, int d) {
         const int k = c >> 1;
@@ -797,6 +847,9 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         atomicAdd(prs + 0 * NPR + k, one << (8 * (v >> 6)));
         if (PL >= 2) atomicAdd(prs + (1 + (v >> 6)) * NPR + k, one << (8 * ((v >> 4) & 3)));
         if (PL >= 3) atomicAdd(prs + (5 + (v >> 4)) * NPR + k, one << (8 * ((v >> 2) & 3)));
+        const int q = c >> 2;
+        if (QL >= 1) atomicAdd(qrs + q, one << (8 * (v >> 6)));
+        if (QL >= 2) atomicAdd(qrs + (1 + (v >> 6)) * NQ + q, one << (8 * ((v >> 4) & 3)));
     };
     constexpr int CH_PF = 2;
     int gxs[CH_PF];
@@ -845,9 +898,14 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         }
         __syncthreads();
         uint32_t k = p.rank, w0, w1;
-        ch4p_gather<GP>(prs, rec, kp, cs, np, w0, w1);
+        if (QL >= 1)
+            ch4q_gather<GQ>(qrs, prs, rec, tid, n, w0, w1);
+        else
+            ch4p_gather<GP>(prs, rec, kp, cs, np, w0, w1);
         const int d3 = ch4_descend(w0, w1, k);
-        if (PL >= 2)
+        if (QL >= 2)
+            ch4q_gather<GQ>(qrs + (1 + d3) * NQ, prs + (1 + d3) * NPR, rec + (1 + d3) * NCP, tid, n, w0, w1);
+        else if (PL >= 2)
             ch4p_gather<GP>(prs + (1 + d3) * NPR, rec + (1 + d3) * NCP, kp, cs, np, w0, w1);
         else
             ch4_gather<G, M>(rec + (1 + d3) * NCP + tid, n, w0, w1);

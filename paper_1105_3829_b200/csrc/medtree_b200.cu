@@ -217,15 +217,15 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     const std::string force = forced_kernel();
     // Kernel choice (measured on B200, tools/probe.py):
     //   median, n <= 5 (8-bit), n <= 7 (16-bit)  -> selection networks
-    //   8-bit, r <= 40 (any rank)                 -> column-histogram gather
-    //   8-bit, 41 <= r <= 127                     -> CTMF tiles (O(1) in r)
+    //   8-bit, r <= 31 (any rank)                 -> column-histogram gather
+    //   8-bit, 32 <= r <= 127                     -> CTMF tiles (O(1) in r)
     //   otherwise                                 -> per-column vertical histograms
     if ((force.empty() || force == "sortnet") && sortnet_applies<P>(p) &&
         (sizeof(P) == 2 || p.radius <= 2 || force == "sortnet"))
         return run_sortnet<P>(p, B, s);
     if (sizeof(P) == 1 && p.radius <= 63 && force == "lob") return run_lob_u8_32(p, B, s);
     if (sizeof(P) == 1 && n <= 255 &&
-        (force == "colhist" || (force.empty() && p.radius <= env_int("MTB_CH_MAX_R", 40))))
+        (force == "colhist" || (force.empty() && p.radius <= env_int("MTB_CH_MAX_R", 31))))
         return run_colhist_u8(p, B, s);
     if (sizeof(P) == 1 && !wide && (force == "ctmf" || force.empty())) return run_ctmf_u8(p, B, s);
     // 16-bit: compact high bytes (sampled spread <= MTB_U16_SPREAD) -> the

@@ -78,10 +78,10 @@ static int run_colhist4_u8(SlabParams p, int B, cudaStream_t s, const char *name
     return run_colhist4_u8_g<T, 1>(p, B, s, name);
 }
 
-template <int T, int G, int M, int PL>
+template <int T, int G, int M, int PL, int QL = 0>
 static int run_colhist4p_u8_gm(SlabParams p, int B, cudaStream_t s, const char *name) {
-    const size_t smem = (size_t)colhist4p_bytes(T, p.radius, PL);
-    auto kern = p.in_rows ? k_colhist4p_u8<T, G, M, PL, true> : k_colhist4p_u8<T, G, M, PL, false>;
+    const size_t smem = (size_t)colhist4p_bytes(T, p.radius, PL, QL);
+    auto kern = p.in_rows ? k_colhist4p_u8<T, G, M, PL, QL, true> : k_colhist4p_u8<T, G, M, PL, QL, false>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
@@ -92,39 +92,40 @@ static int run_colhist4p_u8_gm(SlabParams p, int B, cudaStream_t s, const char *
     return launch(kern, grid, T, smem, s, p, name);
 }
 
-// pair records (G even: n <= 127); PL pair levels
-template <int T, int PL>
+// pair records (G even: n <= 127); PL pair levels, QL quad levels (4n <= 255)
+template <int T, int PL, int QL = 0>
 static int run_colhist4p_u8(SlabParams p, int B, cudaStream_t s, const char *name) {
     const int n = 2 * p.radius + 1;
     if (8 * n <= 255) {
         switch (n % 8) {
-            case 1: return run_colhist4p_u8_gm<T, 8, 1, PL>(p, B, s, name);
-            case 3: return run_colhist4p_u8_gm<T, 8, 3, PL>(p, B, s, name);
-            case 5: return run_colhist4p_u8_gm<T, 8, 5, PL>(p, B, s, name);
-            default: return run_colhist4p_u8_gm<T, 8, 7, PL>(p, B, s, name);
+            case 1: return run_colhist4p_u8_gm<T, 8, 1, PL, QL>(p, B, s, name);
+            case 3: return run_colhist4p_u8_gm<T, 8, 3, PL, QL>(p, B, s, name);
+            case 5: return run_colhist4p_u8_gm<T, 8, 5, PL, QL>(p, B, s, name);
+            default: return run_colhist4p_u8_gm<T, 8, 7, PL, QL>(p, B, s, name);
         }
     }
-    if (4 * n <= 255) return n % 4 == 1 ? run_colhist4p_u8_gm<T, 4, 1, PL>(p, B, s, name)
-                                        : run_colhist4p_u8_gm<T, 4, 3, PL>(p, B, s, name);
+    if (4 * n <= 255) return n % 4 == 1 ? run_colhist4p_u8_gm<T, 4, 1, PL, QL>(p, B, s, name)
+                                        : run_colhist4p_u8_gm<T, 4, 3, PL, QL>(p, B, s, name);
     if (2 * n <= 255) return run_colhist4p_u8_gm<T, 2, 1, PL>(p, B, s, name);
     return run_colhist4_u8<T>(p, B, s, "k_colhist4_u8<256>");  // pair counts would overflow u8
 }
 
-// 8-bit column-histogram gather kernels; the variant by radius (tools/probe.py
-// sweep on config 2): 16-bin records, one pixel per thread for
-// r <= 5, two for r <= 13; radix-4 records (with pair records where they
-// fit) above.  MTB_CH_VAR forces one.
+// 8-bit column-histogram gather kernels; the variant by radius is below.
+// MTB_CH_VAR forces one.
 int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
     int var = env_int("MTB_CH_VAR", -1);
     if (var < 0) {
-        // r >= 14: radix-4 records with pair records for as many upper
-        // levels as keep two 256-thread CTAs per SM (shared memory)
-        const int lim = 113 * 1024;
-        var = p.radius <= 5 ? 0
-              : p.radius <= 13 ? 2
-              : colhist4p_bytes(256, p.radius, 3) <= lim ? 30
-              : colhist4p_bytes(256, p.radius, 2) <= lim ? 31
-                                                        : 12;
+        // measured on config 2 (tools/probe.py sweep):
+        // 16-bin records for r <= 5; radix-4 records for 6..10 (16-bin with
+        // two pixels per thread at r = 8); from r = 11, radix-4 with pair
+        // records for as many upper levels as keep two 256-thread CTAs per SM
+        const int r = p.radius, lim = 113 * 1024;
+        var = r <= 5 ? 0
+              : r == 8 ? 2
+              : r <= 10 ? 12
+              : (r <= 16 && colhist4p_bytes(256, r, 3) <= lim) ? 30
+              : colhist4p_bytes(256, r, 2) <= lim ? 31
+                                                   : 12;
     }
     switch (var) {
         case 0: return run_colhist_u8_ts<128, 1>(p, B, s, "k_colhist_u8<128,1>");
@@ -132,6 +133,10 @@ int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
         case 30: return run_colhist4p_u8<256, 3>(p, B, s, "k_colhist4p_u8<256,3>");
         case 31: return run_colhist4p_u8<256, 2>(p, B, s, "k_colhist4p_u8<256,2>");
         case 34: return run_colhist4p_u8<256, 1>(p, B, s, "k_colhist4p_u8<256,1>");
+        case 40: return run_colhist4p_u8<256, 3, 2>(p, B, s, "k_colhist4p_u8<256,3,q2>");
+        case 41: return run_colhist4p_u8<256, 2, 2>(p, B, s, "k_colhist4p_u8<256,2,q2>");
+        case 42: return run_colhist4p_u8<256, 3, 1>(p, B, s, "k_colhist4p_u8<256,3,q1>");
+        case 43: return run_colhist4p_u8<256, 2, 1>(p, B, s, "k_colhist4p_u8<256,2,q1>");
         default: return run_colhist4_u8<256>(p, B, s, "k_colhist4_u8<256>");
     }
 }
