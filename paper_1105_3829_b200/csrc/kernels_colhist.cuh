@@ -444,10 +444,16 @@ __device__ __forceinline__ unsigned ch4_select(const uint32_t *rp, int NCOL, int
 // PL > 0: also pair records prs [ch4p_recs(PL)][NCP/2] for the upper PL
 // levels (rec row stride NCP even, pad column zero); updated with
 // shared-memory atomics.
-template <int T, int PL = 0, typename P, typename Key, typename Pixel>
+struct Ch4NoExtra {
+    __device__ void operator()(int, unsigned, int) const {}
+};
+
+// extra(c, v, d): optional additional per-pixel record maintenance
+// (called for every pixel entering (+1) / leaving (-1) column c)
+template <int T, int PL = 0, typename P, typename Key, typename Pixel, typename Extra = Ch4NoExtra>
 __device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uint32_t *rec, int NCOL, int X0,
                                           int ya, int yb, Key key, Pixel pixel, uint32_t *prs = nullptr,
-                                          int NCP = 0) {
+                                          int NCP = 0, Extra extra = Extra()) {
     const int tid = threadIdx.x;
     const int r = p.radius, H = p.H, W = p.W;
     const int RS = PL > 0 ? NCP : ch4_stride(NCOL);  // record row stride
@@ -461,6 +467,8 @@ __device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uin
         if (PL >= 3) atomicAdd(prs + (5 + (v >> 4)) * NPR + kk, one << (8 * ((v >> 2) & 3)));
     };
     auto bump2 = [&](int c, unsigned vo, unsigned vi) {
+        extra(c, vo, -1);
+        extra(c, vi, 1);
         const int ko = key(vo), ki = key(vi);
         if (ko == ki) return;
         if (ko >= 0) {
@@ -478,7 +486,9 @@ __device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uin
     for (int c = tid; c < NCOL; c += T) {
         const int gx = clampi(X0 - r + c, 0, W - 1);
         for (int j = -r; j <= r; ++j) {
-            const int kv = key(src_row(p, src, clampi(ya + j, 0, H - 1))[gx]);
+            const unsigned v = src_row(p, src, clampi(ya + j, 0, H - 1))[gx];
+            extra(c, v, 1);
+            const int kv = key(v);
             if (kv >= 0) ch4_bump(recb, RS, c, (unsigned)kv, 1);
         }
     }
@@ -568,7 +578,14 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
 //      with this H select their low byte with rank k.
 // Exact for any image; the cost grows with the number of distinct H per
 // tile, so the host only picks it when the sampled high-byte spread is small.
-template <int T, int G, int M, int PL>
+// WK (compact data): a first sweep keyed by a guessed high byte H0 (the
+// median high byte of a sample of the tile): records of the low bytes of
+// the pixels with high byte H0 plus, per column, the counts below / equal
+// to / above H0 (one word).  A pixel whose rank falls inside the H0 bin is
+// resolved right there (5 gathers instead of phase A + phase B's 8); the
+// rest (marked in the high-byte plane) go through phases A and B, which
+// then skip H0.
+template <int T, int G, int M, int PL, bool WK>
 __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__restrict__ hplane) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
@@ -578,8 +595,10 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
     const int NPR = NCP / 2;
     uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCP]
     uint32_t *prs = rec + CH4_RECS * NCP;                     // [PR][NPR] (PL > 0)
-    int *hfirst = reinterpret_cast<int *>(prs + (PL > 0 ? ch4p_recs(PL) * NPR : 0));  // [256]
+    uint32_t *rec3 = prs + (PL > 0 ? ch4p_recs(PL) * NPR : 0);  // [NCP] below/equal/above H0 (WK)
+    int *hfirst = reinterpret_cast<int *>(rec3 + (WK ? NCP : 0));  // [256]
     int *hlast = hfirst + 256;                                      // [256]
+    int *flags = hlast + 256;                                       // [0]: H0, [1]: any miss
     const int X0 = blockIdx.x * T;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
     if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
@@ -595,10 +614,74 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
         hfirst[i] = 1 << 30;
         hlast[i] = -1;
     }
-    // phase A: high byte and rank within it
+    int H0 = -1;
+    if (WK) {
+        // H0: median high byte of 256 pixels sampled over the tile
+        if (tid == 0) flags[1] = 0;
+        for (int i = tid; i < 256; i += T) hlast[i] = 0;
+        __syncthreads();
+        for (int i = tid; i < 256; i += T) {
+            const int yy = y0 + (int)(((int64_t)i * 97) % (y1 - y0));
+            const int xx = min(X0 + (int)(((int64_t)i * 61) % T), W - 1);
+            atomicAdd(&hlast[src_row(p, src, yy)[xx] >> 8], 1);  // hlast as a scratch histogram
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int acc = 0, h = 0;
+            for (; h < 255; ++h) {
+                acc += hlast[h];
+                if (2 * acc >= 256) break;
+            }
+            flags[0] = h;
+        }
+        __syncthreads();
+        H0 = flags[0];
+        for (int i = tid; i < 256; i += T) hlast[i] = -1;
+        for (int i = tid; i < NCP; i += T) rec3[i] = 0;
+        uint8_t *r3b = reinterpret_cast<uint8_t *>(rec3);
+        const int h0 = H0;
+        ch4_sweep<T, PL, uint16_t>(
+            p, src, rec, NCOL, X0, y0, y1 - 1,
+            [h0](unsigned v) { return (int)(v >> 8) == h0 ? (int)(v & 255) : -1; },
+            [&](int y) {
+                uint32_t w0, w1;
+                ch4_gather<G, M>(rec3 + tid, n, w0, w1);
+                const uint32_t below = w0 & 0xffffu, eq = w0 >> 16;
+                uint32_t k = p.rank;
+                const bool hit = k > below && k <= below + eq;
+                unsigned lo = 0;
+                if (hit) {
+                    k -= below;
+                    lo = ch4_select_p<G, M, PL>(rec, prs, NCP, NPR, tid, n, k);
+                }
+                if (x < W) {
+                    const int64_t o = (int64_t)(y - p.row_begin) * W + x;
+                    if (hit) {
+                        const unsigned v = ((unsigned)h0 << 8) | lo;
+                        dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint16_t)v;
+                        hpl[o] = (uint8_t)h0;
+                    } else {
+                        hpl[o] = (uint8_t)(h0 ^ 1);  // any value != H0 marks a miss
+                        flags[1] = 1;
+                    }
+                }
+            },
+            prs, NCP,
+            [r3b, h0](int c, unsigned v, int d) {
+                const int hb = (int)(v >> 8);
+                r3b[c * 4 + (hb < h0 ? 0 : (hb == h0 ? 1 : 2))] += d;
+            });
+        __syncthreads();
+        if (flags[1] == 0) {  // every pixel of the tile resolved
+            stream_signal(p, y0, y1, X0, X0 + T);
+            return;
+        }
+    }
+    // phase A: high byte and rank within it (WK: only the marked pixels)
     ch4_sweep<T, PL, uint16_t>(
         p, src, rec, NCOL, X0, y0, y1 - 1, [](unsigned v) { return (int)(v >> 8); },
         [&](int y) {
+            if (WK && (x >= W || hpl[(int64_t)(y - p.row_begin) * W + x] == H0)) return;
             uint32_t k = p.rank;
             const unsigned hb = ch4_select_p<G, M, PL>(rec, prs, NCP, NPR, tid, n, k);
             if (x < W) {
@@ -613,10 +696,10 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
         },
         prs, NCP);
     __syncthreads();
-    // phase B: one sweep per high byte used by the tile
+    // phase B: one sweep per high byte used by the tile (WK: H0 is done)
     for (int hb = 0; hb < 256; ++hb) {
         const int ya = hfirst[hb], yb = hlast[hb];  // CTA-uniform
-        if (yb < 0) continue;
+        if (yb < 0 || (WK && hb == H0)) continue;
         ch4_sweep<T, PL, uint16_t>(
             p, src, rec, NCOL, X0, ya, yb,
             [hb](unsigned v) { return (int)(v >> 8) == hb ? (int)(v & 255) : -1; },

@@ -235,7 +235,7 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     if (sizeof(P) == 2 && force.empty()) {
         spread = wide_spread_u16(p, s);
         if (n <= 255 && spread && p.radius <= env_int("MTB_U16_S_MAX_R", 16)) return run_colhist16s_u16(p, B, s);
-        if (n <= 255) return run_colhist16_u16(p, B, s);
+        if (n <= 255) return run_colhist16_u16(p, B, s, !spread);
     }
     if (sizeof(P) == 2 && n <= 255 && force == "colhist") return run_colhist16_u16(p, B, s);
     if (sizeof(P) == 2 && n <= 255 && force == "colhist16s") return run_colhist16s_u16(p, B, s);

@@ -8,10 +8,13 @@
 namespace mtb {
 
 template <int T, int G, int M, int PL>
-static int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s) {
+static int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s, bool wk) {
+    // window-keyed first sweep (compact data); MTB_CH16_WK=0/1 forces
+    wk = env_int("MTB_CH16_WK", wk ? 1 : 0) != 0;
+    const int ncp = PL > 0 ? colhist4p_ncolp(T, p.radius) : ch4_stride(T + 2 * p.radius);
     const size_t smem = (PL > 0 ? (size_t)colhist4p_bytes(T, p.radius, PL) : (size_t)colhist4_bytes(T, p.radius)) +
-                        2 * 256 * sizeof(int);
-    auto kern = k_colhist16_u16<T, G, M, PL>;
+                        (wk ? (size_t)ncp * 4 : 0) + (2 * 256 + 2) * sizeof(int);
+    auto kern = wk ? k_colhist16_u16<T, G, M, PL, true> : k_colhist16_u16<T, G, M, PL, false>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
@@ -36,30 +39,30 @@ static int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s) {
 }
 
 template <int T, int G, int PL>
-static int run_colhist16_u16_g(SlabParams p, int B, cudaStream_t s) {
+static int run_colhist16_u16_g(SlabParams p, int B, cudaStream_t s, bool wk) {
     switch ((2 * p.radius + 1) % G) {
-        case 1: return run_colhist16_u16_gm<T, G, (G > 1 ? 1 : 0), PL>(p, B, s);
-        case 3: return run_colhist16_u16_gm<T, G, (G > 3 ? 3 : 0), PL>(p, B, s);
-        case 5: return run_colhist16_u16_gm<T, G, (G > 5 ? 5 : 0), PL>(p, B, s);
-        case 7: return run_colhist16_u16_gm<T, G, (G > 7 ? 7 : 0), PL>(p, B, s);
-        default: return run_colhist16_u16_gm<T, G, 0, PL>(p, B, s);
+        case 1: return run_colhist16_u16_gm<T, G, (G > 1 ? 1 : 0), PL>(p, B, s, wk);
+        case 3: return run_colhist16_u16_gm<T, G, (G > 3 ? 3 : 0), PL>(p, B, s, wk);
+        case 5: return run_colhist16_u16_gm<T, G, (G > 5 ? 5 : 0), PL>(p, B, s, wk);
+        case 7: return run_colhist16_u16_gm<T, G, (G > 7 ? 7 : 0), PL>(p, B, s, wk);
+        default: return run_colhist16_u16_gm<T, G, 0, PL>(p, B, s, wk);
     }
 }
 
-int run_colhist16_u16(SlabParams p, int B, cudaStream_t s) {
+int run_colhist16_u16(SlabParams p, int B, cudaStream_t s, bool wk) {
     const int n = 2 * p.radius + 1;
     // pair records (upper levels) where two 256-thread CTAs per SM still fit
-    const int lim = 113 * 1024 - 2 * 256 * (int)sizeof(int);
+    const int lim = 113 * 1024 - (2 * 256 + 2) * (int)sizeof(int) - ch4_stride(256 + 2 * p.radius) * 4;
     const int pl = env_int("MTB_CH16_PL", colhist4p_bytes(256, p.radius, 3) <= lim ? 3
                                           : colhist4p_bytes(256, p.radius, 2) <= lim ? 2 : 0);
     if (8 * n <= 255) {
-        if (pl == 3) return run_colhist16_u16_g<256, 8, 3>(p, B, s);
-        if (pl == 2) return run_colhist16_u16_g<256, 8, 2>(p, B, s);
-        return run_colhist16_u16_g<256, 8, 0>(p, B, s);
+        if (pl == 3) return run_colhist16_u16_g<256, 8, 3>(p, B, s, wk);
+        if (pl == 2) return run_colhist16_u16_g<256, 8, 2>(p, B, s, wk);
+        return run_colhist16_u16_g<256, 8, 0>(p, B, s, wk);
     }
-    if (4 * n <= 255) return pl >= 2 ? run_colhist16_u16_g<256, 4, 2>(p, B, s) : run_colhist16_u16_g<256, 4, 0>(p, B, s);
-    if (2 * n <= 255) return run_colhist16_u16_g<256, 2, 0>(p, B, s);
-    return run_colhist16_u16_g<256, 1, 0>(p, B, s);
+    if (4 * n <= 255) return pl >= 2 ? run_colhist16_u16_g<256, 4, 2>(p, B, s, wk) : run_colhist16_u16_g<256, 4, 0>(p, B, s, wk);
+    if (2 * n <= 255) return run_colhist16_u16_g<256, 2, 0>(p, B, s, wk);
+    return run_colhist16_u16_g<256, 1, 0>(p, B, s, wk);
 }
 
 
@@ -68,7 +71,7 @@ static int run_colhist16s_u16_gm(SlabParams p, int B, cudaStream_t s) {
     const int n = 2 * p.radius + 1, NCOL = T + 2 * p.radius;
     const size_t smem = (size_t)colhist4_bytes(T, p.radius) + 16 * T * 2 + ((size_t)(n * T + 15) & ~(size_t)15) +
                         (size_t)NCOL * n * 2;
-    if (smem > 220 * 1024) return run_colhist16_u16(p, B, s);  // sorted columns too large: two-phase kernel
+    if (smem > 220 * 1024) return run_colhist16_u16(p, B, s, false);  // sorted columns too large: two-phase kernel
     auto kern = k_colhist16s_u16<T, G, M>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;

@@ -380,8 +380,9 @@ def test_colhist_variants_all_group_tails(var, name, monkeypatch):
             assert np.array_equal(out, O.iot_filter(img, n, rank=rank)), (var, r, rank)
 
 
-@pytest.mark.parametrize("kind", ["compact", "uniform"])
-def test_colhist16_u16_two_phase(kind, monkeypatch):
+@pytest.mark.parametrize("wk", ["1", "0"])
+@pytest.mark.parametrize("kind", ["compact", "uniform", "two_level"])
+def test_colhist16_u16_two_phase(kind, wk, monkeypatch):
     """k_colhist16_u16 (high byte by column records, then one low-byte sweep
     per high byte used by the tile) at radii covering every group size/tail,
     ragged tiles, min / max / off-centre ranks; the uniform image makes many
@@ -389,10 +390,14 @@ def test_colhist16_u16_two_phase(kind, monkeypatch):
     from paper_1105_3829_b200 import _lib
 
     monkeypatch.setenv("MTB_KERNEL", "colhist")
-    rng = np.random.default_rng(123 if kind == "compact" else 321)
+    monkeypatch.setenv("MTB_CH16_WK", wk)  # window-keyed first sweep on / off
+    rng = np.random.default_rng({"compact": 123, "uniform": 321, "two_level": 55}[kind])
     h, w = 150, 300
     if kind == "compact":
         px = (20000 + rng.normal(0, 250, (h, w))).clip(0, 65535).astype(np.uint16)
+    elif kind == "two_level":  # tiles straddling the step miss the guessed high byte
+        px = (np.where(np.arange(w)[None, :] < 170, 20000, 41000) + rng.normal(0, 200, (h, w)))
+        px = px.clip(0, 65535).astype(np.uint16)
     else:
         px = rng.integers(0, 65536, (h, w)).astype(np.uint16)
     for r in (1, 2, 3, 4, 5, 7, 8, 15, 16, 31, 32, 63, 64, 127):
