@@ -41,7 +41,11 @@ __host__ __device__ inline ColhistGeom colhist_geom(int T, int S, int r) {
     ColhistGeom g;
     g.TW = T * S;
     g.NC = g.TW + 2 * r;
+    // phase length padded so a record row is a multiple of 8 records (32
+    // words): the per-column byte updates then fall in bank 4c+byte/4
+    // whatever the chunk (measured: a radix-4 kernel gained 20% this way)
     g.NCS = (g.NC + S - 1) / S;
+    g.NCS = (g.NCS + (8 / S > 0 ? 8 / S : 1) - 1) / (8 / S > 0 ? 8 / S : 1) * (8 / S > 0 ? 8 / S : 1);
     g.NPOS = g.NCS * S;
     g.bytes = 17 * g.NPOS * 16;
     return g;

@@ -116,12 +116,11 @@ int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
     int var = env_int("MTB_CH_VAR", -1);
     if (var < 0) {
         // measured on config 2 (tools/probe.py sweep):
-        // 16-bin records for r <= 5; radix-4 records for 6..10 (16-bin with
-        // two pixels per thread at r = 8); from r = 11, radix-4 with pair
+        // 16-bin records for r <= 5; radix-4 records for 6..10; from r = 11,
+        // radix-4 with pair
         // records for as many upper levels as keep two 256-thread CTAs per SM
         const int r = p.radius, lim = 113 * 1024;
         var = r <= 5 ? 0
-              : r == 8 ? 2
               : r <= 10 ? 12
               : (r <= 16 && colhist4p_bytes(256, r, 3) <= lim) ? 30
               : colhist4p_bytes(256, r, 2) <= lim ? 31
