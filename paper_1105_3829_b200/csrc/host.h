@@ -45,6 +45,8 @@ inline int launch(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, 
 
 // kernel families in their own translation units
 int run_colhist_u8(SlabParams p, int B, cudaStream_t s);
+int run_colhist4_256(SlabParams p, int B, cudaStream_t s);
+int run_colhist4p_256(SlabParams p, int B, cudaStream_t s, int pl);
 // wk: window-keyed first sweep (pays off on compact data, see kernel)
 int run_colhist16_u16(SlabParams p, int B, cudaStream_t s, bool wk = true);
 int run_colhist16s_u16(SlabParams p, int B, cudaStream_t s);

@@ -313,43 +313,9 @@ __host__ __device__ constexpr int ch4p_recs(int PL) { return PL >= 3 ? 21 : (PL 
 // record rows padded to a multiple of 32 columns (conflict-free updates;
 // pair and quad alignment)
 __host__ __device__ inline int colhist4p_ncolp(int T, int r) { return (T + 2 * r + 31) & ~31; }
-__host__ __device__ inline int colhist4p_bytes(int T, int r, int PL, int QL = 0) {
+__host__ __device__ inline int colhist4p_bytes(int T, int r, int PL) {
     const int ncp = colhist4p_ncolp(T, r);
-    return (CH4_RECS * ncp + ch4p_recs(PL) * (ncp / 2) + ch4p_recs(QL) * (ncp / 4) * (QL > 0)) * 4;
-}
-
-// window of one level from QUAD records (columns 4q..4q+3) for the aligned
-// middle of [a, a+n), pair and single records for the 0-3 columns at
-// either end (predicated loads: the head/tail shape differs per lane).
-// Quad counts are <= 4n: GQ quads per carry-free group.
-template <int GQ>
-__device__ __forceinline__ void ch4q_gather(const uint32_t *qr, const uint32_t *pr, const uint32_t *sr, int a, int n,
-                                            uint32_t &w0, uint32_t &w1) {
-    const int b = a + n;
-    const int a4 = (a + 3) & ~3, b4 = b & ~3;
-    const int h = a4 - a, t = b - b4;
-    const uint32_t hv = ((h & 1) ? sr[a] : 0u) + ((h & 2) ? pr[(a + (h & 1)) >> 1] : 0u);
-    const uint32_t tv = ((t & 2) ? pr[b4 >> 1] : 0u) + ((t & 1) ? sr[b4 + (t & 2)] : 0u);
-    w0 = __byte_perm(hv, 0, 0x4140) + __byte_perm(tv, 0, 0x4140);
-    w1 = __byte_perm(hv, 0, 0x4342) + __byte_perm(tv, 0, 0x4342);
-    const uint32_t *rp = qr + (a4 >> 2);
-    const int nq = (b4 - a4) >> 2;
-    int j = 0;
-    for (; j + GQ <= nq; j += GQ) {
-        uint32_t v = 0;
-#pragma unroll
-        for (int q = 0; q < GQ; ++q) v += rp[j + q];
-        w0 += __byte_perm(v, 0, 0x4140);
-        w1 += __byte_perm(v, 0, 0x4342);
-    }
-    if (GQ > 1 && j < nq) {
-        uint32_t v = 0;
-#pragma unroll
-        for (int q = 0; q < GQ - 1; ++q)
-            if (j + q < nq) v += rp[j + q];
-        w0 += __byte_perm(v, 0, 0x4140);
-        w1 += __byte_perm(v, 0, 0x4342);
-    }
+    return (CH4_RECS * ncp + ch4p_recs(PL) * (ncp / 2)) * 4;
 }
 
 // window of one level from pair records (np = (n-1)/2 pairs from kp) plus
@@ -379,6 +345,7 @@ __device__ __forceinline__ void ch4p_gather(const uint32_t *pr, const uint32_t *
         w1 += __byte_perm(t, 0, 0x4342);
     }
 }
+
 
 // the 4-level selection of the rank-k element (k updated to the rank within
 // the selected value) from the records of the window starting at rp (= record
@@ -589,8 +556,8 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
 // resolved right there (5 gathers instead of phase A + phase B's 8); the
 // rest (marked in the high-byte plane) go through phases A and B, which
 // then skip H0.
-template <int T, int G, int M, int PL, bool WK>
-__global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__restrict__ hplane) {
+template <int T, int G, int M, int PL>
+__global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__restrict__ hplane, bool WK) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int r = p.radius, W = p.W, n = 2 * r + 1;
@@ -600,7 +567,7 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
     uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCP]
     uint32_t *prs = rec + CH4_RECS * NCP;                     // [PR][NPR] (PL > 0)
     uint32_t *rec3 = prs + (PL > 0 ? ch4p_recs(PL) * NPR : 0);  // [NCP] below/equal/above H0 (WK)
-    int *hfirst = reinterpret_cast<int *>(rec3 + (WK ? NCP : 0));  // [256]
+    int *hfirst = reinterpret_cast<int *>(rec3 + NCP);             // [256]
     int *hlast = hfirst + 256;                                      // [256]
     int *flags = hlast + 256;                                       // [0]: H0, [1]: any miss
     const int X0 = blockIdx.x * T;
@@ -885,21 +852,16 @@ namespace mtb {
 // pair changes with shared-memory atomics (adjacent columns belong to
 // adjacent threads); counts never go below zero, so a per-byte decrement
 // never borrows across bytes.
-template <int T, int G, int M, int PL, int QL, bool STREAM>
+template <int T, int G, int M, int PL, bool STREAM>
 __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
-    static_assert(QL <= PL && QL <= 2 && (QL == 0 || G >= 4), "quad levels need pairs and 4n <= 255");
     constexpr int GP = G / 2;
-    constexpr int GQ = G >= 4 ? G / 4 : 1;
     constexpr int PR = ch4p_recs(PL);
-    constexpr int QR = QL > 0 ? ch4p_recs(QL) : 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
     const int NCOL = T + 2 * r, NCP = colhist4p_ncolp(T, r), NPR = NCP / 2;
     uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCP] singles
     uint32_t *prs = rec + CH4_RECS * NCP;                     // [PR][NPR] pairs
-    const int NQ = NCP / 4;
-    uint32_t *qrs = prs + PR * NPR;                            // [QR][NQ] quads
     uint8_t *recb = smem_raw;
     const int X0 = blockIdx.x * T;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
@@ -922,11 +884,6 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         const int row = i / NPR, k = i - row * NPR;
         prs[i] = rec[row * NCP + 2 * k] + rec[row * NCP + 2 * k + 1];
     }
-    for (int i = tid; i < QR * NQ; i += T) {
-        const int row = i / NQ, q = i - row * NQ;
-        const uint32_t *sr = rec + row * NCP + 4 * q;
-        qrs[i] = sr[0] + sr[1] + sr[2] + sr[3];
-    }
     // pair updates: levels 0-2 of value v, +-1 in the byte of the next digit
     auto pbump = [&](int c, unsigned v, int d) {
         const int k = c >> 1;
@@ -934,9 +891,6 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         atomicAdd(prs + 0 * NPR + k, one << (8 * (v >> 6)));
         if (PL >= 2) atomicAdd(prs + (1 + (v >> 6)) * NPR + k, one << (8 * ((v >> 4) & 3)));
         if (PL >= 3) atomicAdd(prs + (5 + (v >> 4)) * NPR + k, one << (8 * ((v >> 2) & 3)));
-        const int q = c >> 2;
-        if (QL >= 1) atomicAdd(qrs + q, one << (8 * (v >> 6)));
-        if (QL >= 2) atomicAdd(qrs + (1 + (v >> 6)) * NQ + q, one << (8 * ((v >> 4) & 3)));
     };
     constexpr int CH_PF = 2;
     int gxs[CH_PF];
@@ -985,14 +939,9 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         }
         __syncthreads();
         uint32_t k = p.rank, w0, w1;
-        if (QL >= 1)
-            ch4q_gather<GQ>(qrs, prs, rec, tid, n, w0, w1);
-        else
-            ch4p_gather<GP>(prs, rec, kp, cs, np, w0, w1);
+        ch4p_gather<GP>(prs, rec, kp, cs, np, w0, w1);
         const int d3 = ch4_descend(w0, w1, k);
-        if (QL >= 2)
-            ch4q_gather<GQ>(qrs + (1 + d3) * NQ, prs + (1 + d3) * NPR, rec + (1 + d3) * NCP, tid, n, w0, w1);
-        else if (PL >= 2)
+        if (PL >= 2)
             ch4p_gather<GP>(prs + (1 + d3) * NPR, rec + (1 + d3) * NCP, kp, cs, np, w0, w1);
         else
             ch4_gather<G, M>(rec + (1 + d3) * NCP + tid, n, w0, w1);

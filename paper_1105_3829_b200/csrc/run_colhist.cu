@@ -78,37 +78,8 @@ static int run_colhist4_u8(SlabParams p, int B, cudaStream_t s, const char *name
     return run_colhist4_u8_g<T, 1>(p, B, s, name);
 }
 
-template <int T, int G, int M, int PL, int QL = 0>
-static int run_colhist4p_u8_gm(SlabParams p, int B, cudaStream_t s, const char *name) {
-    const size_t smem = (size_t)colhist4p_bytes(T, p.radius, PL, QL);
-    auto kern = p.in_rows ? k_colhist4p_u8<T, G, M, PL, QL, true> : k_colhist4p_u8<T, G, M, PL, QL, false>;
-    if (int rc = set_smem(kern, smem)) return rc;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int bx = (p.W + T - 1) / T;
-    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm);
-    dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
-    return launch(kern, grid, T, smem, s, p, name);
-}
-
-// pair records (G even: n <= 127); PL pair levels, QL quad levels (4n <= 255)
-template <int T, int PL, int QL = 0>
-static int run_colhist4p_u8(SlabParams p, int B, cudaStream_t s, const char *name) {
-    const int n = 2 * p.radius + 1;
-    if (8 * n <= 255) {
-        switch (n % 8) {
-            case 1: return run_colhist4p_u8_gm<T, 8, 1, PL, QL>(p, B, s, name);
-            case 3: return run_colhist4p_u8_gm<T, 8, 3, PL, QL>(p, B, s, name);
-            case 5: return run_colhist4p_u8_gm<T, 8, 5, PL, QL>(p, B, s, name);
-            default: return run_colhist4p_u8_gm<T, 8, 7, PL, QL>(p, B, s, name);
-        }
-    }
-    if (4 * n <= 255) return n % 4 == 1 ? run_colhist4p_u8_gm<T, 4, 1, PL, QL>(p, B, s, name)
-                                        : run_colhist4p_u8_gm<T, 4, 3, PL, QL>(p, B, s, name);
-    if (2 * n <= 255) return run_colhist4p_u8_gm<T, 2, 1, PL>(p, B, s, name);
-    return run_colhist4_u8<T>(p, B, s, "k_colhist4_u8<256>");  // pair counts would overflow u8
-}
+// radix-4 records, 256 threads (also the pair kernels' wide-window fallback)
+int run_colhist4_256(SlabParams p, int B, cudaStream_t s) { return run_colhist4_u8<256>(p, B, s, "k_colhist4_u8<256>"); }
 
 // 8-bit column-histogram gather kernels; the variant by radius is below.
 // MTB_CH_VAR forces one.
@@ -129,13 +100,9 @@ int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
     switch (var) {
         case 0: return run_colhist_u8_ts<128, 1>(p, B, s, "k_colhist_u8<128,1>");
         case 2: return run_colhist_u8_ts<128, 2>(p, B, s, "k_colhist_u8<128,2>");
-        case 30: return run_colhist4p_u8<256, 3>(p, B, s, "k_colhist4p_u8<256,3>");
-        case 31: return run_colhist4p_u8<256, 2>(p, B, s, "k_colhist4p_u8<256,2>");
-        case 34: return run_colhist4p_u8<256, 1>(p, B, s, "k_colhist4p_u8<256,1>");
-        case 40: return run_colhist4p_u8<256, 3, 2>(p, B, s, "k_colhist4p_u8<256,3,q2>");
-        case 41: return run_colhist4p_u8<256, 2, 2>(p, B, s, "k_colhist4p_u8<256,2,q2>");
-        case 42: return run_colhist4p_u8<256, 3, 1>(p, B, s, "k_colhist4p_u8<256,3,q1>");
-        case 43: return run_colhist4p_u8<256, 2, 1>(p, B, s, "k_colhist4p_u8<256,2,q1>");
+        case 30: return run_colhist4p_256(p, B, s, 3);
+        case 31: return run_colhist4p_256(p, B, s, 2);
+        case 34: return run_colhist4p_256(p, B, s, 1);
         default: return run_colhist4_u8<256>(p, B, s, "k_colhist4_u8<256>");
     }
 }

@@ -13,8 +13,8 @@ static int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s, bool wk) {
     wk = env_int("MTB_CH16_WK", wk ? 1 : 0) != 0;
     const int ncp = PL > 0 ? colhist4p_ncolp(T, p.radius) : ch4_stride(T + 2 * p.radius);
     const size_t smem = (PL > 0 ? (size_t)colhist4p_bytes(T, p.radius, PL) : (size_t)colhist4_bytes(T, p.radius)) +
-                        (wk ? (size_t)ncp * 4 : 0) + (2 * 256 + 2) * sizeof(int);
-    auto kern = wk ? k_colhist16_u16<T, G, M, PL, true> : k_colhist16_u16<T, G, M, PL, false>;
+                        (size_t)ncp * 4 + (2 * 256 + 2) * sizeof(int);
+    auto kern = k_colhist16_u16<T, G, M, PL>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
@@ -29,7 +29,7 @@ static int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s, bool wk) {
     if (cudaMallocAsync(reinterpret_cast<void **>(&hplane), hbytes, s) != cudaSuccess)
         return fail(MTB_E_CUDA, "k_colhist16_u16: scratch allocation failed");
     if (int rc = set_smem(kern, smem)) return rc;
-    kern<<<grid, T, smem, s>>>(p, hplane);
+    kern<<<grid, T, smem, s>>>(p, hplane, wk);
     cudaError_t e = cudaGetLastError();
     cudaFreeAsync(hplane, s);
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_colhist16_u16: ") + cudaGetErrorString(e));
@@ -65,43 +65,5 @@ int run_colhist16_u16(SlabParams p, int B, cudaStream_t s, bool wk) {
     return run_colhist16_u16_g<256, 1, 0>(p, B, s, wk);
 }
 
-
-template <int T, int G, int M>
-static int run_colhist16s_u16_gm(SlabParams p, int B, cudaStream_t s) {
-    const int n = 2 * p.radius + 1, NCOL = T + 2 * p.radius;
-    const size_t smem = (size_t)colhist4_bytes(T, p.radius) + 16 * T * 2 + ((size_t)(n * T + 15) & ~(size_t)15) +
-                        (size_t)NCOL * n * 2;
-    if (smem > 220 * 1024) return run_colhist16_u16(p, B, s, false);  // sorted columns too large: two-phase kernel
-    auto kern = k_colhist16s_u16<T, G, M>;
-    if (int rc = set_smem(kern, smem)) return rc;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int bx = (p.W + T - 1) / T;
-    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm);
-    if (p.rows_per_cta < 2 * n) p.rows_per_cta = std::min(2 * n, p.row_end - p.row_begin);
-    dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
-    return launch(kern, grid, T, smem, s, p, "k_colhist16s_u16");
-}
-
-template <int T, int G>
-static int run_colhist16s_u16_g(SlabParams p, int B, cudaStream_t s) {
-    switch ((2 * p.radius + 1) % G) {
-        case 1: return run_colhist16s_u16_gm<T, G, (G > 1 ? 1 : 0)>(p, B, s);
-        case 3: return run_colhist16s_u16_gm<T, G, (G > 3 ? 3 : 0)>(p, B, s);
-        case 5: return run_colhist16s_u16_gm<T, G, (G > 5 ? 5 : 0)>(p, B, s);
-        case 7: return run_colhist16s_u16_gm<T, G, (G > 7 ? 7 : 0)>(p, B, s);
-        default: return run_colhist16s_u16_gm<T, G, 0>(p, B, s);
-    }
-}
-
-// widely spread 16-bit data; sorted columns need n <= 255 (u8 run starts)
-int run_colhist16s_u16(SlabParams p, int B, cudaStream_t s) {
-    const int n = 2 * p.radius + 1;
-    if (8 * n <= 255) return run_colhist16s_u16_g<128, 8>(p, B, s);
-    if (4 * n <= 255) return run_colhist16s_u16_g<128, 4>(p, B, s);
-    if (2 * n <= 255) return run_colhist16s_u16_g<128, 2>(p, B, s);
-    return run_colhist16s_u16_g<128, 1>(p, B, s);
-}
 
 }  // namespace mtb
