@@ -307,7 +307,8 @@ def run_ours(args):
         e2e = {"value": round(len(RADII) * H * W * ws / dt / 1e6, 3), "unit": UNIT,
                "h2d_bytes_per_step": len(RADII) * H * W, "d2h_bytes_per_step": len(RADII) * H * W,
                "api": "paper_1105_3829_b200.filter_host_buffer -> mtb_filter_host (C ABI, pinned host "
-                      "frames, row bands pipelined copy/filter/copy)"}
+                      "frames; copies overlapped with filtering: row bands for r < 12, one streaming "
+                      "launch fed by stream memory ops for r >= 12)"}
 
     if rank != 0:
         if pg:
