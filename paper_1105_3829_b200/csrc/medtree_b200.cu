@@ -13,6 +13,7 @@
 #include "host.h"
 #include "kernels_vert.cuh"
 #include "kernels_sortnet.cuh"
+#include "kernels_med3.cuh"
 #include "kernels_select.cuh"
 #include <cstdlib>
 
@@ -159,8 +160,31 @@ static bool sortnet_applies(const SlabParams &p) {
     return n <= 7 && (uint32_t)((n * n + 1) / 2) == p.rank;
 }
 
+// 3x3 median of 8-bit frames (k_med3_u8): row bands sized so the grid is
+// one wave of resident CTAs
+static int run_med3(SlabParams p, int B, cudaStream_t s) {
+    const int rows = p.row_end - p.row_begin;
+    const int bx = (p.W + 1023) / 1024;
+    int per_sm = 4;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_med3_u8, 128, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t slots = (int64_t)sm_count() * per_sm;
+    int64_t bands = slots / ((int64_t)bx * B);
+    if (bands < 1) bands = 1;
+    int rt = (int)((rows + bands - 1) / bands);
+    const int min_rt = env_int("MTB_MED3_MIN_RT", 8);
+    if (rt < min_rt) rt = min_rt;
+    if (rt > rows) rt = rows;
+    p.rows_per_cta = rt;
+    dim3 grid(bx, (rows + rt - 1) / rt, B);
+    return launch(k_med3_u8, grid, 128, 0, s, p, "k_med3_u8");
+}
+
 template <typename P>
 static int run_sortnet(SlabParams p, int B, cudaStream_t s) {
+    if (sizeof(P) == 1 && p.radius == 1 && strcmp(forced_kernel(), "sortnet") != 0 &&
+        (int64_t)p.src_rows * p.src_pitch < (1ll << 31))
+        return run_med3(p, B, s);
     switch (p.radius) {
         case 1: return run_sortnet_n<3, 4, 8, P>(p, B, s, "k_sortnet<3>");
         case 2:
@@ -220,7 +244,7 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     //   8-bit, r <= 31 (any rank)                 -> column-histogram gather
     //   8-bit, 32 <= r <= 127                     -> CTMF tiles (O(1) in r)
     //   otherwise                                 -> per-column vertical histograms
-    if ((force.empty() || force == "sortnet") && sortnet_applies<P>(p) &&
+    if ((force.empty() || force == "sortnet" || force == "med3") && sortnet_applies<P>(p) &&
         (sizeof(P) == 2 || p.radius <= 2 || force == "sortnet"))
         return run_sortnet<P>(p, B, s);
     if (sizeof(P) == 1 && p.radius <= 63 && force == "lob") return run_lob_u8_32(p, B, s);
