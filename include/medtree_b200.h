@@ -89,6 +89,19 @@ int mtb_median_batch_u16(const uint16_t *src, int64_t src_image_stride, int64_t 
 int mtb_filter_host(const void *src, void *dst, int32_t bit_depth, int32_t H, int32_t W,
                     int32_t radius, int64_t rank, const void *lut, uint32_t flags);
 
+/* A sequence of n_frames HOST frames of one geometry (e.g. a video, or one
+ * frame at several radii), each filtered as by mtb_filter_host, with the
+ * copies of neighbouring frames overlapped: frame i+1 goes host->device and
+ * frame i-1 device->host while frame i is filtered (a ring of 3 device
+ * buffer pairs).  srcs[i] / dsts[i]: host frames [H][W] (page-locked for
+ * asynchronous copies); radii[i]: window radius; ranks: per-frame 1-based
+ * rank, or NULL for the median.  Synchronous: returns when every result is
+ * on the host.  The batched form of the reference's per-image
+ * filter_image / WindowEngine.run loop (engine.py:162-184, :209-262). */
+int mtb_filter_host_frames(const void *const *srcs, void *const *dsts, const int32_t *radii,
+                           const int64_t *ranks, int32_t n_frames, int32_t bit_depth,
+                           int32_t H, int32_t W, const void *lut, uint32_t flags);
+
 /* Independent exact selection on DEVICE buffers: per pixel, the bits of the
  * rank-th smallest window value are decided from the top by counting passes
  * over the n x n replicate-clamped window (O(d * n^2) per pixel).  Shares no

@@ -26,6 +26,7 @@ EXPORTS = (
     "mtb_median_batch_u8",
     "mtb_median_batch_u16",
     "mtb_filter_host",
+    "mtb_filter_host_frames",
     "mtb_rank_bruteforce",
     "mtb_launch_count",
     "mtb_last_kernel",
@@ -67,6 +68,7 @@ def load() -> ctypes.CDLL:
             ("mtb_median_batch_u8", batch),
             ("mtb_median_batch_u16", batch),
             ("mtb_filter_host", [p, p, i32, i32, i32, i32, i64, p, u32]),
+            ("mtb_filter_host_frames", [p, p, p, p, i32, i32, i32, i32, p, u32]),
             ("mtb_rank_bruteforce", [p, i64, p, i64, i32, i32, i32, i32, i64, p]),
         ):
             fn = getattr(lib, name)

@@ -566,6 +566,113 @@ static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W
     return rc ? rc : rs;
 }
 
+// ---- sequence of host frames (mtb_filter_host_frames): whole-frame jobs on
+// a ring of NB device buffer pairs.  Job i's host->device copy (copy stream)
+// waits only for job i-NB's filter to release its source buffer; its filter
+// (compute stream) waits for its copy and for job i-NB's device->host copy
+// to release the destination buffer; its device->host copy waits for its
+// filter.  So frame i+1 arrives and frame i-1 leaves while frame i is being
+// filtered: the copy engines and the SMs stay busy across the sequence.
+struct FramesCtx {
+    static constexpr int NB = 3;
+    int dev = -1;
+    void *dsrc[NB] = {}, *ddst[NB] = {}, *dlut = nullptr;
+    size_t cap = 0;
+    cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
+    cudaEvent_t ein[NB], ek[NB], eout[NB];
+};
+static FramesCtx g_frames[64];
+
+static int frames_ctx(FramesCtx *&ctx, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return fail(MTB_E_CUDA, "device index out of range");
+    ctx = &g_frames[dev];
+    auto ok = [](cudaError_t e, const char *what) {
+        return e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    if (ctx->dev < 0) {
+        int rc = ok(cudaStreamCreateWithFlags(&ctx->sh, cudaStreamNonBlocking), "cudaStreamCreate");
+        if (!rc) rc = ok(cudaStreamCreateWithFlags(&ctx->sc, cudaStreamNonBlocking), "cudaStreamCreate");
+        if (!rc) rc = ok(cudaStreamCreateWithFlags(&ctx->sd, cudaStreamNonBlocking), "cudaStreamCreate");
+        if (!rc) rc = ok(cudaMalloc(&ctx->dlut, 65536 * 2), "cudaMalloc");
+        for (int j = 0; j < FramesCtx::NB && !rc; ++j) {
+            rc = ok(cudaEventCreateWithFlags(&ctx->ein[j], cudaEventDisableTiming), "cudaEventCreate");
+            if (!rc) rc = ok(cudaEventCreateWithFlags(&ctx->ek[j], cudaEventDisableTiming), "cudaEventCreate");
+            if (!rc) rc = ok(cudaEventCreateWithFlags(&ctx->eout[j], cudaEventDisableTiming), "cudaEventCreate");
+        }
+        if (rc) return rc;
+        ctx->dev = dev;
+    }
+    if (ctx->cap < bytes) {
+        cudaDeviceSynchronize();
+        for (int j = 0; j < FramesCtx::NB; ++j) {
+            if (ctx->dsrc[j]) cudaFree(ctx->dsrc[j]);
+            if (ctx->ddst[j]) cudaFree(ctx->ddst[j]);
+            ctx->dsrc[j] = ctx->ddst[j] = nullptr;
+        }
+        ctx->cap = 0;
+        for (int j = 0; j < FramesCtx::NB; ++j) {
+            if (int rc = ok(cudaMalloc(&ctx->dsrc[j], bytes), "cudaMalloc")) return rc;
+            if (int rc = ok(cudaMalloc(&ctx->ddst[j], bytes), "cudaMalloc")) return rc;
+        }
+        ctx->cap = bytes;
+    }
+    return MTB_OK;
+}
+
+static int host_frames(const void *const *srcs, void *const *dsts, const int32_t *radii, const int64_t *ranks,
+                       int n, int bit_depth, int H, int W, const void *lut, uint32_t flags) {
+    std::lock_guard<std::mutex> lock(g_host_mu);
+    const size_t es = bit_depth == 8 ? 1 : 2;
+    const size_t bytes = (size_t)H * W * es;
+    FramesCtx *ctx = nullptr;
+    if (int rc = frames_ctx(ctx, bytes)) return rc;
+    auto ok = [](cudaError_t e, const char *what) {
+        return e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    int rc = MTB_OK;
+    if (lut) {
+        rc = ok(cudaMemcpyAsync(ctx->dlut, lut, ((size_t)1 << bit_depth) * es, cudaMemcpyHostToDevice, ctx->sc),
+                "H2D lut");
+    }
+    constexpr int NB = FramesCtx::NB;
+    for (int i = 0; i < n && rc == MTB_OK; ++i) {
+        const int j = i % NB;
+        if (!srcs[i] || !dsts[i]) {
+            rc = fail(MTB_E_INVAL, "null src/dst pointer (frame " + std::to_string(i) + ")");
+            break;
+        }
+        if (i >= NB) cudaStreamWaitEvent(ctx->sh, ctx->ek[j], 0);  // job i-NB done reading dsrc[j]
+        rc = ok(cudaMemcpyAsync(ctx->dsrc[j], srcs[i], bytes, cudaMemcpyHostToDevice, ctx->sh), "H2D");
+        if (rc) break;
+        cudaEventRecord(ctx->ein[j], ctx->sh);
+        cudaStreamWaitEvent(ctx->sc, ctx->ein[j], 0);
+        if (i >= NB) cudaStreamWaitEvent(ctx->sc, ctx->eout[j], 0);  // job i-NB's result copied out
+        if (bit_depth == 16)
+            g_spread_hint = spread_distinct_host(static_cast<const uint16_t *>(srcs[i]), W, H, W);
+        SlabParams p = make_params(ctx->dsrc[j], W, 0, H, ctx->ddst[j], W, H, W, 0, H, radii[i],
+                                   ranks ? ranks[i] : 0, lut ? ctx->dlut : nullptr);
+        if (!ranks) {
+            const int64_t nn = 2 * (int64_t)radii[i] + 1;
+            p.rank = (uint32_t)((nn * nn + 1) / 2);
+        }
+        (void)flags;
+        rc = bit_depth == 8 ? run<uint8_t>(p, 1, ctx->sc) : run<uint16_t>(p, 1, ctx->sc);
+        g_spread_hint = -1;
+        if (rc) break;
+        cudaEventRecord(ctx->ek[j], ctx->sc);
+        cudaStreamWaitEvent(ctx->sd, ctx->ek[j], 0);
+        rc = ok(cudaMemcpyAsync(dsts[i], ctx->ddst[j], bytes, cudaMemcpyDeviceToHost, ctx->sd), "D2H");
+        if (rc) break;
+        cudaEventRecord(ctx->eout[j], ctx->sd);
+    }
+    const int r1 = ok(cudaStreamSynchronize(ctx->sd), "cudaStreamSynchronize");
+    const int r2 = ok(cudaStreamSynchronize(ctx->sc), "cudaStreamSynchronize");
+    const int r3 = ok(cudaStreamSynchronize(ctx->sh), "cudaStreamSynchronize");
+    return rc ? rc : (r1 ? r1 : (r2 ? r2 : r3));
+}
+
 extern "C" {
 
 int mtb_median_u8(const uint8_t *src, int64_t src_pitch, int32_t src_row0, int32_t src_rows,
@@ -617,6 +724,18 @@ int mtb_filter_host(const void *src, void *dst, int32_t bit_depth, int32_t H, in
     if (!src || !dst) return fail(MTB_E_INVAL, "null src/dst pointer");
     if (H < 1 || W < 1) return fail(MTB_E_INVAL, "pixels must be a non-empty 2D array");
     return host_pipeline(src, dst, bit_depth, H, W, radius, rank, lut, flags);
+}
+
+int mtb_filter_host_frames(const void *const *srcs, void *const *dsts, const int32_t *radii, const int64_t *ranks,
+                           int32_t n_frames, int32_t bit_depth, int32_t H, int32_t W, const void *lut,
+                           uint32_t flags) {
+    if (bit_depth != 8 && bit_depth != 16)
+        return fail(MTB_E_INVAL, "bit_depth must be 8 or 16, got " + std::to_string(bit_depth));
+    if (n_frames < 0) return fail(MTB_E_INVAL, "n_frames must be >= 0");
+    if (n_frames == 0) return MTB_OK;
+    if (!srcs || !dsts || !radii) return fail(MTB_E_INVAL, "null srcs/dsts/radii array");
+    if (H < 1 || W < 1) return fail(MTB_E_INVAL, "pixels must be a non-empty 2D array");
+    return host_frames(srcs, dsts, radii, ranks, n_frames, bit_depth, H, W, lut, flags);
 }
 
 int mtb_rank_bruteforce(const void *src, int64_t src_pitch, void *dst, int64_t dst_pitch, int32_t bit_depth,

@@ -271,3 +271,56 @@ def filter_host_buffer(src: np.ndarray, radius: int, rank: int | None = None,
         int(radius), int(rank), lut_ptr, _lib.FLAG_ADAPTIVE if adaptive else 0)
     _lib.check(rc)
     return dst
+
+
+def filter_host_frames(srcs, radii, ranks=None, lut: np.ndarray | None = None,
+                       outs=None) -> list:
+    """A sequence of host frames of one shape and dtype through the C ABI's
+    multi-frame HOST entry (mtb_filter_host_frames): frame i+1's copy in and
+    frame i-1's copy out overlap frame i's filtering.  ``radii``: one radius
+    per frame (or one int for all); ``ranks``: per-frame 1-based ranks or
+    None (medians); ``outs``: optional C-contiguous destinations.  Page-locked
+    frames (numpy views of pinned torch tensors) make the copies
+    asynchronous.  Returns the list of filtered frames."""
+    srcs = [np.ascontiguousarray(s) for s in srcs]
+    if not srcs:
+        return []
+    s0 = srcs[0]
+    if s0.dtype not in (np.uint8, np.uint16) or s0.ndim != 2:
+        raise ValueError("frames must be 2-D uint8 or uint16 arrays")
+    if any(s.shape != s0.shape or s.dtype != s0.dtype for s in srcs):
+        raise ValueError("all frames must share one shape and dtype")
+    n = len(srcs)
+    radii = [int(radii)] * n if np.isscalar(radii) else [int(r) for r in radii]
+    if len(radii) != n:
+        raise ValueError("one radius per frame")
+    for r in radii:
+        if r < 1:
+            raise ValueError(f"window must be an odd integer >= 3, got {2 * r + 1}")
+    if outs is None:
+        outs = [np.empty_like(s0) for _ in range(n)]
+    elif len(outs) != n or any(o.shape != s0.shape or o.dtype != s0.dtype or not o.flags.c_contiguous
+                                for o in outs):
+        raise ValueError("outs must be C-contiguous frames of the inputs' shape and dtype")
+    H, W = s0.shape
+    bits = 8 if s0.dtype == np.uint8 else 16
+    P = ctypes.c_void_p * n
+    src_arr = P(*[s.ctypes.data for s in srcs])
+    dst_arr = P(*[o.ctypes.data for o in outs])
+    rad_arr = (ctypes.c_int32 * n)(*radii)
+    rank_arr = None
+    if ranks is not None:
+        if len(ranks) != n:
+            raise ValueError("one rank per frame")
+        rank_arr = (ctypes.c_int64 * n)(*[int(k) for k in ranks])
+    lut_ptr = None
+    if lut is not None:
+        lut = np.ascontiguousarray(lut, dtype=s0.dtype)
+        lut_ptr = lut.ctypes.data
+    rc = _lib.load().mtb_filter_host_frames(
+        ctypes.cast(src_arr, ctypes.c_void_p), ctypes.cast(dst_arr, ctypes.c_void_p),
+        ctypes.cast(rad_arr, ctypes.c_void_p),
+        ctypes.cast(rank_arr, ctypes.c_void_p) if rank_arr is not None else None,
+        n, bits, H, W, lut_ptr, 0)
+    _lib.check(rc)
+    return outs

@@ -56,6 +56,22 @@ def test_abi_rejects_invalid_arguments_without_device():
     assert rc == _lib.MTB_E_INVAL
     rc = lib.mtb_filter_host(dummy, dummy, 12, 8, 8, 1, 5, None, 0)
     assert rc == _lib.MTB_E_INVAL and b"bit_depth" in lib.mtb_last_error()
+    rc = lib.mtb_filter_host_frames(dummy, dummy, dummy, None, 2, 12, 8, 8, None, 0)
+    assert rc == _lib.MTB_E_INVAL and b"bit_depth" in lib.mtb_last_error()
+    rc = lib.mtb_filter_host_frames(None, dummy, dummy, None, 2, 8, 8, 8, None, 0)
+    assert rc == _lib.MTB_E_INVAL and b"null" in lib.mtb_last_error()
+    assert lib.mtb_filter_host_frames(None, None, None, None, 0, 8, 8, 8, None, 0) == _lib.MTB_OK
+
+
+def test_host_frames_validates_before_any_device_call():
+    px = np.zeros((8, 8), np.uint8)
+    with pytest.raises(ValueError, match="shape and dtype"):
+        mtb.filter_host_frames([px, np.zeros((8, 9), np.uint8)], 1)
+    with pytest.raises(ValueError, match="one radius per frame"):
+        mtb.filter_host_frames([px, px], [1, 2, 3])
+    with pytest.raises(ValueError, match="odd integer"):
+        mtb.filter_host_frames([px], 0)
+    assert mtb.filter_host_frames([], 3) == []
 
 
 # ----------------------------------------------------------- validation

@@ -202,6 +202,28 @@ def test_host_buffer_entry_point(rng):
                           O.iot_filter(px16, 7, max_error=16))
 
 
+def test_host_frames_sequence(rng):
+    """mtb_filter_host_frames: a sequence longer than the buffer ring (3),
+    mixed radii and ranks, 8- and 16-bit, pinned and pageable frames, a value
+    map -- every frame equal to its own oracle result."""
+    frames = [workloads.cfg2_blur_sp_u8(70, 150 + 0 * i) for i in range(7)]
+    frames = [np.ascontiguousarray(np.roll(f, 5 * i, axis=1)) for i, f in enumerate(frames)]
+    radii = [1, 3, 7, 2, 15, 31, 5]
+    pinned = [torch.from_numpy(f).pin_memory().numpy() for f in frames]
+    outs = mtb.filter_host_frames(pinned, radii)
+    for f, r, o in zip(frames, radii, outs):
+        assert np.array_equal(o, O.iot_filter(f, 2 * r + 1)), r
+    ranks = [1, 49, 10, 25, 100, 1000, 121]
+    outs = mtb.filter_host_frames(frames, radii, ranks=ranks)
+    for f, r, k, o in zip(frames, radii, ranks, outs):
+        assert np.array_equal(o, O.iot_filter(f, 2 * r + 1, k)), (r, k)
+    f16 = [rng.integers(0, 65536, (40, 52)).astype(np.uint16) for _ in range(4)]
+    lut = mtb.value_map(mtb.uniform_topology(16), 16)
+    outs = mtb.filter_host_frames(f16, 3, lut=lut)
+    for f, o in zip(f16, outs):
+        assert np.array_equal(o, O.iot_filter(f, 7, max_error=16))
+
+
 @pytest.mark.parametrize("bits,r,bands,stream", [(8, 2, None, None), (8, 9, "3", None), (8, 40, None, None),
                                                  (16, 5, None, None), (16, 20, "5", None), (8, 3, "16", None),
                                                  (8, 2, None, "1"), (8, 40, None, "0"), (8, 70, None, "1"),
