@@ -92,7 +92,7 @@ __device__ __forceinline__ void med3_band(const SlabParams &p, const uint8_t *sr
             const uint32_t a = __vmaxu2(__vmaxu2(mn[2 * k], mn[2 * k + 1]), mn[2 * k + 2]);
             const uint32_t c = __vminu2(__vminu2(mx[2 * k], mx[2 * k + 1]), mx[2 * k + 2]);
             const uint32_t b = med3u2(md[2 * k], md[2 * k + 1], md[2 * k + 2]);
-            o[k] = med3u2(a, b, c);
+            o[k] = med3u2(a, b, c);  // (med3 via min/max: 4 ops, as the sum form)
         }
         uint32_t w0 = __byte_perm(o[0], o[1], 0x6420), w1 = __byte_perm(o[2], o[3], 0x6420);
         uint8_t *d = dst + (int64_t)(y - p.row_begin) * p.dst_pitch + x0;
@@ -134,22 +134,21 @@ __device__ __forceinline__ void med3_band(const SlabParams &p, const uint8_t *sr
         f1 = load(y + 5);
         f2 = load(y + 6);
         uint32_t mn[9], md[9], mx[9];
-        uint32_t clo[9], chi[9];
+        // 3-sort of every packed column: min3, max3 (VIMNMX3) and the sum
+        // minus both (lanes <= 765: no carry / borrow across lanes)
 #pragma unroll
         for (int m = 0; m < 9; ++m) {
-            clo[m] = __vminu2(qb[m], qc[m]);  // core: rows y, y+1
-            chi[m] = __vmaxu2(qb[m], qc[m]);
-            mn[m] = __vminu2(clo[m], qa[m]);  // row y: + row y-1
-            mx[m] = __vmaxu2(chi[m], qa[m]);
-            md[m] = __vmaxu2(clo[m], __vminu2(chi[m], qa[m]));
+            mn[m] = __vminu2(__vminu2(qa[m], qb[m]), qc[m]);  // row y: rows y-1, y, y+1
+            mx[m] = __vmaxu2(__vmaxu2(qa[m], qb[m]), qc[m]);
+            md[m] = qa[m] + qb[m] + qc[m] - mn[m] - mx[m];
         }
         store(y, mn, md, mx);
         if (y + 1 < Y1) {
 #pragma unroll
             for (int m = 0; m < 9; ++m) {
-                mn[m] = __vminu2(clo[m], qd[m]);  // row y+1: + row y+2
-                mx[m] = __vmaxu2(chi[m], qd[m]);
-                md[m] = __vmaxu2(clo[m], __vminu2(chi[m], qd[m]));
+                mn[m] = __vminu2(__vminu2(qb[m], qc[m]), qd[m]);  // row y+1: rows y, y+1, y+2
+                mx[m] = __vmaxu2(__vmaxu2(qb[m], qc[m]), qd[m]);
+                md[m] = qb[m] + qc[m] + qd[m] - mn[m] - mx[m];
             }
             store(y + 1, mn, md, mx);
         }
@@ -182,6 +181,147 @@ __global__ void __launch_bounds__(128) k_med3_u8(SlabParams p) {
             med3_band<false>(p, src, dst, x0, Y0, Y1);
     }
     stream_signal(p, Y0, Y1, blockIdx.x * 1024, blockIdx.x * 1024 + 1024);
+}
+
+// ---------------------------------------------------------------------------
+// k_med3t_u8: the same selection with the band's rows staged by TMA bulk
+// copies.  The register kernel above keeps only ~4 rows per warp in flight,
+// so on a one-wave grid it is latency-bound (Little's law).  Here thread 0
+// of each CTA issues, at launch, one cp.async.bulk per source row of the
+// CTA's whole band (RT + 2 rows x 1056 B, each completing on its own
+// mbarrier): the entire frame is requested in the first microsecond, and
+// threads walk down their 8 columns as rows land.
+//
+// CTA = 128 threads x 8 columns = 1024 output columns; staged row segment
+// = columns [X-16, X+1040) (16-byte aligned, clipped to the image).
+// Per output row and thread: one LDS.64 (own 8 columns) + two byte loads
+// (left / right neighbours, clamped to the image); 9 packed columns, each
+// 3-sorted from (min3, max3, sum - min3 - max3) with 3-input VIMNMX3.U16x2;
+// four pair medians med3(max3(mins), med3(meds), min3(maxes)).
+// Requires W % 16 == 0 and 16-byte aligned rows (host-checked).
+constexpr int M3T_SEG = 1056;
+
+__device__ __forceinline__ uint32_t m3t_smem(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t min3u2(uint32_t a, uint32_t b, uint32_t c) { return __vminu2(__vminu2(a, b), c); }
+__device__ __forceinline__ uint32_t max3u2(uint32_t a, uint32_t b, uint32_t c) { return __vmaxu2(__vmaxu2(a, b), c); }
+
+// median of three packed u16 pairs: a + b + c - min3 - max3 (lanes <= 765,
+// no carry or borrow crosses a lane)
+__device__ __forceinline__ uint32_t med3s(uint32_t a, uint32_t b, uint32_t c) {
+    return a + b + c - min3u2(a, b, c) - max3u2(a, b, c);
+}
+
+__global__ void __launch_bounds__(128) k_med3t_u8(SlabParams p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int tid = threadIdx.x;
+    const int W = p.W, H = p.H;
+    const int X = blockIdx.x * 1024;
+    const int Y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
+    const int Y1 = min(Y0 + p.rows_per_cta, p.row_end);
+    const int NR = Y1 - Y0 + 2;  // staged rows Y0-1 .. Y1
+    const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
+    uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
+    const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);  // [NR]
+    uint8_t *rows = smem_raw + ((NR * 8 + 127) & ~127);      // [NR][M3T_SEG]
+    stream_wait_rows(p, Y1 + 1);
+    // staged column span [gx0, gx1): multiples of 16 (W % 16 == 0)
+    const int gx0 = max(X - 16, 0), gx1 = min(X + 1040, W);
+    const int off = gx0 - (X - 16);  // 16 at the left image edge, else 0
+    const uint32_t bytes = (uint32_t)(gx1 - gx0);
+    if (tid == 0) {
+        for (int i = 0; i < NR; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(m3t_smem(bar + i)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < NR; ++i) {
+            const int gy = clampi(Y0 - 1 + i, 0, H - 1);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m3t_smem(bar + i)),
+                         "r"(bytes) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    m3t_smem(rows + i * M3T_SEG + off)),
+                "l"(src_row(p, src, gy) + gx0), "r"(bytes), "r"(m3t_smem(bar + i))
+                : "memory");
+        }
+    }
+    __syncthreads();  // barriers initialised before anyone waits
+    const int x0 = X + 8 * tid;
+    const bool act = x0 < W;  // W % 16 == 0: an active thread's 8 columns are all inside
+    // smem offsets of this thread's 8 columns and its clamped neighbours
+    const int ow = 16 + 8 * tid;
+    const int ol = act ? 16 + clampi(x0 - 1, 0, W - 1) - X : 16;
+    const int orr = act ? 16 + min(x0 + 8, W - 1) - X : 16;
+    auto wait_row = [&](int i) {
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n .reg .pred P;\n"
+                " mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
+                " selp.b32 %0, 1, 0, P;\n}\n"
+                : "=r"(done)
+                : "r"(m3t_smem(bar + i)), "r"(0u)
+                : "memory");
+        }
+    };
+    // packed columns Q_m = (col x0-1+m, col x0+m), m = 0..8, of staged row i
+    auto pack = [&](int i, uint32_t (&q)[9]) {
+        wait_row(i);
+        const uint8_t *rb = rows + i * M3T_SEG;
+        const uint2 v = *reinterpret_cast<const uint2 *>(rb + ow);
+        const uint32_t L = rb[ol], R = rb[orr];
+        const uint32_t mid = __byte_perm(v.x, v.y, 0x5432);  // cols x0+2 .. x0+5
+        q[0] = __byte_perm(v.x, L, 0x5054);
+        q[1] = __byte_perm(v.x, 0, 0x4140);
+        q[2] = __byte_perm(v.x, 0, 0x4241);
+        q[3] = __byte_perm(v.x, 0, 0x4342);
+        q[4] = __byte_perm(mid, 0, 0x4241);
+        q[5] = __byte_perm(v.y, 0, 0x4140);
+        q[6] = __byte_perm(v.y, 0, 0x4241);
+        q[7] = __byte_perm(v.y, 0, 0x4342);
+        q[8] = __byte_perm(v.y, R, 0x5453);
+    };
+    uint32_t qa[9], qb[9], qc[9];
+    pack(0, qa);
+    pack(1, qb);
+    uint8_t *d = dst + (int64_t)(Y0 - p.row_begin) * p.dst_pitch + x0;
+#pragma unroll 1
+    for (int i = 2; i < NR; ++i) {
+        pack(i, qc);
+        uint32_t mn[9], md[9], mx[9];
+#pragma unroll
+        for (int m = 0; m < 9; ++m) {
+            mn[m] = min3u2(qa[m], qb[m], qc[m]);
+            mx[m] = max3u2(qa[m], qb[m], qc[m]);
+            md[m] = qa[m] + qb[m] + qc[m] - mn[m] - mx[m];
+        }
+        uint32_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            o[k] = med3s(max3u2(mn[2 * k], mn[2 * k + 1], mn[2 * k + 2]), med3s(md[2 * k], md[2 * k + 1], md[2 * k + 2]),
+                         min3u2(mx[2 * k], mx[2 * k + 1], mx[2 * k + 2]));
+        uint32_t w0 = __byte_perm(o[0], o[1], 0x6420), w1 = __byte_perm(o[2], o[3], 0x6420);
+        if (lut) {
+            uint32_t b[8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                b[j] = __ldg(lut + ((w0 >> (8 * j)) & 0xffu));
+                b[4 + j] = __ldg(lut + ((w1 >> (8 * j)) & 0xffu));
+            }
+            w0 = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+            w1 = b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24);
+        }
+        if (act) *reinterpret_cast<uint2 *>(d) = make_uint2(w0, w1);
+        d += p.dst_pitch;
+#pragma unroll
+        for (int m = 0; m < 9; ++m) {
+            qa[m] = qb[m];
+            qb[m] = qc[m];
+        }
+    }
+    stream_signal(p, Y0, Y1, X, X + 1024);
 }
 
 }  // namespace mtb

@@ -162,7 +162,34 @@ static bool sortnet_applies(const SlabParams &p) {
 
 // 3x3 median of 8-bit frames (k_med3_u8): row bands sized so the grid is
 // one wave of resident CTAs
+// TMA-staged variant: 16-byte aligned rows, W % 16 == 0; bands sized for
+// one wave (the whole frame is requested at launch)
+static int run_med3t(SlabParams p, int B, cudaStream_t s) {
+    const int rows = p.row_end - p.row_begin;
+    const int bx = (p.W + 1023) / 1024;
+    const int per_sm = env_int("MTB_MED3T_CTAS", 8);
+    const int64_t slots = (int64_t)sm_count() * per_sm;
+    int64_t bands = slots / ((int64_t)bx * B);
+    if (bands < 1) bands = 1;
+    int rt = (int)((rows + bands - 1) / bands);
+    rt = std::max(rt, env_int("MTB_MED3_MIN_RT", 8));
+    rt = std::min(rt, std::min(rows, 190));  // (rt + 2) rows of 1056 B + barriers <= 200 KB
+    p.rows_per_cta = rt;
+    const size_t smem = (size_t)(((rt + 2) * 8 + 127) & ~127) + (size_t)(rt + 2) * M3T_SEG;
+    dim3 grid(bx, (rows + rt - 1) / rt, B);
+    return launch(k_med3t_u8, grid, 128, smem, s, p, "k_med3t_u8");
+}
+
+static bool med3t_applies(const SlabParams &p, int B) {
+    const auto a16 = [](uintptr_t v) { return (v & 15) == 0; };
+    return p.W % 16 == 0 && a16((uintptr_t)p.src) && a16((uintptr_t)p.dst) && a16((uintptr_t)p.src_pitch) &&
+           a16((uintptr_t)p.dst_pitch) &&
+           (B == 1 || (a16((uintptr_t)p.src_img_stride) && a16((uintptr_t)p.dst_img_stride))) &&
+           env_int("MTB_MED3T", 1) != 0;
+}
+
 static int run_med3(SlabParams p, int B, cudaStream_t s) {
+    if (med3t_applies(p, B)) return run_med3t(p, B, s);
     const int rows = p.row_end - p.row_begin;
     const int bx = (p.W + 1023) / 1024;
     int per_sm = 4;

@@ -473,53 +473,66 @@ def test_colhist16s_u16_sorted_columns(kind, monkeypatch):
             assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (kind, r, rank)
 
 
-# ------------------------------------------ k_med3_u8 (3x3, register-resident)
+# ------------------------------------------ 3x3 kernels (k_med3_u8 / k_med3t_u8)
 
 def _pitched(px, pad):
     """CUDA view of px whose rows sit in a buffer `pad` columns wider than
-    the next multiple of 8 (64-bit aligned pitch, as k_med3_u8 needs)."""
+    the next multiple of 16 (aligned pitch, as the vector / TMA paths need)."""
     H, W = px.shape
-    buf = torch.zeros((H, ((W + 7) & ~7) + pad), dtype=torch.uint8, device="cuda")
+    buf = torch.zeros((H, ((W + 15) & ~15) + pad), dtype=torch.from_numpy(px).dtype, device="cuda")
     buf[:, :W] = torch.from_numpy(px).cuda()
     return buf[:, :W]
 
 
-@pytest.mark.parametrize("rt", ["1", "2", "8", "32"])
-def test_med3_u8_shapes_slabs_batch_lut(rt, monkeypatch):
-    """3x3 median: every width tail (partial last lane, widths below one
-    lane, lanes beyond W), odd and even band heights, slab calls, batch,
-    value map, unaligned pitches (byte path).  All vs the oracle."""
+@pytest.mark.parametrize("tma,rt", [("1", "1"), ("1", "2"), ("1", "8"), ("1", "40"),
+                                    ("0", "1"), ("0", "2"), ("0", "8"), ("0", "32")])
+def test_med3_u8_shapes_slabs_batch_lut(tma, rt, monkeypatch):
+    """3x3 median, both kernels (TMA-staged for W % 16 == 0 with aligned
+    rows, register-resident otherwise): every width tail (partial last lane
+    and CTA, widths below one lane), odd and even band heights, slab calls,
+    batch, value map, unaligned pitches.  All vs the oracle."""
     from paper_1105_3829_b200 import _lib
 
+    monkeypatch.setenv("MTB_MED3T", tma)
     monkeypatch.setenv("MTB_MED3_MIN_RT", rt)
     rng = np.random.default_rng(31)
-    for H, W in [(1, 1), (1, 9), (2, 3), (3, 8), (5, 7), (17, 255), (19, 256), (33, 257),
-                 (40, 1023), (35, 1025), (21, 2100), (64, 64)]:
+
+    def expect(W, aligned=True):
+        return "k_med3t_u8" if (tma == "1" and W % 16 == 0 and aligned) else "k_med3_u8"
+
+    for H, W in [(1, 1), (1, 9), (2, 3), (3, 8), (5, 7), (1, 16), (2, 32), (17, 255), (19, 256),
+                 (33, 257), (40, 1023), (35, 1025), (21, 1040), (300, 1040), (21, 2100), (64, 64),
+                 (9, 4096)]:
         px = rng.integers(0, 256, (H, W), dtype=np.uint8)
         ref = O.iot_filter(px, 3)
-        o = _pitched(np.zeros_like(px), 0)
-        out = mtb.rank_filter(_pitched(px, 8), 1, out=o).cpu().numpy()
-        assert _lib.last_kernel().startswith("k_med3_u8"), _lib.last_kernel()
-        assert np.array_equal(out, ref), (H, W)
-    # slabs of a 61 x 300 frame, each with its 1-row halo
-    px = workloads.cfg2_blur_sp_u8(61, 300)
-    ref = O.iot_filter(px, 3)
-    dev = _pitched(px, 0)
-    for a, b in [(0, 7), (7, 30), (30, 61), (60, 61)]:
-        s0, s1 = max(a - 1, 0), min(b + 1, 61)
-        out = mtb.rank_filter(dev[s0:s1], 1, rows=(a, b), src_row0=s0, height=61)
-        assert _lib.last_kernel().startswith("k_med3_u8")
-        assert np.array_equal(out.cpu().numpy(), ref[a:b]), (a, b)
+        for pad in (0, 8):
+            o = _pitched(np.zeros_like(px), pad)
+            out = mtb.rank_filter(_pitched(px, pad), 1, out=o).cpu().numpy()
+            assert _lib.last_kernel() == expect(W, pad == 0), (H, W, pad, _lib.last_kernel())
+            assert np.array_equal(out, ref), (H, W, pad)
+    # slabs of a frame, each with its 1-row halo
+    for W in (300, 320):
+        px = workloads.cfg2_blur_sp_u8(61, W)
+        ref = O.iot_filter(px, 3)
+        dev = _pitched(px, 0)
+        for a, b in [(0, 7), (7, 30), (30, 61), (60, 61)]:
+            s0, s1 = max(a - 1, 0), min(b + 1, 61)
+            o = _pitched(np.zeros((b - a, W), np.uint8), 0)
+            out = mtb.rank_filter(dev[s0:s1], 1, out=o, rows=(a, b), src_row0=s0, height=61)
+            assert _lib.last_kernel() == expect(W)
+            assert np.array_equal(out.cpu().numpy(), ref[a:b]), (W, a, b)
     # batch
-    b5 = workloads.cfg5_batch_u8(3, 70, 136)
-    out = mtb.rank_filter(torch.from_numpy(b5).cuda(), 1).cpu().numpy()
-    assert _lib.last_kernel().startswith("k_med3_u8")
-    for i in range(3):
-        assert np.array_equal(out[i], O.iot_filter(b5[i], 3)), i
+    for W in (136, 144):
+        b5 = workloads.cfg5_batch_u8(3, 70, W)
+        out = mtb.rank_filter(torch.from_numpy(b5).cuda(), 1).cpu().numpy()
+        assert _lib.last_kernel() == expect(W)
+        for i in range(3):
+            assert np.array_equal(out[i], O.iot_filter(b5[i], 3)), (W, i)
     # reduced precision through the value map
-    px = rng.integers(0, 256, (45, 333), dtype=np.uint8)
-    o, _ = mtb.filter_image(px, 3, max_error=16)
-    assert np.array_equal(o.pixels, O.iot_filter(px, 3, max_error=16))
+    for W in (333, 336):
+        px = rng.integers(0, 256, (45, W), dtype=np.uint8)
+        o, _ = mtb.filter_image(px, 3, max_error=16)
+        assert np.array_equal(o.pixels, O.iot_filter(px, 3, max_error=16)), W
     # unaligned pitches (byte loads / stores), and the forced selection network
     for W in (101, 1029, 2050):
         px = rng.integers(0, 256, (30, W), dtype=np.uint8)
