@@ -8,7 +8,7 @@ python bench.py > $out/bench_full.json 2> $out/bench_full.err || exit 1
 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-extra > /dev/null 2>&1 &&
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-extra > $out/ncu_l.log 2>&1
-for spec in "r3 2 3" "r7 2 7" "r15 2 15" "r31 2 31" "r63 2 63" "cfg4_r15 4 15" "cfg3_r15 3 15" "cfg3_r31 3 31"; do
+for spec in "r1 2 1" "r3 2 3" "r7 2 7" "r15 2 15" "r31 2 31" "r63 2 63" "cfg4_r15 4 15" "cfg3_r15 3 15" "cfg3_r31 3 31"; do
   set -- $spec
   tools/prof_one.sh f_$1 $2 $3 "" > /dev/null
   python tools/ncu_summary.py $out/prof_f_$1.ncu-rep > $out/sum_f_$1.txt 2>&1
