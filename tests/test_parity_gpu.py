@@ -227,7 +227,8 @@ def test_host_frames_sequence(rng):
 @pytest.mark.parametrize("bits,r,bands,stream", [(8, 2, None, None), (8, 9, "3", None), (8, 40, None, None),
                                                  (16, 5, None, None), (16, 20, "5", None), (8, 3, "16", None),
                                                  (8, 2, None, "1"), (8, 40, None, "0"), (8, 70, None, "1"),
-                                                 (16, 3, None, "1"), (16, 6, None, "1"), (8, 1, None, "1")])
+                                                 (16, 3, None, "1"), (16, 6, None, "1"), (8, 1, None, "1"),
+                                                 (8, 1, "3", "0")])
 def test_host_pipeline_bands(bits, r, bands, stream, monkeypatch):
     """mtb_filter_host overlaps copies with filtering -- row bands, or one
     streaming launch whose CTAs wait for their rows (stream memory ops);
@@ -238,7 +239,9 @@ def test_host_pipeline_bands(bits, r, bands, stream, monkeypatch):
     if stream:
         monkeypatch.setenv("MTB_HOST_STREAM", stream)
     rng = np.random.default_rng(bits * 100 + r)
-    H, W = 1300, 333
+    # r = 1: W % 16 == 0 takes the TMA-staged 3x3 kernel (streaming case),
+    # W = 333 the register one (banded case)
+    H, W = 1300, (336 if (r == 1 and bands is None) else 333)
     if bits == 8:
         px = workloads.cfg2_blur_sp_u8(H, W, seed=r)
     else:
