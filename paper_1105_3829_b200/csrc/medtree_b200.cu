@@ -430,9 +430,10 @@ static int host_ctx(HostCtx *&ctx, size_t bytes) {
 // line boundaries, so no L1 line ever mixes arrived and pending rows.
 typedef int (*write32_fn)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
 
-static int host_stream(HostCtx *ctx, const void *src, void *dst, int bit_depth, int H, int W, int radius,
-                       int64_t rank, const void *lut, uint32_t flags) {
-    static write32_fn write32 = nullptr, wait32 = nullptr;
+// driver stream memory operations (resolved at run time: no link-time
+// libcuda dependency); false when the driver does not provide them
+static bool stream_mem_ops(write32_fn &write32, write32_fn &wait32) {
+    static write32_fn w = nullptr, t = nullptr;
     static int resolved = 0;
     if (!resolved) {
         void *fw = nullptr, *fwt = nullptr;
@@ -440,15 +441,23 @@ static int host_stream(HostCtx *ctx, const void *src, void *dst, int bit_depth, 
         if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fw, cudaEnableDefault, &q1) == cudaSuccess &&
             cudaGetDriverEntryPoint("cuStreamWaitValue32", &fwt, cudaEnableDefault, &q2) == cudaSuccess &&
             q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && fw && fwt) {
-            write32 = reinterpret_cast<write32_fn>(fw);
-            wait32 = reinterpret_cast<write32_fn>(fwt);
+            w = reinterpret_cast<write32_fn>(fw);
+            t = reinterpret_cast<write32_fn>(fwt);
             resolved = 1;
         } else {
             cudaGetLastError();
             resolved = -1;
         }
     }
-    if (resolved < 0) return 1;  // caller falls back to the banded path
+    write32 = w;
+    wait32 = t;
+    return resolved > 0;
+}
+
+static int host_stream(HostCtx *ctx, const void *src, void *dst, int bit_depth, int H, int W, int radius,
+                       int64_t rank, const void *lut, uint32_t flags) {
+    write32_fn write32 = nullptr, wait32 = nullptr;
+    if (!stream_mem_ops(write32, wait32)) return 1;  // caller falls back to the banded path
     const size_t es = bit_depth == 8 ? 1 : 2;
     const size_t row = (size_t)W * es, total = (size_t)H * row;
     const int K = std::max(1, std::min(env_int("MTB_HOST_IN_CHUNKS", 4), H / 128));    // input chunks
@@ -602,8 +611,10 @@ static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W
 // filtered: the copy engines and the SMs stay busy across the sequence.
 struct FramesCtx {
     static constexpr int NB = 3;
+    static constexpr int NFLAGS = 64;  // per slot: [0] rows arrived, [1..] output pixels per chunk
     int dev = -1;
     void *dsrc[NB] = {}, *ddst[NB] = {}, *dlut = nullptr;
+    unsigned int *dflags = nullptr;  // [NB][NFLAGS]
     size_t cap = 0;
     cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
     cudaEvent_t ein[NB], ek[NB], eout[NB];
@@ -623,6 +634,7 @@ static int frames_ctx(FramesCtx *&ctx, size_t bytes) {
         if (!rc) rc = ok(cudaStreamCreateWithFlags(&ctx->sc, cudaStreamNonBlocking), "cudaStreamCreate");
         if (!rc) rc = ok(cudaStreamCreateWithFlags(&ctx->sd, cudaStreamNonBlocking), "cudaStreamCreate");
         if (!rc) rc = ok(cudaMalloc(&ctx->dlut, 65536 * 2), "cudaMalloc");
+        if (!rc) rc = ok(cudaMalloc(&ctx->dflags, FramesCtx::NB * FramesCtx::NFLAGS * sizeof(unsigned int)), "cudaMalloc");
         for (int j = 0; j < FramesCtx::NB && !rc; ++j) {
             rc = ok(cudaEventCreateWithFlags(&ctx->ein[j], cudaEventDisableTiming), "cudaEventCreate");
             if (!rc) rc = ok(cudaEventCreateWithFlags(&ctx->ek[j], cudaEventDisableTiming), "cudaEventCreate");
@@ -664,16 +676,51 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
                 "H2D lut");
     }
     constexpr int NB = FramesCtx::NB;
+    // MTB_FRAMES_STREAM=1: streaming frames -- each frame's rows arrive in
+    // chunks (CTAs wait on a row counter) and its results leave in chunks
+    // (the copy-out stream waits on per-chunk pixel counters), so a frame
+    // also overlaps its OWN copies.  Off by default: on the config-2 sweep
+    // it measured 24.1 against 24.8 Gpix/s for whole-frame copies (the
+    // stream-op latencies cost more than the exposed first copy-in and last
+    // copy-out).
+    write32_fn write32 = nullptr, wait32 = nullptr;
+    const bool streaming = env_int("MTB_FRAMES_STREAM", 0) != 0 && std::string(forced_kernel()) != "lob" &&
+                           stream_mem_ops(write32, wait32) && H >= 256;  // (lob has no streaming hooks)
+    const size_t row = (size_t)W * es;
+    const int KI = std::max(1, std::min(env_int("MTB_FRAMES_IN_CHUNKS", 4), H / 128));
+    const int KO = std::max(1, std::min(env_int("MTB_FRAMES_OUT_CHUNKS", 4), std::min(FramesCtx::NFLAGS - 1, H / 128)));
+    const int C = (H + KO - 1) / KO, nout = (H + C - 1) / C;
     for (int i = 0; i < n && rc == MTB_OK; ++i) {
         const int j = i % NB;
         if (!srcs[i] || !dsts[i]) {
             rc = fail(MTB_E_INVAL, "null src/dst pointer (frame " + std::to_string(i) + ")");
             break;
         }
+        unsigned int *fl = ctx->dflags + j * FramesCtx::NFLAGS;
         if (i >= NB) cudaStreamWaitEvent(ctx->sh, ctx->ek[j], 0);  // job i-NB done reading dsrc[j]
-        rc = ok(cudaMemcpyAsync(ctx->dsrc[j], srcs[i], bytes, cudaMemcpyHostToDevice, ctx->sh), "H2D");
+        if (streaming) {
+            // counters reset before this frame's kernel or copy-out can look at them
+            rc = ok(cudaMemsetAsync(fl, 0, (1 + nout) * sizeof(unsigned int), ctx->sh), "memset");
+            if (rc) break;
+            cudaEventRecord(ctx->ein[j], ctx->sh);
+            const char *s8 = static_cast<const char *>(srcs[i]);
+            size_t b = 0;
+            for (int q = 0; q < KI && !rc; ++q) {
+                const int R = (int)((int64_t)H * (q + 1) / KI);
+                const size_t e = q == KI - 1 ? bytes : std::min(bytes, ((size_t)R * row + 127) & ~(size_t)127);
+                if (e > b) {
+                    rc = ok(cudaMemcpyAsync(static_cast<char *>(ctx->dsrc[j]) + b, s8 + b, e - b,
+                                            cudaMemcpyHostToDevice, ctx->sh), "H2D");
+                    b = e;
+                }
+                if (!rc && write32(ctx->sh, (unsigned long long)fl, (unsigned int)R, 0) != 0)
+                    rc = fail(MTB_E_CUDA, "cuStreamWriteValue32 failed");
+            }
+        } else {
+            rc = ok(cudaMemcpyAsync(ctx->dsrc[j], srcs[i], bytes, cudaMemcpyHostToDevice, ctx->sh), "H2D");
+            if (!rc) cudaEventRecord(ctx->ein[j], ctx->sh);
+        }
         if (rc) break;
-        cudaEventRecord(ctx->ein[j], ctx->sh);
         cudaStreamWaitEvent(ctx->sc, ctx->ein[j], 0);
         if (i >= NB) cudaStreamWaitEvent(ctx->sc, ctx->eout[j], 0);  // job i-NB's result copied out
         if (bit_depth == 16)
@@ -684,13 +731,35 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
             const int64_t nn = 2 * (int64_t)radii[i] + 1;
             p.rank = (uint32_t)((nn * nn + 1) / 2);
         }
+        if (streaming) {
+            p.in_rows = fl;
+            p.out_px = fl + 1;
+            p.out_chunk = C;
+        }
         (void)flags;
         rc = bit_depth == 8 ? run<uint8_t>(p, 1, ctx->sc) : run<uint16_t>(p, 1, ctx->sc);
         g_spread_hint = -1;
-        if (rc) break;
+        if (rc) {
+            // release CTAs of this or earlier frames that might wait on rows
+            if (streaming) write32(ctx->sh, (unsigned long long)fl, (unsigned int)H, 0);
+            break;
+        }
         cudaEventRecord(ctx->ek[j], ctx->sc);
-        cudaStreamWaitEvent(ctx->sd, ctx->ek[j], 0);
-        rc = ok(cudaMemcpyAsync(dsts[i], ctx->ddst[j], bytes, cudaMemcpyDeviceToHost, ctx->sd), "D2H");
+        char *d8 = static_cast<char *>(dsts[i]);
+        if (streaming) {
+            cudaStreamWaitEvent(ctx->sd, ctx->ein[j], 0);  // counters reset for this frame
+            for (int c = 0; c < nout && !rc; ++c) {
+                const int a = c * C, e = std::min(H, a + C);
+                if (wait32(ctx->sd, (unsigned long long)(fl + 1 + c), (unsigned int)((e - a) * W), 0) != 0)
+                    rc = fail(MTB_E_CUDA, "cuStreamWaitValue32 failed");
+                else
+                    rc = ok(cudaMemcpyAsync(d8 + (size_t)a * row, static_cast<char *>(ctx->ddst[j]) + (size_t)a * row,
+                                            (size_t)(e - a) * row, cudaMemcpyDeviceToHost, ctx->sd), "D2H");
+            }
+        } else {
+            cudaStreamWaitEvent(ctx->sd, ctx->ek[j], 0);
+            rc = ok(cudaMemcpyAsync(d8, ctx->ddst[j], bytes, cudaMemcpyDeviceToHost, ctx->sd), "D2H");
+        }
         if (rc) break;
         cudaEventRecord(ctx->eout[j], ctx->sd);
     }

@@ -202,11 +202,13 @@ def test_host_buffer_entry_point(rng):
                           O.iot_filter(px16, 7, max_error=16))
 
 
-def test_host_frames_sequence(rng):
+@pytest.mark.parametrize("stream", ["1", "0"])
+def test_host_frames_sequence(rng, stream, monkeypatch):
     """mtb_filter_host_frames: a sequence longer than the buffer ring (3),
     mixed radii and ranks, 8- and 16-bit, pinned and pageable frames, a value
     map -- every frame equal to its own oracle result."""
-    frames = [workloads.cfg2_blur_sp_u8(70, 150 + 0 * i) for i in range(7)]
+    monkeypatch.setenv("MTB_FRAMES_STREAM", stream)
+    frames = [workloads.cfg2_blur_sp_u8(300, 150) for i in range(7)]
     frames = [np.ascontiguousarray(np.roll(f, 5 * i, axis=1)) for i, f in enumerate(frames)]
     radii = [1, 3, 7, 2, 15, 31, 5]
     pinned = [torch.from_numpy(f).pin_memory().numpy() for f in frames]
@@ -217,7 +219,7 @@ def test_host_frames_sequence(rng):
     outs = mtb.filter_host_frames(frames, radii, ranks=ranks)
     for f, r, k, o in zip(frames, radii, ranks, outs):
         assert np.array_equal(o, O.iot_filter(f, 2 * r + 1, k)), (r, k)
-    f16 = [rng.integers(0, 65536, (40, 52)).astype(np.uint16) for _ in range(4)]
+    f16 = [rng.integers(0, 65536, (260, 52)).astype(np.uint16) for _ in range(4)]
     lut = mtb.value_map(mtb.uniform_topology(16), 16)
     outs = mtb.filter_host_frames(f16, 3, lut=lut)
     for f, o in zip(f16, outs):
