@@ -14,6 +14,7 @@
 #include "kernels_vert.cuh"
 #include "kernels_sortnet.cuh"
 #include "kernels_med3.cuh"
+#include "kernels_mednet.cuh"
 #include "kernels_select.cuh"
 #include <cstdlib>
 
@@ -207,8 +208,36 @@ static int run_med3(SlabParams p, int B, cudaStream_t s) {
     return launch(k_med3_u8, grid, 128, 0, s, p, "k_med3_u8");
 }
 
+// n = 5, 7 medians from sorted packed columns with merge sharing (k_mednet)
+template <int N, typename P>
+static int run_mednet(SlabParams p, int B, cudaStream_t s, const char *name) {
+    const size_t smem = (size_t)mn_smem(N);
+    auto kern = k_mednet<N, P>;
+    if (int rc = set_smem(kern, smem)) return rc;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, MN_T, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int rows = p.row_end - p.row_begin;
+    const int bx = (p.W + MN_TX - 1) / MN_TX;
+    const int64_t slots = (int64_t)sm_count() * per_sm * env_int("MTB_MN_WAVES", 2);
+    int64_t bands = slots / ((int64_t)bx * B);
+    if (bands < 1) bands = 1;
+    int rt = (int)((rows + bands - 1) / bands);
+    rt = std::max(rt, env_int("MTB_MN_MIN_RT", 16));
+    rt = (rt + 1) & ~1;  // two output rows per step
+    if (rt > rows) rt = rows;
+    p.rows_per_cta = rt;
+    dim3 grid(bx, (rows + rt - 1) / rt, B);
+    return launch(kern, grid, MN_T, smem, s, p, name);
+}
+
 template <typename P>
 static int run_sortnet(SlabParams p, int B, cudaStream_t s) {
+    if ((p.radius == 2 || p.radius == 3) && env_int("MTB_MEDNET", 1) != 0 &&
+        strcmp(forced_kernel(), "sortnet") != 0) {
+        if (p.radius == 2) return run_mednet<5, P>(p, B, s, sizeof(P) == 1 ? "k_mednet<5,u8>" : "k_mednet<5,u16>");
+        return run_mednet<7, P>(p, B, s, sizeof(P) == 1 ? "k_mednet<7,u8>" : "k_mednet<7,u16>");
+    }
     if (sizeof(P) == 1 && p.radius == 1 && strcmp(forced_kernel(), "sortnet") != 0 &&
         (int64_t)p.src_rows * p.src_pitch < (1ll << 31))
         return run_med3(p, B, s);
@@ -267,12 +296,14 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     const bool wide = n * n > 65535;
     const std::string force = forced_kernel();
     // Kernel choice (measured on B200, tools/probe.py):
-    //   median, n <= 5 (8-bit), n <= 7 (16-bit)  -> selection networks
+    //   median, r = 1 (8-bit)                     -> 3x3 kernels (k_med3t / k_med3)
+    //   median, r = 2, 3                          -> sorted packed columns + shared merges (k_mednet)
+    //   median, r = 1 (16-bit)                    -> selection network (k_sortnet<3>)
     //   8-bit, r <= 31 (any rank)                 -> column-histogram gather
     //   8-bit, 32 <= r <= 127                     -> CTMF tiles (O(1) in r)
     //   otherwise                                 -> per-column vertical histograms
-    if ((force.empty() || force == "sortnet" || force == "med3") && sortnet_applies<P>(p) &&
-        (sizeof(P) == 2 || p.radius <= 2 || force == "sortnet"))
+    if ((force.empty() || force == "sortnet" || force == "med3" || force == "mednet") && sortnet_applies<P>(p) &&
+        (sizeof(P) == 2 || p.radius <= env_int("MTB_NET_MAX_R_U8", 3) || force == "sortnet" || force == "mednet"))
         return run_sortnet<P>(p, B, s);
     if (sizeof(P) == 1 && p.radius <= 63 && force == "lob") return run_lob_u8_32(p, B, s);
     if (sizeof(P) == 1 && n <= 255 &&

@@ -548,3 +548,48 @@ def test_med3_u8_shapes_slabs_batch_lut(tma, rt, monkeypatch):
     out = mtb.rank_filter(torch.from_numpy(px).cuda(), 1).cpu().numpy()
     assert _lib.last_kernel() == "k_sortnet<3>"
     assert np.array_equal(out, O.iot_filter(px, 3))
+
+
+# ------------------------------------------ n = 5, 7 medians (k_mednet)
+
+@pytest.mark.parametrize("bits", [8, 16])
+@pytest.mark.parametrize("rt", ["2", "16", "40"])
+def test_mednet_shapes_slabs_batch_lut(bits, rt, monkeypatch):
+    """k_mednet (sorted packed columns, shared merges): n = 5 and 7, 8- and
+    16-bit, widths around the 512-column CTA tile and the 4-column thread
+    tile, heights 1..RT+3 (odd band tails), slabs, batch, value map, ties
+    (few distinct values).  All vs the oracle."""
+    from paper_1105_3829_b200 import _lib
+
+    monkeypatch.setenv("MTB_KERNEL", "mednet")
+    monkeypatch.setenv("MTB_MN_MIN_RT", rt)
+    rng = np.random.default_rng(57 + bits)
+    hi = 256 if bits == 8 else 65536
+    dt = np.uint8 if bits == 8 else np.uint16
+    for n in (5, 7):
+        for H, W in [(1, 1), (2, 5), (3, 3), (7, 7), (5, 13), (9, 512), (17, 513), (33, 1030),
+                     (41, 300), (64, 64), (20, 2053)]:
+            if n > 2 * min(H, W) + 1:
+                continue
+            for vals in (hi, 3):
+                px = rng.integers(0, vals, (H, W)).astype(dt)
+                out = mtb.rank_filter(torch.from_numpy(px).cuda(), n // 2).cpu().numpy()
+                assert _lib.last_kernel().startswith("k_mednet"), _lib.last_kernel()
+                assert np.array_equal(out, O.iot_filter(px, n)), (n, H, W, vals)
+        # slabs of a 61-row frame with their halos
+        px = rng.integers(0, hi, (61, 700)).astype(dt)
+        ref = O.iot_filter(px, n)
+        r = n // 2
+        dev = torch.from_numpy(px).cuda()
+        for a, b in [(0, 9), (9, 30), (30, 61), (60, 61)]:
+            s0, s1 = max(a - r, 0), min(b + r, 61)
+            out = mtb.rank_filter(dev[s0:s1], r, rows=(a, b), src_row0=s0, height=61)
+            assert np.array_equal(out.cpu().numpy(), ref[a:b]), (n, a, b)
+        # batch
+        bt = rng.integers(0, hi, (3, 40, 520)).astype(dt)
+        out = mtb.rank_filter(torch.from_numpy(bt).cuda(), r).cpu().numpy()
+        for i in range(3):
+            assert np.array_equal(out[i], O.iot_filter(bt[i], n)), (n, i)
+        # value map (reduced precision)
+        o, _ = mtb.filter_image(px, n, max_error=16)
+        assert np.array_equal(o.pixels, O.iot_filter(px, n, max_error=16)), n
