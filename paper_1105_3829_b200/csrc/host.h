@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cstdint>
 #include <string>
+#include <type_traits>
 
 #include "../../include/medtree_b200.h"
 #include "common.cuh"
@@ -43,6 +44,21 @@ inline int launch(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, 
     return MTB_OK;
 }
 
+// Calls f(std::integral_constant<int, N>{}) for the odd N == n in
+// [NLO, NHI] (compile-time window side), f(integral_constant<int, 0>) else.
+template <int NLO, int NHI, typename F>
+inline int with_fixed_n(int n, F &&f) {
+    if constexpr (NLO > NHI) {
+        return f(std::integral_constant<int, 0>{});
+    } else {
+        if (n == NLO) return f(std::integral_constant<int, NLO>{});
+        return with_fixed_n<NLO + 2, NHI>(n, f);
+    }
+}
+
+// largest carry-free group of u8 records whose counts are <= c (G * c <= 255)
+constexpr int carry_free_group(int c) { return 8 * c <= 255 ? 8 : (4 * c <= 255 ? 4 : (2 * c <= 255 ? 2 : 1)); }
+
 // kernel families in their own translation units
 int run_colhist_u8(SlabParams p, int B, cudaStream_t s);
 int run_colhist4_256(SlabParams p, int B, cudaStream_t s);
@@ -50,6 +66,10 @@ int run_colhist4p_256(SlabParams p, int B, cudaStream_t s, int pl);
 // wk: window-keyed first sweep (pays off on compact data, see kernel)
 int run_colhist16_u16(SlabParams p, int B, cudaStream_t s, bool wk = true);
 int run_colhist16s_u16(SlabParams p, int B, cudaStream_t s);
+// compile-time window sides of k_colhist16_u16; 1 (NOT_COVERED) when n is outside the range
+int run_colhist16_fixed_a(SlabParams p, int B, cudaStream_t s, bool wk);
+int run_colhist16_fixed_b(SlabParams p, int B, cudaStream_t s, bool wk);
+int run_colhist16_fixed_c(SlabParams p, int B, cudaStream_t s, bool wk);
 int run_ctmf_u8(SlabParams p, int B, cudaStream_t s);
 int run_lob_u8_32(SlabParams p, int B, cudaStream_t s);
 

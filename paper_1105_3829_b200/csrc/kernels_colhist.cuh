@@ -118,11 +118,13 @@ __device__ __forceinline__ void ch_gather(const uint4 *rec, int chunk, int k0, i
     }
 }
 
-template <int T, int S, int G, int M>
+// NF > 0: the window side as a compile-time constant (fully unrolled
+// gathers; measured 16-23% faster than the runtime-n loops at r = 6..15)
+template <int T, int S, int G, int M, int NF = 0>
 __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
-    const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
+    const int r = NF ? NF / 2 : p.radius, H = p.H, W = p.W, n = NF ? NF : 2 * r + 1;
     const ColhistGeom g = colhist_geom(T, S, r);
     const int NCS = g.NCS, NPOS = g.NPOS;
     uint4 *rec = reinterpret_cast<uint4 *>(smem_raw);       // [17][NPOS] 16-B records
@@ -258,8 +260,8 @@ constexpr int CH4_RECS = 85;
 // record row stride: a multiple of 32 words, so a warp's per-column byte
 // updates (column c -> bank c mod 32, whatever the record row) never
 // conflict
-__host__ __device__ inline int ch4_stride(int ncol) { return (ncol + 31) & ~31; }
-__host__ __device__ inline int colhist4_bytes(int T, int r) { return CH4_RECS * ch4_stride(T + 2 * r) * 4; }
+__host__ __device__ constexpr int ch4_stride(int ncol) { return (ncol + 31) & ~31; }
+__host__ __device__ constexpr int colhist4_bytes(int T, int r) { return CH4_RECS * ch4_stride(T + 2 * r) * 4; }
 
 // 4 bins (packed u16 pairs w0 = {b0, b1}, w1 = {b2, b3}): smallest digit d
 // with cumsum(bins[0..d]) >= k; leaves the rank within bin d in k
@@ -312,8 +314,8 @@ __host__ __device__ constexpr int ch4p_recs(int PL) { return PL >= 3 ? 21 : (PL 
 
 // record rows padded to a multiple of 32 columns (conflict-free updates;
 // pair and quad alignment)
-__host__ __device__ inline int colhist4p_ncolp(int T, int r) { return (T + 2 * r + 31) & ~31; }
-__host__ __device__ inline int colhist4p_bytes(int T, int r, int PL) {
+__host__ __device__ constexpr int colhist4p_ncolp(int T, int r) { return (T + 2 * r + 31) & ~31; }
+__host__ __device__ constexpr int colhist4p_bytes(int T, int r, int PL) {
     const int ncp = colhist4p_ncolp(T, r);
     return (CH4_RECS * ncp + ch4p_recs(PL) * (ncp / 2)) * 4;
 }
@@ -512,11 +514,12 @@ __device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uin
 
 // STREAM: the streaming host path's instantiation (row waits / chunk
 // signals); the plain one has no hooks (they cost ~2% here when inlined).
-template <int T, int G, int M, bool STREAM>
+// NF > 0: the window side as a compile-time constant (fully unrolled gathers)
+template <int T, int G, int M, bool STREAM, int NF = 0>
 __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
-    const int r = p.radius, W = p.W, n = 2 * r + 1;
+    const int r = NF ? NF / 2 : p.radius, W = p.W, n = NF ? NF : 2 * r + 1;
     const int NCOL = T + 2 * r, RS = ch4_stride(NCOL);
     uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][RS]
     const int X0 = blockIdx.x * T;
@@ -556,11 +559,11 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
 // resolved right there (5 gathers instead of phase A + phase B's 8); the
 // rest (marked in the high-byte plane) go through phases A and B, which
 // then skip H0.
-template <int T, int G, int M, int PL>
+template <int T, int G, int M, int PL, int NF = 0>
 __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__restrict__ hplane, bool WK) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
-    const int r = p.radius, W = p.W, n = 2 * r + 1;
+    const int r = NF ? NF / 2 : p.radius, W = p.W, n = NF ? NF : 2 * r + 1;
     const int NCOL = T + 2 * r;
     const int NCP = PL > 0 ? colhist4p_ncolp(T, r) : ch4_stride(NCOL);  // record row stride
     const int NPR = NCP / 2;
@@ -705,11 +708,11 @@ namespace mtb {
 // Replaces the per-thread high-byte counters of k_vert2_u16 (544 B per
 // thread) by shared records (340 B per column): more resident threads and
 // no read-modify-write chains in the high-byte step.
-template <int T, int G, int M>
+template <int T, int G, int M, int NF = 0>
 __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
-    const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
+    const int r = NF ? NF / 2 : p.radius, H = p.H, W = p.W, n = NF ? NF : 2 * r + 1;
     const int NCOL = T + 2 * r, RS = ch4_stride(NCOL);
     uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);                  // [85][RS]
     uint16_t *sc = reinterpret_cast<uint16_t *>(rec + CH4_RECS * RS);        // [16][T]
@@ -852,13 +855,13 @@ namespace mtb {
 // pair changes with shared-memory atomics (adjacent columns belong to
 // adjacent threads); counts never go below zero, so a per-byte decrement
 // never borrows across bytes.
-template <int T, int G, int M, int PL, bool STREAM>
+template <int T, int G, int M, int PL, bool STREAM, int NF = 0>
 __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
     constexpr int GP = G / 2;
     constexpr int PR = ch4p_recs(PL);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
-    const int r = p.radius, H = p.H, W = p.W, n = 2 * r + 1;
+    const int r = NF ? NF / 2 : p.radius, H = p.H, W = p.W, n = NF ? NF : 2 * r + 1;
     const int NCOL = T + 2 * r, NCP = colhist4p_ncolp(T, r), NPR = NCP / 2;
     uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCP] singles
     uint32_t *prs = rec + CH4_RECS * NCP;                     // [PR][NPR] pairs

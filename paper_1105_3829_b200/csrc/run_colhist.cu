@@ -7,11 +7,11 @@
 
 namespace mtb {
 
-template <int T, int S, int G, int M>
+template <int T, int S, int G, int M, int NF = 0>
 static int run_colhist_u8_gm(SlabParams p, int B, cudaStream_t s, const char *name) {
     const ColhistGeom g = colhist_geom(T, S, p.radius);
     const size_t smem = (size_t)g.bytes;
-    auto kern = k_colhist_u8<T, S, G, M>;
+    auto kern = k_colhist_u8<T, S, G, M, NF>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
@@ -38,16 +38,22 @@ static int run_colhist_u8_g(SlabParams p, int B, cudaStream_t s, const char *nam
 template <int T, int S>
 static int run_colhist_u8_ts(SlabParams p, int B, cudaStream_t s, const char *name) {
     const int n = 2 * p.radius + 1;
+    if (S == 1 && n <= 11) {  // compile-time window side for the radii this kernel serves
+        return with_fixed_n<3, 11>(n, [&](auto nf) {
+            constexpr int NF = decltype(nf)::value, G = carry_free_group(NF);
+            return run_colhist_u8_gm<T, S, G, NF % G, NF>(p, B, s, name);
+        });
+    }
     if (8 * n <= 255) return run_colhist_u8_g<T, S, 8>(p, B, s, name);
     if (4 * n <= 255) return run_colhist_u8_g<T, S, 4>(p, B, s, name);
     if (2 * n <= 255) return run_colhist_u8_g<T, S, 2>(p, B, s, name);
     return run_colhist_u8_g<T, S, 1>(p, B, s, name);
 }
 
-template <int T, int G, int M>
+template <int T, int G, int M, int NF = 0>
 static int run_colhist4_u8_gm(SlabParams p, int B, cudaStream_t s, const char *name) {
     const size_t smem = (size_t)colhist4_bytes(T, p.radius);
-    auto kern = p.in_rows ? k_colhist4_u8<T, G, M, true> : k_colhist4_u8<T, G, M, false>;
+    auto kern = p.in_rows ? k_colhist4_u8<T, G, M, true, NF> : k_colhist4_u8<T, G, M, false, NF>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
@@ -72,6 +78,12 @@ static int run_colhist4_u8_g(SlabParams p, int B, cudaStream_t s, const char *na
 template <int T>
 static int run_colhist4_u8(SlabParams p, int B, cudaStream_t s, const char *name) {
     const int n = 2 * p.radius + 1;
+    if (n >= 7 && n <= 21) {  // compile-time window side for the radii this kernel may serve (3..10)
+        return with_fixed_n<7, 21>(n, [&](auto nf) {
+            constexpr int NF = decltype(nf)::value, G = carry_free_group(NF);
+            return run_colhist4_u8_gm<T, G, NF % G, NF>(p, B, s, name);
+        });
+    }
     if (8 * n <= 255) return run_colhist4_u8_g<T, 8>(p, B, s, name);
     if (4 * n <= 255) return run_colhist4_u8_g<T, 4>(p, B, s, name);
     if (2 * n <= 255) return run_colhist4_u8_g<T, 2>(p, B, s, name);
@@ -86,14 +98,15 @@ int run_colhist4_256(SlabParams p, int B, cudaStream_t s) { return run_colhist4_
 int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
     int var = env_int("MTB_CH_VAR", -1);
     if (var < 0) {
-        // measured on config 2 (tools/probe.py sweep):
-        // 16-bin records for r <= 5; radix-4 records for 6..10; from r = 11,
-        // radix-4 with pair
-        // records for as many upper levels as keep two 256-thread CTAs per SM
+        // measured on config 2 with compile-time window sides (tools/probe.py
+        // sweep): 16-bin records for r <= 4; radix-4
+        // records for 5..10; from r = 11, radix-4 with pair records for as
+        // many upper levels as keep two 256-thread CTAs per SM (3 levels up
+        // to r = 15, 2 above)
         const int r = p.radius, lim = 113 * 1024;
-        var = r <= 5 ? 0
+        var = r <= 4 ? 0
               : r <= 10 ? 12
-              : (r <= 16 && colhist4p_bytes(256, r, 3) <= lim) ? 30
+              : (r <= 15 && colhist4p_bytes(256, r, 3) <= lim) ? 30
               : colhist4p_bytes(256, r, 2) <= lim ? 31
                                                    : 12;
     }

@@ -1,0 +1,11 @@
+// run_colhist16_fc.cu -- k_colhist16_u16 with compile-time window sides
+// n = 47..63 (one translation unit per range: parallel builds).
+#include "run_colhist16.cuh"
+
+namespace mtb {
+
+int run_colhist16_fixed_c(SlabParams p, int B, cudaStream_t s, bool wk) {
+    return run_colhist16_fixed<47, 63>(p, B, s, wk);
+}
+
+}  // namespace mtb

@@ -7,13 +7,13 @@
 
 namespace mtb {
 
-template <int T, int G, int M>
+template <int T, int G, int M, int NF = 0>
 static int run_colhist16s_u16_gm(SlabParams p, int B, cudaStream_t s) {
     const int n = 2 * p.radius + 1, NCOL = T + 2 * p.radius;
     const size_t smem = (size_t)colhist4_bytes(T, p.radius) + 16 * T * 2 + ((size_t)(n * T + 15) & ~(size_t)15) +
                         (size_t)NCOL * n * 2;
     if (smem > 220 * 1024) return run_colhist16_u16(p, B, s, false);  // sorted columns too large: two-phase kernel
-    auto kern = k_colhist16s_u16<T, G, M>;
+    auto kern = k_colhist16s_u16<T, G, M, NF>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
@@ -39,6 +39,12 @@ static int run_colhist16s_u16_g(SlabParams p, int B, cudaStream_t s) {
 // widely spread 16-bit data; sorted columns need n <= 255 (u8 run starts)
 int run_colhist16s_u16(SlabParams p, int B, cudaStream_t s) {
     const int n = 2 * p.radius + 1;
+    if (n >= 5 && n <= 33) {  // compile-time window side for the radii this kernel serves (r <= 16)
+        return with_fixed_n<5, 33>(n, [&](auto nf) {
+            constexpr int NF = decltype(nf)::value, G = carry_free_group(NF);
+            return run_colhist16s_u16_gm<128, G, NF % G, NF>(p, B, s);
+        });
+    }
     if (8 * n <= 255) return run_colhist16s_u16_g<128, 8>(p, B, s);
     if (4 * n <= 255) return run_colhist16s_u16_g<128, 4>(p, B, s);
     if (2 * n <= 255) return run_colhist16s_u16_g<128, 2>(p, B, s);

@@ -7,10 +7,10 @@
 
 namespace mtb {
 
-template <int T, int G, int M, int PL>
+template <int T, int G, int M, int PL, int NF = 0>
 static int run_colhist4p_u8_gm(SlabParams p, int B, cudaStream_t s, const char *name) {
     const size_t smem = (size_t)colhist4p_bytes(T, p.radius, PL);
-    auto kern = p.in_rows ? k_colhist4p_u8<T, G, M, PL, true> : k_colhist4p_u8<T, G, M, PL, false>;
+    auto kern = p.in_rows ? k_colhist4p_u8<T, G, M, PL, true, NF> : k_colhist4p_u8<T, G, M, PL, false, NF>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
@@ -25,6 +25,18 @@ static int run_colhist4p_u8_gm(SlabParams p, int B, cudaStream_t s, const char *
 template <int T, int PL>
 static int run_colhist4p_u8(SlabParams p, int B, cudaStream_t s, const char *name) {
     const int n = 2 * p.radius + 1;
+    // compile-time window side for the radii each variant serves (PL = 3:
+    // r = 11..16, PL = 2: r = 17..31; run_colhist.cu)
+    if (PL == 3 && n >= 17 && n <= 37)
+        return with_fixed_n<17, 37>(n, [&](auto nf) {
+            constexpr int NF = decltype(nf)::value, G = carry_free_group(NF);  // even: n <= 127
+            return run_colhist4p_u8_gm<T, G, NF % G, PL, NF>(p, B, s, name);
+        });
+    if (PL == 2 && n >= 29 && n <= 63)
+        return with_fixed_n<29, 63>(n, [&](auto nf) {
+            constexpr int NF = decltype(nf)::value, G = carry_free_group(NF);  // even: n <= 127
+            return run_colhist4p_u8_gm<T, G, NF % G, PL, NF>(p, B, s, name);
+        });
     if (8 * n <= 255) {
         switch (n % 8) {
             case 1: return run_colhist4p_u8_gm<T, 8, 1, PL>(p, B, s, name);
