@@ -299,15 +299,15 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     //   median, r = 1 (8-bit)                     -> 3x3 kernels (k_med3t / k_med3)
     //   median, r = 2, 3                          -> sorted packed columns + shared merges (k_mednet)
     //   median, r = 1 (16-bit)                    -> selection network (k_sortnet<3>)
-    //   8-bit, r <= 31 (any rank)                 -> column-histogram gather
-    //   8-bit, 32 <= r <= 127                     -> CTMF tiles (O(1) in r)
+    //   8-bit, r <= 32 (any rank)                 -> column-histogram gather
+    //   8-bit, 33 <= r <= 127                     -> CTMF tiles (O(1) in r)
     //   otherwise                                 -> per-column vertical histograms
     if ((force.empty() || force == "sortnet" || force == "med3" || force == "mednet") && sortnet_applies<P>(p) &&
         (sizeof(P) == 2 || p.radius <= env_int("MTB_NET_MAX_R_U8", 3) || force == "sortnet" || force == "mednet"))
         return run_sortnet<P>(p, B, s);
     if (sizeof(P) == 1 && p.radius <= 63 && force == "lob") return run_lob_u8_32(p, B, s);
     if (sizeof(P) == 1 && n <= 255 &&
-        (force == "colhist" || (force.empty() && p.radius <= env_int("MTB_CH_MAX_R", 31))))
+        (force == "colhist" || (force.empty() && p.radius <= env_int("MTB_CH_MAX_R", 32))))
         return run_colhist_u8(p, B, s);
     if (sizeof(P) == 1 && !wide && (force == "ctmf" || force.empty())) return run_ctmf_u8(p, B, s);
     // 16-bit: compact high bytes (sampled spread <= MTB_U16_SPREAD) -> the

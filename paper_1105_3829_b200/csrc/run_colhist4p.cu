@@ -26,14 +26,14 @@ template <int T, int PL>
 static int run_colhist4p_u8(SlabParams p, int B, cudaStream_t s, const char *name) {
     const int n = 2 * p.radius + 1;
     // compile-time window side for the radii each variant serves (PL = 3:
-    // r = 11..16, PL = 2: r = 17..31; run_colhist.cu)
+    // r = 11..15, PL = 2: r = 16..32; run_colhist.cu)
     if (PL == 3 && n >= 17 && n <= 37)
         return with_fixed_n<17, 37>(n, [&](auto nf) {
             constexpr int NF = decltype(nf)::value, G = carry_free_group(NF);  // even: n <= 127
             return run_colhist4p_u8_gm<T, G, NF % G, PL, NF>(p, B, s, name);
         });
-    if (PL == 2 && n >= 29 && n <= 63)
-        return with_fixed_n<29, 63>(n, [&](auto nf) {
+    if (PL == 2 && n >= 29 && n <= 65)
+        return with_fixed_n<29, 65>(n, [&](auto nf) {
             constexpr int NF = decltype(nf)::value, G = carry_free_group(NF);  // even: n <= 127
             return run_colhist4p_u8_gm<T, G, NF % G, PL, NF>(p, B, s, name);
         });

@@ -6,13 +6,13 @@
 
 namespace mtb {
 
-template <int S>
+template <int S, int MF = -1>
 static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     const CtmfGeom g = ctmf_geom(S, p.radius);
     const int rows = p.row_end - p.row_begin;
     const int tiles_x = (p.W + g.TW - 1) / g.TW;
     const size_t smem = (size_t)g.warp_bytes * CT_WARPS;
-    auto kern = k_ctmf_u8<S>;
+    auto kern = k_ctmf_u8<S, MF>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CT_WARPS * 32, smem);
@@ -62,6 +62,14 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
 }
 
 int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
+    if (env_int("MTB_CT_S", 8) == 8) {  // n mod 8 as a compile-time constant (n odd)
+        switch ((2 * p.radius + 1) % 8) {
+            case 1: return run_ctmf_u8_s<8, 1>(p, B, s);
+            case 3: return run_ctmf_u8_s<8, 3>(p, B, s);
+            case 5: return run_ctmf_u8_s<8, 5>(p, B, s);
+            default: return run_ctmf_u8_s<8, 7>(p, B, s);
+        }
+    }
     return env_int("MTB_CT_S", 8) == 8 ? run_ctmf_u8_s<8>(p, B, s) : run_ctmf_u8_s<16>(p, B, s);
 }
 
