@@ -100,12 +100,13 @@ int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
     if (var < 0) {
         // measured on config 2 with compile-time window sides (tools/probe.py
         // sweep): 16-bin records for r <= 4; radix-4
-        // records for 5..10; from r = 11, radix-4 with pair records for as
+        // records for 5..10 (128-thread CTAs: 3% ahead of 256 and 512); from
+        // r = 11, radix-4 with pair records for as
         // many upper levels as keep two 256-thread CTAs per SM (3 levels up
         // to r = 15, 2 above)
         const int r = p.radius, lim = 113 * 1024;
         var = r <= 4 ? 0
-              : r <= 10 ? 12
+              : r <= 10 ? 13
               : (r <= 15 && colhist4p_bytes(256, r, 3) <= lim) ? 30
               : colhist4p_bytes(256, r, 2) <= lim ? 31
                                                    : 12;
@@ -116,6 +117,7 @@ int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
         case 30: return run_colhist4p_256(p, B, s, 3);
         case 31: return run_colhist4p_256(p, B, s, 2);
         case 34: return run_colhist4p_256(p, B, s, 1);
+        case 13: return run_colhist4_u8<128>(p, B, s, "k_colhist4_u8<128>");
         default: return run_colhist4_u8<256>(p, B, s, "k_colhist4_u8<256>");
     }
 }
