@@ -708,6 +708,8 @@ namespace mtb {
 // Replaces the per-thread high-byte counters of k_vert2_u16 (544 B per
 // thread) by shared records (340 B per column): more resident threads and
 // no read-modify-write chains in the high-byte step.
+constexpr int CH16S_CMAX = 24;  // low-byte candidates kept per thread (k_colhist16s_u16)
+
 template <int T, int G, int M, int NF = 0>
 __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -718,6 +720,7 @@ __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
     uint16_t *sc = reinterpret_cast<uint16_t *>(rec + CH4_RECS * RS);        // [16][T]
     uint8_t *rpos = reinterpret_cast<uint8_t *>(sc + 16 * T);                // [n][T]
     uint16_t *scol = reinterpret_cast<uint16_t *>(rpos + ((n * T + 15) & ~15));  // [NCOL][n]
+    uint8_t *cand = reinterpret_cast<uint8_t *>(scol + ((NCOL * n + 7) & ~7));     // [CH16S_CMAX][T]
     uint8_t *recb = reinterpret_cast<uint8_t *>(rec);
     const int X0 = blockIdx.x * T;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
@@ -782,8 +785,56 @@ __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
         // high byte and rank within it
         uint32_t k = p.rank;
         const unsigned hb = ch4_select<G, M>(rec + tid, RS, n, k);
-        // low byte: runs of [256H, 256H+256) in the window columns
+        // low byte: runs of [256H, 256H+256) in the window columns.  The
+        // low bytes found are collected (a handful on spread data: ~n^2/256
+        // per bin) and the k-th smallest is counted out of them; a bin with
+        // more than CH16S_CMAX values takes the two counting passes below.
         const unsigned vb = hb << 8, ve = vb + 256;
+        int cnt = 0;
+        for (int j0 = 0; j0 < n; j0 += 8) {
+            const uint16_t *aa[8];
+            unsigned vv[8];
+            int e0[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                aa[u] = wcol + min(j0 + u, n - 1) * n;
+                vv[u] = vb;
+            }
+            lower_bound_multi<8>(aa, n, vv, e0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (j0 + u >= n) break;
+                rpos[(j0 + u) * T + tid] = (uint8_t)e0[u];
+                const uint16_t *a = aa[u];
+                for (int e = e0[u]; e < n; ++e) {
+                    const unsigned v = a[e];
+                    if (v >= ve) break;
+                    if (cnt < CH16S_CMAX) cand[cnt * T + tid] = (uint8_t)v;
+                    ++cnt;
+                }
+            }
+        }
+        if (cnt <= CH16S_CMAX) {
+            // k-th smallest (1-based) of the cnt candidates: the value with
+            // fewer than k candidates below it and at least k at or below
+            unsigned lo = 0;
+            for (int i = 0; i < cnt; ++i) {
+                const unsigned ci = cand[i * T + tid];
+                uint32_t below = 0, atmost = 0;
+                for (int jj = 0; jj < cnt; ++jj) {
+                    const unsigned cj = cand[jj * T + tid];
+                    below += cj < ci ? 1u : 0u;
+                    atmost += cj <= ci ? 1u : 0u;
+                }
+                if (below < k && k <= atmost) {
+                    lo = ci;
+                    break;
+                }
+            }
+            const unsigned v = vb | lo;
+            if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint16_t)v;
+            continue;
+        }
 #pragma unroll
         for (int q = 0; q < 16; ++q) sc[q * T + tid] = 0;
         for (int j0 = 0; j0 < n; j0 += 8) {
