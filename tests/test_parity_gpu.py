@@ -594,3 +594,19 @@ def test_mednet_shapes_slabs_batch_lut(bits, rt, monkeypatch):
         # value map (reduced precision)
         o, _ = mtb.filter_image(px, n, max_error=16)
         assert np.array_equal(o.pixels, O.iot_filter(px, n, max_error=16)), n
+
+
+@pytest.mark.parametrize("ndev", [2, 3])
+def test_filter_image_device_slabs(ndev):
+    """filter_image(devices=[...]): one row slab per listed device with its
+    halo rows from the host copy (the multi-GPU decomposition; the same
+    device listed several times stands in for several GPUs here) -- equal to
+    the single-device result and the oracle, 8- and 16-bit, with bands."""
+    rng = np.random.default_rng(ndev)
+    px = workloads.cfg2_blur_sp_u8(301, 257, seed=ndev)
+    for n in (3, 9, 31):
+        out, _ = mtb.filter_image(px, n, devices=[0] * ndev, bands=2)
+        assert np.array_equal(out.pixels, O.iot_filter(px, n)), n
+    px16 = rng.integers(0, 65536, (123, 80)).astype(np.uint16)
+    out = mtb.median_filter(px16, 4, devices=[0] * ndev)
+    assert np.array_equal(out, O.iot_filter(px16, 9))
