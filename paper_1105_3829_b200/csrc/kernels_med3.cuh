@@ -283,13 +283,8 @@ __global__ void __launch_bounds__(128) k_med3t_u8(SlabParams p) {
         q[7] = __byte_perm(v.y, 0, 0x4342);
         q[8] = __byte_perm(v.y, R, 0x5453);
     };
-    uint32_t qa[9], qb[9], qc[9];
-    pack(0, qa);
-    pack(1, qb);
-    uint8_t *d = dst + (int64_t)(Y0 - p.row_begin) * p.dst_pitch + x0;
-#pragma unroll 1
-    for (int i = 2; i < NR; ++i) {
-        pack(i, qc);
+    // one output row from its three packed input rows
+    auto row_out = [&](const uint32_t (&qa)[9], const uint32_t (&qb)[9], const uint32_t (&qc)[9], uint8_t *d) {
         uint32_t mn[9], md[9], mx[9];
 #pragma unroll
         for (int m = 0; m < 9; ++m) {
@@ -314,12 +309,32 @@ __global__ void __launch_bounds__(128) k_med3t_u8(SlabParams p) {
             w1 = b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24);
         }
         if (act) *reinterpret_cast<uint2 *>(d) = make_uint2(w0, w1);
-        d += p.dst_pitch;
+    };
+    // two output rows per step (two independent selection chains per
+    // thread); staged rows i-2 .. i+1
+    uint32_t qa[9], qb[9];
+    pack(0, qa);
+    pack(1, qb);
+    uint8_t *d = dst + (int64_t)(Y0 - p.row_begin) * p.dst_pitch + x0;
+    int i = 2;
+#pragma unroll 1
+    for (; i + 1 < NR; i += 2) {
+        uint32_t qc[9], qd[9];
+        pack(i, qc);
+        pack(i + 1, qd);
+        row_out(qa, qb, qc, d);
+        row_out(qb, qc, qd, d + p.dst_pitch);
+        d += 2 * p.dst_pitch;
 #pragma unroll
         for (int m = 0; m < 9; ++m) {
-            qa[m] = qb[m];
-            qb[m] = qc[m];
+            qa[m] = qc[m];
+            qb[m] = qd[m];
         }
+    }
+    if (i < NR) {
+        uint32_t qc[9];
+        pack(i, qc);
+        row_out(qa, qb, qc, d);
     }
     stream_signal(p, Y0, Y1, X, X + 1024);
 }
