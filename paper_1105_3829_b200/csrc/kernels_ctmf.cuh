@@ -293,9 +293,96 @@ __device__ __forceinline__ bool ct_rows_aligned16(const void *src, int64_t pitch
 
 // MF >= 0: n mod S as a compile-time constant (measured: r = 63 1.11 -> 0.99 ms
 // with the whole radius fixed; the partial-chunk loops are what unrolls)
+// ---------------------------------------------------------------------------
+// k_ctmf_pre_u8: every tile row's span snapshots in one pass, before the
+// tiles run.  Thread = image column: it builds the 256-bin histogram of the
+// span of the first tile row of its segment (rows clamp(Y0-r .. Y0+r)),
+// then slides down tile row by tile row (one row out, one in per step),
+// writing after each tile row the 16-B cumulative coarse counts and the 16
+// fine chunks (17 x 16 B) at pre[(z*tiles_y + ty)*W + x].  The tiles then
+// initialise every pass from two 16-B loads per column instead of scanning
+// n rows per column twice (the two snapshot scans were ~25% of the CTMF
+// kernel's instructions).
+constexpr int CTP_T = 128;
+constexpr int CTP_STRIDE = 272;  // per-thread histogram bytes (17 x 16: 16-B aligned rows)
+
+template <int T = CTP_T>  // (a template: the header is included by several translation units)
+__global__ void __launch_bounds__(T) k_ctmf_pre_u8(SlabParams p, int tiles_y, int seg, uint4 *__restrict__ pre) {
+    // per thread 272 B = [cumulative coarse counts (16 B)][256 fine counts]:
+    // the warp's 32 records are one contiguous 8704-B block, laid out
+    // exactly as its 32 columns' snapshots in `pre` -> coalesced copy-out
+    __shared__ __align__(16) uint8_t hist[T * CTP_STRIDE];
+    const int tid = threadIdx.x, lane = tid & 31, warp0 = tid & ~31;
+    const int W = p.W, H = p.H, r = p.radius, th = p.rows_per_cta;
+    const int xw = blockIdx.x * T + warp0;  // the warp's first column
+    const int x = xw + lane;
+    const int ty0 = blockIdx.y * seg, ty1 = min(ty0 + seg, tiles_y);
+    const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
+    if (p.in_rows) {  // streaming: the segment's rows have arrived
+        stream_wait_rows(p, min(p.row_begin + ty1 * th + r, H));
+    }
+    if (xw >= W || ty0 >= ty1) return;  // warp-uniform (no block barriers below)
+    const int xc = min(x, W - 1);  // lanes past the image edge shadow the last column
+    uint8_t *rec = hist + tid * CTP_STRIDE;
+    uint8_t *h = rec + 16;
+    uint4 *h4 = reinterpret_cast<uint4 *>(h);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) h4[q] = make_uint4(0, 0, 0, 0);
+    const int Ya = p.row_begin + ty0 * th;
+    // 16 loads in flight per thread (the rows come from L2; latency-bound otherwise)
+    int j = -r;
+    for (; j + 15 <= r; j += 16) {
+        unsigned v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = __ldg(src_row(p, src, clampi(Ya + j + u, 0, H - 1)) + xc);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) h[v[u]] += 1;
+    }
+    for (; j <= r; ++j) h[__ldg(src_row(p, src, clampi(Ya + j, 0, H - 1)) + xc)] += 1;
+    int y = Ya;
+    const int nw = min(32, W - xw);  // columns of this warp inside the image
+    for (int ty = ty0; ty < ty1; ++ty) {
+        const int Y0 = p.row_begin + ty * th;
+        for (; y + 8 <= Y0; y += 8) {  // slide the span down to rows Y0-r .. Y0+r
+            unsigned vo[8], vi[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                vo[u] = __ldg(src_row(p, src, clampi(y + u - r, 0, H - 1)) + xc);
+                vi[u] = __ldg(src_row(p, src, clampi(y + u + r + 1, 0, H - 1)) + xc);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                h[vo[u]] -= 1;
+                h[vi[u]] += 1;
+            }
+        }
+        for (; y < Y0; ++y) {
+            const unsigned vo = __ldg(src_row(p, src, clampi(y - r, 0, H - 1)) + xc);
+            const unsigned vi = __ldg(src_row(p, src, clampi(y + r + 1, 0, H - 1)) + xc);
+            h[vo] -= 1;
+            h[vi] += 1;
+        }
+        uint32_t acc = 0, cw[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const uint4 c = h4[q];
+            cw[q >> 2] |= acc << (8 * (q & 3));
+            acc += __vsadu4(c.x, 0) + __vsadu4(c.y, 0) + __vsadu4(c.z, 0) + __vsadu4(c.w, 0);
+        }
+        *reinterpret_cast<uint4 *>(rec) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+        __syncwarp();
+        // copy-out: the warp's nw records, 16 B per lane and step
+        const uint4 *blk = reinterpret_cast<const uint4 *>(hist + warp0 * CTP_STRIDE);
+        uint4 *o = pre + ((size_t)(blockIdx.z * tiles_y + ty) * W + xw) * 17;
+        for (int e = lane; e < nw * 17; e += 32) o[e] = blk[e];
+        __syncwarp();
+    }
+}
+
 template <int S, int MF = -1>
 __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int tiles_x, int tiles_y,
-                                                        uint8_t *__restrict__ snap, int snap_two_scans) {
+                                                        uint8_t *__restrict__ snap, int snap_two_scans,
+                                                        const uint4 *__restrict__ pre) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -414,7 +501,9 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
         }
         __syncwarp();
     };
-    if (snap) {
+    // precomputed snapshots (k_ctmf_pre_u8): cu at pre_t[17 gx], chunk b at pre_t[17 gx + 1 + b]
+    const uint4 *pre_t = pre ? pre + (size_t)(blockIdx.z * tiles_y + ty) * W * 17 : nullptr;
+    if (snap && !pre) {
         const size_t slot = ((size_t)blockIdx.z * gridDim.x + blockIdx.x) * CT_WARPS + warp;
         uint8_t *rec = snap + slot * snap_stride;
         snap_cu = reinterpret_cast<uint4 *>(rec);
@@ -441,7 +530,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
     for (int pass = 0;; ++pass) {
         if (pass > 0) {
             if (tile_mask == 0) break;
-            if (pass == 1 && snap && snap_two_scans) {
+            if (pass == 1 && snap && !pre && snap_two_scans) {
                 __syncwarp();
                 snap_scan(false, true, tile_mask);
 #pragma unroll
@@ -478,12 +567,13 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
         };
         // --- column histograms for row Y0: rows clamp(Y0-r .. Y0+r)
         __syncwarp();
-        if (snap) {
+        if (snap || pre) {
             for (int c = lane; c < g.NCP; c += 32) {
                 uint32_t cnt[4] = {0, 0, 0, 0};
                 uint32_t bl = 0;
                 if (c < g.NC) {
-                    const uint4 cu = __ldcg(snap_cu + c);
+                    const int gxc = clampi(X0 - r + c, 0, W - 1);
+                    const uint4 cu = pre ? __ldcg(pre_t + (size_t)gxc * 17) : __ldcg(snap_cu + c);
                     // coarse counts = next cumulative - cumulative (bytewise, no borrow)
                     const uint32_t cwv[4] = {cu.x, cu.y, cu.z, cu.w};
                     const uint32_t nxt[4] = {__funnelshift_r(cwv[0], cwv[1], 8), __funnelshift_r(cwv[1], cwv[2], 8),
@@ -499,6 +589,10 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
                         bl = (wsel >> (8 * (beta & 3))) & 0xffu;
                         const uint32_t dsel = beta < 8 ? (beta < 4 ? d[0] : d[1]) : (beta < 12 ? d[2] : d[3]);
                         if ((dsel >> (8 * (beta & 3))) & 0xffu) {
+                            uint4 f;
+                            if (pre) {
+                                f = __ldcg(pre_t + (size_t)gxc * 17 + 1 + beta);
+                            } else {
                             // chunk index = off + number of present bins below beta
                             int k = __ldcg(snap_off + c);
 #pragma unroll
@@ -507,7 +601,8 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
                                 const uint32_t sel = nb >= 4 ? 0xffffffffu : ((1u << (8 * nb)) - 1u);
                                 k += __popc(__vcmpne4(d[i], 0) & sel & needb[i]) >> 3;
                             }
-                            const uint4 f = __ldcg(snap_heap + k);
+                            f = __ldcg(snap_heap + k);
+                            }
                             cnt[0] = f.x; cnt[1] = f.y; cnt[2] = f.z; cnt[3] = f.w;
                         }
                     }

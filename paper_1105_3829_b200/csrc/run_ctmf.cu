@@ -42,19 +42,36 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     const int resident = (int)((sm_count() * per_sm + B - 1) / B);
     if (env_int("MTB_CT_PERSIST", 1) && ctas > resident) ctas = resident > 0 ? resident : 1;
     dim3 grid(ctas, 1, B);
+    // span snapshots of every tile row, computed up front (k_ctmf_pre_u8);
+    // MTB_CT_PRE=0: per-warp snapshot scans inside the tiles instead
+    uint4 *pre = nullptr;
+    if (env_int("MTB_CT_PRE", 1)) {
+        keep_pool_memory();
+        const size_t pre_bytes = (size_t)B * tiles_y * p.W * 17 * sizeof(uint4);
+        if (cudaMallocAsync(reinterpret_cast<void **>(&pre), pre_bytes, s) != cudaSuccess) {
+            cudaGetLastError();
+            pre = nullptr;
+        } else {
+            const int seg = env_int("MTB_CT_PRE_SEG", 2);
+            dim3 pg((p.W + CTP_T - 1) / CTP_T, (tiles_y + seg - 1) / seg, B);
+            k_ctmf_pre_u8<CTP_T><<<pg, CTP_T, 0, s>>>(p, tiles_y, seg, pre);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+        }
+    }
     // per-tile column snapshots (stream-ordered pool allocation, kept cached)
     uint8_t *snap = nullptr;
     const size_t snap_bytes = (size_t)ctas * CT_WARPS * B * ((((size_t)g.NCP * 18 + 15) & ~(size_t)15) + (size_t)g.NCP * 256);
-    if (env_int("MTB_CT_SNAP", 1)) {
+    if (!pre && env_int("MTB_CT_SNAP", 1)) {
         keep_pool_memory();
         if (cudaMallocAsync(reinterpret_cast<void **>(&snap), snap_bytes, s) != cudaSuccess) {
             cudaGetLastError();
             snap = nullptr;  // fall back to rescanning the spans
         }
     }
-    kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y, snap, env_int("MTB_CT_SCAN2", 1));
+    kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y, snap, env_int("MTB_CT_SCAN2", 1), pre);
     cudaError_t e = cudaGetLastError();
     if (snap) cudaFreeAsync(snap, s);
+    if (pre) cudaFreeAsync(pre, s);
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_ctmf_u8: ") + cudaGetErrorString(e));
     g_kernel = S == 8 ? "k_ctmf_u8<8>" : "k_ctmf_u8<16>";
     g_launches.fetch_add(1, std::memory_order_relaxed);
