@@ -43,7 +43,7 @@ struct CtmfGeom {
     int warp_bytes;
 };
 
-__host__ __device__ inline CtmfGeom ctmf_geom(int S, int r) {
+__host__ __device__ inline CtmfGeom ctmf_geom(int S, int r, int stage_rows = CT_STAGE_ROWS) {
     CtmfGeom g;
     g.S = S;
     g.TW = 32 * S;
@@ -52,7 +52,7 @@ __host__ __device__ inline CtmfGeom ctmf_geom(int S, int r) {
     g.colh_bytes = 2 * g.NCP * 16;
     g.below_bytes = (g.NCP + 8) * 2;  // + dummy counter
     g.SPB = (g.NC + 16 + 15) & ~15;
-    g.warp_bytes = g.colh_bytes + ((g.below_bytes + 15) & ~15) + CT_STAGE_ROWS * g.SPB;
+    g.warp_bytes = g.colh_bytes + ((g.below_bytes + 15) & ~15) + stage_rows * g.SPB;
     return g;
 }
 
@@ -379,8 +379,13 @@ __global__ void __launch_bounds__(T) k_ctmf_pre_u8(SlabParams p, int tiles_y, in
     }
 }
 
-template <int S, int MF = -1>
-__global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int tiles_x, int tiles_y,
+// PRE: initialised from k_ctmf_pre_u8's snapshots only (`pre` required):
+// no staged init batches, so the stage holds the two rows of a row update
+// and four CTAs fit per SM.  CTB: CTAs per SM the registers are budgeted
+// for (4: 16 warps at 128 registers, with spills -- pays from r ~ 80; 3:
+// 12 warps at 168).
+template <int S, int MF = -1, bool PRE = false, int CTB = 3>
+__global__ void __launch_bounds__(CT_WARPS * 32, CTB) k_ctmf_u8(SlabParams p, int tiles_x, int tiles_y,
                                                         uint8_t *__restrict__ snap, int snap_two_scans,
                                                         const uint4 *__restrict__ pre) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -391,7 +396,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
     const int first_tile = blockIdx.x * CT_WARPS + warp;
     if (first_tile >= tiles_x * tiles_y) return;
     const int r = p.radius;
-    const CtmfGeom g = ctmf_geom(S, r);
+    const CtmfGeom g = ctmf_geom(S, r, PRE ? 2 : CT_STAGE_ROWS);
     unsigned char *base = smem_raw + (size_t)warp * g.warp_bytes;
     uint4 *colA = reinterpret_cast<uint4 *>(base);               // bins 0-7
     uint4 *colB = colA + g.NCP;                                  // bins 8-15
@@ -503,7 +508,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
     };
     // precomputed snapshots (k_ctmf_pre_u8): cu at pre_t[17 gx], chunk b at pre_t[17 gx + 1 + b]
     const uint4 *pre_t = pre ? pre + (size_t)(blockIdx.z * tiles_y + ty) * W * 17 : nullptr;
-    if (snap && !pre) {
+    if (!PRE && snap && !pre) {
         const size_t slot = ((size_t)blockIdx.z * gridDim.x + blockIdx.x) * CT_WARPS + warp;
         uint8_t *rec = snap + slot * snap_stride;
         snap_cu = reinterpret_cast<uint4 *>(rec);
@@ -530,7 +535,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
     for (int pass = 0;; ++pass) {
         if (pass > 0) {
             if (tile_mask == 0) break;
-            if (pass == 1 && snap && !pre && snap_two_scans) {
+            if (!PRE && pass == 1 && snap && !pre && snap_two_scans) {
                 __syncwarp();
                 snap_scan(false, true, tile_mask);
 #pragma unroll
@@ -567,7 +572,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 3) k_ctmf_u8(SlabParams p, int 
         };
         // --- column histograms for row Y0: rows clamp(Y0-r .. Y0+r)
         __syncwarp();
-        if (snap || pre) {
+        if (PRE || snap || pre) {
             for (int c = lane; c < g.NCP; c += 32) {
                 uint32_t cnt[4] = {0, 0, 0, 0};
                 uint32_t bl = 0;

@@ -6,13 +6,16 @@
 
 namespace mtb {
 
+// use_pre: snapshots from k_ctmf_pre_u8 (the PRE kernel: 4 CTAs per SM);
+// if their workspace cannot be allocated, the per-tile scans instead
 template <int S, int MF = -1>
-static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
-    const CtmfGeom g = ctmf_geom(S, p.radius);
+static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s, bool use_pre) {
+    const CtmfGeom g = ctmf_geom(S, p.radius, use_pre ? 2 : CT_STAGE_ROWS);
     const int rows = p.row_end - p.row_begin;
     const int tiles_x = (p.W + g.TW - 1) / g.TW;
     const size_t smem = (size_t)g.warp_bytes * CT_WARPS;
-    auto kern = k_ctmf_u8<S, MF>;
+    const bool ctb4 = use_pre && p.radius >= env_int("MTB_CT_CTB4_R", 80);
+    auto kern = ctb4 ? k_ctmf_u8<S, MF, true, 4> : (use_pre ? k_ctmf_u8<S, MF, true, 3> : k_ctmf_u8<S, MF, false, 3>);
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CT_WARPS * 32, smem);
@@ -45,12 +48,12 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
     // span snapshots of every tile row, computed up front (k_ctmf_pre_u8);
     // MTB_CT_PRE=0: per-warp snapshot scans inside the tiles instead
     uint4 *pre = nullptr;
-    if (env_int("MTB_CT_PRE", 1)) {
+    if (use_pre) {
         keep_pool_memory();
         const size_t pre_bytes = (size_t)B * tiles_y * p.W * 17 * sizeof(uint4);
         if (cudaMallocAsync(reinterpret_cast<void **>(&pre), pre_bytes, s) != cudaSuccess) {
             cudaGetLastError();
-            pre = nullptr;
+            return run_ctmf_u8_s<S, MF>(p, B, s, false);
         } else {
             const int seg = env_int("MTB_CT_PRE_SEG", 2);
             dim3 pg((p.W + CTP_T - 1) / CTP_T, (tiles_y + seg - 1) / seg, B);
@@ -79,15 +82,16 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s) {
 }
 
 int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
+    const bool pre = env_int("MTB_CT_PRE", 1) != 0;
     if (env_int("MTB_CT_S", 8) == 8) {  // n mod 8 as a compile-time constant (n odd)
         switch ((2 * p.radius + 1) % 8) {
-            case 1: return run_ctmf_u8_s<8, 1>(p, B, s);
-            case 3: return run_ctmf_u8_s<8, 3>(p, B, s);
-            case 5: return run_ctmf_u8_s<8, 5>(p, B, s);
-            default: return run_ctmf_u8_s<8, 7>(p, B, s);
+            case 1: return run_ctmf_u8_s<8, 1>(p, B, s, pre);
+            case 3: return run_ctmf_u8_s<8, 3>(p, B, s, pre);
+            case 5: return run_ctmf_u8_s<8, 5>(p, B, s, pre);
+            default: return run_ctmf_u8_s<8, 7>(p, B, s, pre);
         }
     }
-    return env_int("MTB_CT_S", 8) == 8 ? run_ctmf_u8_s<8>(p, B, s) : run_ctmf_u8_s<16>(p, B, s);
+    return run_ctmf_u8_s<16>(p, B, s, pre);
 }
 
 template <int L>
