@@ -299,7 +299,10 @@ __device__ __forceinline__ bool ct_rows_aligned16(const void *src, int64_t pitch
 // span of the first tile row of its segment (rows clamp(Y0-r .. Y0+r)),
 // then slides down tile row by tile row (one row out, one in per step),
 // writing after each tile row the 16-B cumulative coarse counts and the 16
-// fine chunks (17 x 16 B) at pre[(z*tiles_y + ty)*W + x].  The tiles then
+// fine chunks: pre[((z*tiles_y + ty)*17 + q)*W + x], q = 0 the cumulative
+// counts, q = 1..16 the chunks -- component-major, so a warp's stores and
+// a tile's loads of one component over consecutive columns are contiguous.
+// The tiles then
 // initialise every pass from two 16-B loads per column instead of scanning
 // n rows per column twice (the two snapshot scans were ~25% of the CTMF
 // kernel's instructions).
@@ -308,14 +311,12 @@ constexpr int CTP_STRIDE = 272;  // per-thread histogram bytes (17 x 16: 16-B al
 
 template <int T = CTP_T>  // (a template: the header is included by several translation units)
 __global__ void __launch_bounds__(T) k_ctmf_pre_u8(SlabParams p, int tiles_y, int seg, uint4 *__restrict__ pre) {
-    // per thread 272 B = [cumulative coarse counts (16 B)][256 fine counts]:
-    // the warp's 32 records are one contiguous 8704-B block, laid out
-    // exactly as its 32 columns' snapshots in `pre` -> coalesced copy-out
+    // per thread 272 B = [cumulative coarse counts (16 B)][256 fine counts]
     __shared__ __align__(16) uint8_t hist[T * CTP_STRIDE];
-    const int tid = threadIdx.x, lane = tid & 31, warp0 = tid & ~31;
+    const int tid = threadIdx.x, warp0 = tid & ~31;
     const int W = p.W, H = p.H, r = p.radius, th = p.rows_per_cta;
     const int xw = blockIdx.x * T + warp0;  // the warp's first column
-    const int x = xw + lane;
+    const int x = xw + (tid & 31);
     const int ty0 = blockIdx.y * seg, ty1 = min(ty0 + seg, tiles_y);
     const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
     if (p.in_rows) {  // streaming: the segment's rows have arrived
@@ -340,7 +341,6 @@ __global__ void __launch_bounds__(T) k_ctmf_pre_u8(SlabParams p, int tiles_y, in
     }
     for (; j <= r; ++j) h[__ldg(src_row(p, src, clampi(Ya + j, 0, H - 1)) + xc)] += 1;
     int y = Ya;
-    const int nw = min(32, W - xw);  // columns of this warp inside the image
     for (int ty = ty0; ty < ty1; ++ty) {
         const int Y0 = p.row_begin + ty * th;
         for (; y + 8 <= Y0; y += 8) {  // slide the span down to rows Y0-r .. Y0+r
@@ -369,13 +369,12 @@ __global__ void __launch_bounds__(T) k_ctmf_pre_u8(SlabParams p, int tiles_y, in
             cw[q >> 2] |= acc << (8 * (q & 3));
             acc += __vsadu4(c.x, 0) + __vsadu4(c.y, 0) + __vsadu4(c.z, 0) + __vsadu4(c.w, 0);
         }
-        *reinterpret_cast<uint4 *>(rec) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
-        __syncwarp();
-        // copy-out: the warp's nw records, 16 B per lane and step
-        const uint4 *blk = reinterpret_cast<const uint4 *>(hist + warp0 * CTP_STRIDE);
-        uint4 *o = pre + ((size_t)(blockIdx.z * tiles_y + ty) * W + xw) * 17;
-        for (int e = lane; e < nw * 17; e += 32) o[e] = blk[e];
-        __syncwarp();
+        if (x < W) {
+            uint4 *o = pre + (size_t)(blockIdx.z * tiles_y + ty) * 17 * W + x;
+            o[0] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) o[(size_t)(1 + q) * W] = h4[q];
+        }
     }
 }
 
@@ -506,8 +505,8 @@ __global__ void __launch_bounds__(CT_WARPS * 32, CTB) k_ctmf_u8(SlabParams p, in
         }
         __syncwarp();
     };
-    // precomputed snapshots (k_ctmf_pre_u8): cu at pre_t[17 gx], chunk b at pre_t[17 gx + 1 + b]
-    const uint4 *pre_t = pre ? pre + (size_t)(blockIdx.z * tiles_y + ty) * W * 17 : nullptr;
+    // precomputed snapshots (k_ctmf_pre_u8): cu at pre_t[gx], chunk b at pre_t[(1 + b) W + gx]
+    const uint4 *pre_t = pre ? pre + (size_t)(blockIdx.z * tiles_y + ty) * 17 * W : nullptr;
     if (!PRE && snap && !pre) {
         const size_t slot = ((size_t)blockIdx.z * gridDim.x + blockIdx.x) * CT_WARPS + warp;
         uint8_t *rec = snap + slot * snap_stride;
@@ -578,7 +577,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32, CTB) k_ctmf_u8(SlabParams p, in
                 uint32_t bl = 0;
                 if (c < g.NC) {
                     const int gxc = clampi(X0 - r + c, 0, W - 1);
-                    const uint4 cu = pre ? __ldcg(pre_t + (size_t)gxc * 17) : __ldcg(snap_cu + c);
+                    const uint4 cu = pre ? __ldcg(pre_t + gxc) : __ldcg(snap_cu + c);
                     // coarse counts = next cumulative - cumulative (bytewise, no borrow)
                     const uint32_t cwv[4] = {cu.x, cu.y, cu.z, cu.w};
                     const uint32_t nxt[4] = {__funnelshift_r(cwv[0], cwv[1], 8), __funnelshift_r(cwv[1], cwv[2], 8),
@@ -596,7 +595,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32, CTB) k_ctmf_u8(SlabParams p, in
                         if ((dsel >> (8 * (beta & 3))) & 0xffu) {
                             uint4 f;
                             if (pre) {
-                                f = __ldcg(pre_t + (size_t)gxc * 17 + 1 + beta);
+                                f = __ldcg(pre_t + (size_t)(1 + beta) * W + gxc);
                             } else {
                             // chunk index = off + number of present bins below beta
                             int k = __ldcg(snap_off + c);
