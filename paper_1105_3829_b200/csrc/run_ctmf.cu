@@ -25,7 +25,9 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s, bool use_pre) {
     const int n = 2 * p.radius + 1;
     const int64_t warps = (int64_t)sm_count() * per_sm * CT_WARPS;
     const double per_stripe = (double)warps / ((double)tiles_x * B);  // warps per column stripe
-    const int target = env_int("MTB_CT_MIN_TH", n / 3 > 24 ? n / 3 : 24);
+    // (with up-front snapshots a tile's init is two loads per column: from
+    // n >= 97 shorter tiles balance better -- r = 63 0.82 -> 0.79 ms)
+    const int target = env_int("MTB_CT_MIN_TH", (use_pre && n >= 97) ? 24 : (n / 3 > 24 ? n / 3 : 24));
     int th;
     if (per_stripe >= 1.0) {
         int k = (int)((double)rows / (target * per_stripe) + 0.5);
