@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
 #pragma unroll
             for (int u = 0; u < CH_PF; ++u) {
                 const int c = tid + u * T;
-                if (c < g.NC && pvo[u] != pvi[u]) bump(c, pvo[u], pvi[u]);
+                if (c < g.NC) bump(c, pvo[u], pvi[u]);  // (vo == vi cancels: no data-dependent branch)
             }
             if (g.NC > CH_PF * T) {  // narrow CTA, wide halo: the rest without prefetch
                 const uint8_t *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
@@ -442,8 +442,7 @@ __device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uin
     auto bump2 = [&](int c, unsigned vo, unsigned vi) {
         extra(c, vo, -1);
         extra(c, vi, 1);
-        const int ko = key(vo), ki = key(vi);
-        if (ko == ki) return;
+        const int ko = key(vo), ki = key(vi);  // (ko == ki cancels: no data-dependent branch)
         if (ko >= 0) {
             ch4_bump(recb, RS, c, (unsigned)ko, -1);
             if (PL > 0) pbump(c, (unsigned)ko, -1);
@@ -494,7 +493,7 @@ __device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uin
 #pragma unroll
             for (int u = 0; u < CH_PF; ++u) {
                 const int c = tid + u * T;
-                if (c < NCOL && pvo[u] != pvi[u]) bump2(c, pvo[u], pvi[u]);
+                if (c < NCOL) bump2(c, pvo[u], pvi[u]);
             }
             if (NCOL > CH_PF * T) {  // narrow CTA, wide halo: the rest without prefetch
                 const P *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
@@ -969,7 +968,7 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
 #pragma unroll
             for (int u = 0; u < CH_PF; ++u) {
                 const int c = tid + u * T;
-                if (c < NCOL && pvo[u] != pvi[u]) {
+                if (c < NCOL) {  // (vo == vi cancels: no data-dependent branch)
                     ch4_bump(recb, NCP, c, pvo[u], -1);
                     ch4_bump(recb, NCP, c, pvi[u], 1);
                     pbump(c, pvo[u], -1);
