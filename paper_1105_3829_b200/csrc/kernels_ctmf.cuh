@@ -372,8 +372,13 @@ __global__ void __launch_bounds__(T) k_ctmf_pre_u8(SlabParams p, int tiles_y, in
         if (x < W) {
             uint4 *o = pre + (size_t)(blockIdx.z * tiles_y + ty) * 17 * W + x;
             o[0] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+            // empty chunks are not written: a tile loads chunk b only when the
+            // cumulative counts show coarse bin b present in the column
 #pragma unroll
-            for (int q = 0; q < 16; ++q) o[(size_t)(1 + q) * W] = h4[q];
+            for (int q = 0; q < 16; ++q) {
+                const uint4 c = h4[q];
+                if (c.x | c.y | c.z | c.w) o[(size_t)(1 + q) * W] = c;
+            }
         }
     }
 }
