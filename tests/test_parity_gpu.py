@@ -610,3 +610,32 @@ def test_filter_image_device_slabs(ndev):
     px16 = rng.integers(0, 65536, (123, 80)).astype(np.uint16)
     out = mtb.median_filter(px16, 4, devices=[0] * ndev)
     assert np.array_equal(out, O.iot_filter(px16, 9))
+
+
+@pytest.mark.parametrize("pre,ctb4", [("1", "1000"), ("1", "1"), ("0", "1000")])
+def test_ctmf_slabs_batch_lut(pre, ctb4, monkeypatch):
+    """The CTMF tile kernel with up-front span snapshots (both register
+    budgets) and with per-tile scans: slab calls with row_begin > 0 (the
+    snapshot rows follow the slab), a batch of images (one snapshot set per
+    image), a value map, a ragged last tile column -- all vs the oracle."""
+    from paper_1105_3829_b200 import _lib
+
+    monkeypatch.setenv("MTB_KERNEL", "ctmf")
+    monkeypatch.setenv("MTB_CT_PRE", pre)
+    monkeypatch.setenv("MTB_CT_CTB4_R", ctb4)
+    px = workloads.cfg2_blur_sp_u8(230, 333, seed=11)
+    H = px.shape[0]
+    for r in (33, 48, 63):
+        ref = O.iot_filter(px, 2 * r + 1)
+        dev = torch.from_numpy(px).cuda()
+        for a, b in [(0, 57), (57, 170), (170, 230)]:
+            top, bot = max(0, a - r), min(H, b + r)
+            out = mtb.rank_filter(dev[top:bot], r, rows=(a, b), src_row0=top, height=H)
+            assert _lib.last_kernel().startswith("k_ctmf_u8")
+            assert np.array_equal(out.cpu().numpy(), ref[a:b]), (r, a, b)
+    bt = workloads.cfg5_batch_u8(3, 150, 290)
+    out = mtb.rank_filter(torch.from_numpy(bt).cuda(), 40).cpu().numpy()
+    for i in range(3):
+        assert np.array_equal(out[i], O.iot_filter(bt[i], 81)), i
+    o, _ = mtb.filter_image(px, 99, max_error=8)
+    assert np.array_equal(o.pixels, O.iot_filter(px, 99, max_error=8))
