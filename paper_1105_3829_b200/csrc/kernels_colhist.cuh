@@ -307,6 +307,23 @@ __device__ __forceinline__ void ch4_bump(uint8_t *recb, int NCOL, int c, unsigne
     recb[((21 + (v >> 2)) * NCOL + c) * 4 + (v & 3)] += d;
 }
 
+// The same for the per-row updates: one shared-memory atomic add per level
+// (a single instruction; the word belongs to this thread's column, so
+// there is no contention), the +-1 shifted into the byte of the digit (a
+// decrement never borrows: the count it decrements is >= 1).  Measured
+// 9-20% faster kernels at r = 5..31 than byte read-modify-writes.  The
+// column builds of ch4_sweep and k_colhist16s keep the byte form (atomic
+// builds made the 16-bit keyed sweeps 20% slower); k_colhist4p uses atomics
+// for its build as well.
+__device__ __forceinline__ void ch4_bump_upd(uint8_t *recb, int NCOL, int c, unsigned v, int d) {
+    uint32_t *rw = reinterpret_cast<uint32_t *>(recb);
+    const unsigned one = (unsigned)d;
+    atomicAdd(rw + (0 * NCOL + c), one << (8 * (v >> 6)));
+    atomicAdd(rw + ((1 + (v >> 6)) * NCOL + c), one << (8 * ((v >> 4) & 3)));
+    atomicAdd(rw + ((5 + (v >> 4)) * NCOL + c), one << (8 * ((v >> 2) & 3)));
+    atomicAdd(rw + ((21 + (v >> 2)) * NCOL + c), one << (8 * (v & 3)));
+}
+
 // PL = number of levels with pair records (3: levels 0-2, 21 record rows;
 // 2: levels 0-1, 5 rows) -- fewer when shared memory would otherwise drop
 // the CTA below two per SM.
@@ -444,11 +461,11 @@ __device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uin
         extra(c, vi, 1);
         const int ko = key(vo), ki = key(vi);  // (ko == ki cancels: no data-dependent branch)
         if (ko >= 0) {
-            ch4_bump(recb, RS, c, (unsigned)ko, -1);
+            ch4_bump_upd(recb, RS, c, (unsigned)ko, -1);
             if (PL > 0) pbump(c, (unsigned)ko, -1);
         }
         if (ki >= 0) {
-            ch4_bump(recb, RS, c, (unsigned)ki, 1);
+            ch4_bump_upd(recb, RS, c, (unsigned)ki, 1);
             if (PL > 0) pbump(c, (unsigned)ki, 1);
         }
     };
@@ -761,8 +778,8 @@ __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
                     const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
                     if (vo == vi) continue;
                     if ((vo >> 8) != (vi >> 8)) {
-                        ch4_bump(recb, RS, c, vo >> 8, -1);
-                        ch4_bump(recb, RS, c, vi >> 8, 1);
+                        ch4_bump_upd(recb, RS, c, vo >> 8, -1);
+                        ch4_bump_upd(recb, RS, c, vi >> 8, 1);
                     }
                     uint16_t *a = scol + c * n;
                     const uint16_t *const aa[2] = {a, a};
@@ -930,7 +947,10 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
     __syncthreads();
     for (int c = tid; c < NCOL; c += T) {
         const int gx = clampi(X0 - r + c, 0, W - 1);
-        for (int j = -r; j <= r; ++j) ch4_bump(recb, NCP, c, __ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx), 1);
+        // (atomic adds here too: measured r = 15 0.358 -> 0.319 ms, r = 31
+        // 0.595 -> 0.530 against byte read-modify-writes)
+        for (int j = -r; j <= r; ++j)
+            ch4_bump_upd(recb, NCP, c, __ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx), 1);
     }
     __syncthreads();
     for (int i = tid; i < PR * NPR; i += T) {
@@ -969,8 +989,8 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
             for (int u = 0; u < CH_PF; ++u) {
                 const int c = tid + u * T;
                 if (c < NCOL) {  // (vo == vi cancels: no data-dependent branch)
-                    ch4_bump(recb, NCP, c, pvo[u], -1);
-                    ch4_bump(recb, NCP, c, pvi[u], 1);
+                    ch4_bump_upd(recb, NCP, c, pvo[u], -1);
+                    ch4_bump_upd(recb, NCP, c, pvi[u], 1);
                     pbump(c, pvo[u], -1);
                     pbump(c, pvi[u], 1);
                 }
@@ -982,8 +1002,8 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
                     const int gx = clampi(X0 - r + c, 0, W - 1);
                     const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
                     if (vo == vi) continue;
-                    ch4_bump(recb, NCP, c, vo, -1);
-                    ch4_bump(recb, NCP, c, vi, 1);
+                    ch4_bump_upd(recb, NCP, c, vo, -1);
+                    ch4_bump_upd(recb, NCP, c, vi, 1);
                     pbump(c, vo, -1);
                     pbump(c, vi, 1);
                 }
