@@ -155,12 +155,15 @@ __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
 
     const int k0 = tid * S;  // stripe column of the first window's left edge
     const int xt = X0 + k0;
+    // one shared-memory atomic add per counter (see ch4_bump_upd): the
+    // 32-bit word holding the byte, +-1 shifted into it
+    uint32_t *recw = reinterpret_cast<uint32_t *>(smem_raw);
     auto bump = [&](int c, unsigned vo, unsigned vi) {
         const int pc = ch_pos<S>(c, NCS);
-        recb[((vo >> 4) * NPOS + pc) * 16 + (vo & 15)] -= 1;
-        recb[((vi >> 4) * NPOS + pc) * 16 + (vi & 15)] += 1;
-        recb[(16 * NPOS + pc) * 16 + (vo >> 4)] -= 1;
-        recb[(16 * NPOS + pc) * 16 + (vi >> 4)] += 1;
+        atomicAdd(recw + ((vo >> 4) * NPOS + pc) * 4 + ((vo & 15) >> 2), 0xffffffffu << (8 * (vo & 3)));
+        atomicAdd(recw + ((vi >> 4) * NPOS + pc) * 4 + ((vi & 15) >> 2), 1u << (8 * (vi & 3)));
+        atomicAdd(recw + (16 * NPOS + pc) * 4 + (vo >> 6), 0xffffffffu << (8 * ((vo >> 4) & 3)));
+        atomicAdd(recw + (16 * NPOS + pc) * 4 + (vi >> 6), 1u << (8 * ((vi >> 4) & 3)));
     };
     // the stripe columns this thread moves down each row; their leaving /
     // entering pixels of the NEXT row are loaded a row ahead (latency hidden
