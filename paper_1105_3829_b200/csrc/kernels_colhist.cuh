@@ -145,10 +145,11 @@ __global__ void __launch_bounds__(T) k_colhist_u8(SlabParams p) {
     for (int c = tid; c < g.NC; c += T) {
         const int gx = clampi(X0 - r + c, 0, W - 1);
         const int pc = ch_pos<S>(c, NCS);
+        uint32_t *rw = reinterpret_cast<uint32_t *>(smem_raw);
         for (int j = -r; j <= r; ++j) {
             const unsigned v = __ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx);
-            recb[((v >> 4) * NPOS + pc) * 16 + (v & 15)] += 1;
-            recb[(16 * NPOS + pc) * 16 + (v >> 4)] += 1;
+            atomicAdd(rw + ((v >> 4) * NPOS + pc) * 4 + ((v & 15) >> 2), 1u << (8 * (v & 3)));
+            atomicAdd(rw + (16 * NPOS + pc) * 4 + (v >> 6), 1u << (8 * ((v >> 4) & 3)));
         }
     }
     __syncthreads();
@@ -550,13 +551,13 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
     const int x = X0 + tid;
     if (STREAM) stream_wait_rows(p, y1 + r);
-    ch4_sweep<T, 0, uint8_t>(
-        p, src, rec, NCOL, X0, y0, y1 - 1, [](unsigned v) { return (int)v; },
-        [&](int y) {
-            uint32_t k = p.rank;
-            const unsigned v = ch4_select<G, M>(rec + tid, RS, n, k);
-            if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
-        });
+    auto key = [](unsigned v) { return (int)v; };
+    auto pix = [&](int y) {
+        uint32_t k = p.rank;
+        const unsigned v = ch4_select<G, M>(rec + tid, RS, n, k);
+        if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
+    };
+    ch4_sweep<T, 0, uint8_t>(p, src, rec, NCOL, X0, y0, y1 - 1, key, pix);
     if (STREAM) stream_signal(p, y0, y1, X0, X0 + T);
 }
 
