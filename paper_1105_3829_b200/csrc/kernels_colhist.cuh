@@ -810,26 +810,29 @@ __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
         // per bin) and the k-th smallest is counted out of them; a bin with
         // more than CH16S_CMAX values takes the two counting passes below.
         const unsigned vb = hb << 8, ve = vb + 256;
+        // Each window column's run of high byte H is read off the column's
+        // high-byte records, no search: its start is the column's count of
+        // high bytes below H (the bytes below H's digit in the four record
+        // words on H's path) and its length the count of H (the last
+        // word's byte) -- four independent loads per column instead of a
+        // dependent binary search plus a scan to the run's end.
         int cnt = 0;
-        for (int j0 = 0; j0 < n; j0 += 8) {
-            const uint16_t *aa[8];
-            unsigned vv[8];
-            int e0[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                aa[u] = wcol + min(j0 + u, n - 1) * n;
-                vv[u] = vb;
-            }
-            lower_bound_multi<8>(aa, n, vv, e0);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (j0 + u >= n) break;
-                rpos[(j0 + u) * T + tid] = (uint8_t)e0[u];
-                const uint16_t *a = aa[u];
-                for (int e = e0[u]; e < n; ++e) {
-                    const unsigned v = a[e];
-                    if (v >= ve) break;
-                    if (cnt < CH16S_CMAX) cand[cnt * T + tid] = (uint8_t)v;
+        {
+            const unsigned d3 = hb >> 6, d2 = (hb >> 4) & 3, d1 = (hb >> 2) & 3, d0 = hb & 3;
+            const uint32_t *r0 = rec + tid, *r1 = rec + (1 + d3) * RS + tid;
+            const uint32_t *r2 = rec + (5 + (hb >> 4)) * RS + tid, *r3 = rec + (21 + (hb >> 2)) * RS + tid;
+            auto below = [](uint32_t w, unsigned d) {  // sum of the bytes below byte d (<= n < 256)
+                const uint32_t m = d ? (0xffffffffu >> (32 - 8 * d)) : 0u;
+                return ((w & m) * 0x01010101u) >> 24;
+            };
+            for (int j = 0; j < n; ++j) {
+                const uint32_t w3 = r3[j];
+                const int e0 = (int)(below(r0[j], d3) + below(r1[j], d2) + below(r2[j], d1) + below(w3, d0));
+                const int ne = (int)((w3 >> (8 * d0)) & 0xffu);
+                rpos[j * T + tid] = (uint8_t)e0;
+                const uint16_t *a = wcol + j * n;
+                for (int e = e0; e < e0 + ne; ++e) {
+                    if (cnt < CH16S_CMAX) cand[cnt * T + tid] = (uint8_t)a[e];
                     ++cnt;
                 }
             }
