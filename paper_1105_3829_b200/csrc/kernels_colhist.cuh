@@ -632,7 +632,6 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
         H0 = flags[0];
         for (int i = tid; i < 256; i += T) hlast[i] = -1;
         for (int i = tid; i < NCP; i += T) rec3[i] = 0;
-        uint8_t *r3b = reinterpret_cast<uint8_t *>(rec3);
         const int h0 = H0;
         ch4_sweep<T, PL, uint16_t>(
             p, src, rec, NCOL, X0, y0, y1 - 1,
@@ -661,9 +660,10 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
                 }
             },
             prs, NCP,
-            [r3b, h0](int c, unsigned v, int d) {
+            [rec3, h0](int c, unsigned v, int d) {
+                // one shared-memory atomic add (see ch4_bump_upd)
                 const int hb = (int)(v >> 8);
-                r3b[c * 4 + (hb < h0 ? 0 : (hb == h0 ? 1 : 2))] += d;
+                atomicAdd(rec3 + c, (unsigned)d << (8 * (hb < h0 ? 0 : (hb == h0 ? 1 : 2))));
             });
         __syncthreads();
         if (flags[1] == 0) {  // every pixel of the tile resolved
