@@ -98,15 +98,14 @@ int run_colhist4_256(SlabParams p, int B, cudaStream_t s) { return run_colhist4_
 int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
     int var = env_int("MTB_CH_VAR", -1);
     if (var < 0) {
-        // measured on config 2 with compile-time window sides (tools/probe.py
-        // sweep): 16-bin records for r <= 4; radix-4
-        // records for 5..10 (128-thread CTAs: 3% ahead of 256 and 512); from
-        // r = 11, radix-4 with pair records for as
-        // many upper levels as keep two 256-thread CTAs per SM (3 levels up
-        // to r = 15, 2 above)
+        // measured on config 2 with compile-time window sides and atomic
+        // record updates (tools/probe.py sweep):
+        // 16-bin records for r <= 2; from r = 3 radix-4 records with pair
+        // records for as many upper levels as keep two 256-thread CTAs per
+        // SM (3 levels up to r = 15, 2 above).  Plain radix-4 (var 12/13)
+        // trails them by 3-15% over r = 3..10.
         const int r = p.radius, lim = 113 * 1024;
-        var = r <= 4 ? 0
-              : r <= 10 ? 13
+        var = r <= 2 ? 0
               : (r <= 15 && colhist4p_bytes(256, r, 3) <= lim) ? 30
               : colhist4p_bytes(256, r, 2) <= lim ? 31
                                                    : 12;

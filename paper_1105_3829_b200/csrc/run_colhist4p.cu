@@ -27,8 +27,8 @@ static int run_colhist4p_u8(SlabParams p, int B, cudaStream_t s, const char *nam
     const int n = 2 * p.radius + 1;
     // compile-time window side for the radii each variant serves (PL = 3:
     // r = 11..15, PL = 2: r = 16..32; run_colhist.cu)
-    if (PL == 3 && n >= 17 && n <= 37)
-        return with_fixed_n<17, 37>(n, [&](auto nf) {
+    if (PL == 3 && n >= 5 && n <= 37)
+        return with_fixed_n<5, 37>(n, [&](auto nf) {
             constexpr int NF = decltype(nf)::value, G = carry_free_group(NF);  // even: n <= 127
             return run_colhist4p_u8_gm<T, G, NF % G, PL, NF>(p, B, s, name);
         });
