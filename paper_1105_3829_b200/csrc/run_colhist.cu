@@ -102,11 +102,11 @@ int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
         // record updates (tools/probe.py sweep):
         // 16-bin records for r <= 2; from r = 3 radix-4 records with pair
         // records for as many upper levels as keep two 256-thread CTAs per
-        // SM (3 levels up to r = 15, 2 above).  Plain radix-4 (var 12/13)
+        // SM (3 levels up to r = 16, 2 above).  Plain radix-4 (var 12/13)
         // trails them by 3-15% over r = 3..10.
         const int r = p.radius, lim = 113 * 1024;
         var = r <= 2 ? 0
-              : (r <= 15 && colhist4p_bytes(256, r, 3) <= lim) ? 30
+              : (r <= 16 && colhist4p_bytes(256, r, 3) <= lim) ? 30
               : colhist4p_bytes(256, r, 2) <= lim ? 31
                                                    : 12;
     }
