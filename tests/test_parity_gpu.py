@@ -639,3 +639,41 @@ def test_ctmf_slabs_batch_lut(pre, ctb4, monkeypatch):
         assert np.array_equal(out[i], O.iot_filter(bt[i], 81)), i
     o, _ = mtb.filter_image(px, 99, max_error=8)
     assert np.array_equal(o.pixels, O.iot_filter(px, 99, max_error=8))
+
+
+# ------------------------------------------ every radius through the default dispatch
+
+_SWEEP_R = list(range(1, 71)) + [80, 90, 97]  # 97: the largest window a 97-row frame allows
+
+
+@pytest.mark.parametrize("kind", ["u8", "u8_smooth", "u16_uniform", "u16_compact"])
+def test_default_dispatch_every_radius(kind):
+    """Each radius 1..70 (and a spread above) through the default dispatch on
+    a ragged 97 x 333 frame: every compile-time window side the kernels are
+    instantiated for (merge networks, 16-bin, radix-4 and pair-record
+    column histograms, the sorted-column and two-phase 16-bit kernels, the
+    CTMF tiles) meets the oracle, for the median and an off-centre rank."""
+    from paper_1105_3829_b200 import _lib
+
+    rng = np.random.default_rng({"u8": 91, "u8_smooth": 94, "u16_uniform": 92, "u16_compact": 93}[kind])
+    h, w = 97, 333
+    if kind == "u8":
+        px = rng.integers(0, 256, (h, w)).astype(np.uint8)
+    elif kind == "u8_smooth":  # few levels, long runs: many rows whose in/out pixels cancel
+        px = ((np.arange(w)[None, :] // 40 + np.arange(h)[:, None] // 30) * 37 % 256
+              + rng.integers(0, 2, (h, w))).astype(np.uint8)
+    elif kind == "u16_uniform":
+        px = rng.integers(0, 65536, (h, w)).astype(np.uint16)
+    else:
+        px = (30000 + rng.normal(0, 300, (h, w))).clip(0, 65535).astype(np.uint16)
+    dev = torch.from_numpy(px).cuda()
+    seen = set()
+    for r in _SWEEP_R:
+        n = 2 * r + 1
+        for rank in (None, (n * n) // 5 + 1):
+            out = mtb.rank_filter(dev, r, rank=rank).cpu().numpy()
+            seen.add(_lib.last_kernel())
+            assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (kind, r, rank, _lib.last_kernel())
+    assert len(seen) >= 3, seen
+    with pytest.raises(ValueError):
+        mtb.rank_filter(dev, 98)
