@@ -708,16 +708,19 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
                 "H2D lut");
     }
     constexpr int NB = FramesCtx::NB;
-    // MTB_FRAMES_STREAM=1: streaming frames -- each frame's rows arrive in
-    // chunks (CTAs wait on a row counter) and its results leave in chunks
-    // (the copy-out stream waits on per-chunk pixel counters), so a frame
-    // also overlaps its OWN copies.  Off by default: on the config-2 sweep
-    // it measured 24.1 against 24.8 Gpix/s for whole-frame copies (the
-    // stream-op latencies cost more than the exposed first copy-in and last
-    // copy-out).
+    // Streaming frames: a frame's rows arrive in chunks (CTAs wait on a row
+    // counter) and its results leave in chunks (the copy-out stream waits on
+    // per-chunk pixel counters), so the frame also overlaps its OWN copies.
+    // MTB_FRAMES_STREAM = 4 (default): the first frame of the order only --
+    // its copy-in is the one nothing else hides (config-2 sweep, e2e, mean
+    // of 6 / 7 runs: 32.5 against 31.8 Gpix/s with whole-frame copies);
+    // 1: every frame (31.5: the stream-op latencies cost more than they
+    // hide in the middle of the sequence); 2: first and last (32.3, noisier);
+    // 3: last only (31.7); 0: none.
     write32_fn write32 = nullptr, wait32 = nullptr;
-    const bool streaming = env_int("MTB_FRAMES_STREAM", 0) != 0 && std::string(forced_kernel()) != "lob" &&
-                           stream_mem_ops(write32, wait32) && H >= 256;  // (lob has no streaming hooks)
+    const int smode = env_int("MTB_FRAMES_STREAM", 4);
+    const bool can_stream = smode != 0 && std::string(forced_kernel()) != "lob" &&
+                            stream_mem_ops(write32, wait32) && H >= 256;  // (lob has no streaming hooks)
     const size_t row = (size_t)W * es;
     const int KI = std::max(1, std::min(env_int("MTB_FRAMES_IN_CHUNKS", 4), H / 128));
     const int KO = std::max(1, std::min(env_int("MTB_FRAMES_OUT_CHUNKS", 4), std::min(FramesCtx::NFLAGS - 1, H / 128)));
@@ -745,6 +748,10 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
             break;
         }
         unsigned int *fl = ctx->dflags + j * FramesCtx::NFLAGS;
+        // smode 1: every frame streams; 2: the first and last (the copies
+        // nothing else hides); 3: the last only
+        const bool streaming = can_stream && (smode == 1 || (smode == 2 && (q == 0 || q == n - 1)) ||
+                                              (smode == 3 && q == n - 1) || (smode == 4 && q == 0));
         if (q >= NB) cudaStreamWaitEvent(ctx->sh, ctx->ek[j], 0);  // job i-NB done reading dsrc[j]
         if (streaming) {
             // counters reset before this frame's kernel or copy-out can look at them

@@ -202,7 +202,7 @@ def test_host_buffer_entry_point(rng):
                           O.iot_filter(px16, 7, max_error=16))
 
 
-@pytest.mark.parametrize("stream", ["1", "0"])
+@pytest.mark.parametrize("stream", ["1", "0", "2", "3", "4"])
 def test_host_frames_sequence(rng, stream, monkeypatch):
     """mtb_filter_host_frames: a sequence longer than the buffer ring (3),
     mixed radii and ranks, 8- and 16-bit, pinned and pageable frames, a value
