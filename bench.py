@@ -59,18 +59,51 @@ def _dist():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML
+    in-process every ~2 ms (a timed region of a few tens of ms still gets
+    many samples under load), else nvidia-smi -lms 50."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
-        self.index = index
+        cvd = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [x.strip() for x in cvd.split(",") if x.strip()]
+        self.index = int(ids[index]) if index < len(ids) and ids[index].isdigit() else index
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
         self.lines: list[str] = []
 
+    def _nvml_loop(self):
+        p, h = self.nvml
+        bits = [("hw_slowdown", getattr(p, "nvmlClocksEventReasonHwSlowdown", 0x8)),
+                ("hw_thermal_slowdown", getattr(p, "nvmlClocksEventReasonHwThermalSlowdown", 0x40)),
+                ("sw_thermal_slowdown", getattr(p, "nvmlClocksEventReasonSwThermalSlowdown", 0x20)),
+                ("sw_power_cap", getattr(p, "nvmlClocksEventReasonSwPowerCap", 0x4))]
+        mx = p.nvmlDeviceGetMaxClockInfo(h, p.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = p.nvmlDeviceGetClockInfo(h, p.NVML_CLOCK_SM)
+                rs = p.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                break
+            flags = ["Active" if rs & b else "Not Active" for _, b in bits]
+            self.lines.append(", ".join([str(sm), str(mx), hex(rs)] + flags))
+            time.sleep(0.002)
+
     def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index))
+            self._t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self._t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -87,6 +120,9 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.nvml is not None:
+            self.stop.set()
+            self._t.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
