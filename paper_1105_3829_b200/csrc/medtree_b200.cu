@@ -739,6 +739,24 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
         std::vector<int> byr(order);
         std::stable_sort(byr.begin(), byr.end(), [&](int a, int b) { return radii[a] > radii[b]; });
         for (int q = 0, lo = 0, hi = n - 1; q < n; ++q) order[q] = (q & 1) ? byr[hi--] : byr[lo++];
+        // MTB_FRAMES_PERM="a,b,...": positions in the radius-descending list (tuning)
+        if (const char *pe = getenv("MTB_FRAMES_PERM")) {
+            std::vector<int> perm;
+            for (const char *c = pe; *c;) {
+                char *e = nullptr;
+                const long v = strtol(c, &e, 10);
+                if (e == c) break;
+                perm.push_back((int)v);
+                c = *e ? e + 1 : e;
+            }
+            if ((int)perm.size() == n) {
+                std::vector<char> seen(n, 0);
+                bool okp = true;
+                for (int v : perm) okp = okp && v >= 0 && v < n && !seen[v] && (seen[v] = 1);
+                if (okp)
+                    for (int q = 0; q < n; ++q) order[q] = byr[perm[q]];
+            }
+        }
     }
     for (int q = 0; q < n && rc == MTB_OK; ++q) {
         const int i = order[q];
