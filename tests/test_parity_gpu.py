@@ -226,6 +226,18 @@ def test_host_frames_sequence(rng, stream, monkeypatch):
         assert np.array_equal(o, O.iot_filter(f, 7, max_error=16))
 
 
+@pytest.mark.parametrize("perm", ["6,0,5,1,4,2,3", "0,1,2,3,4,5,6", "0,0,1,2,3,4,5", "junk"])
+def test_host_frames_explicit_order(perm, monkeypatch):
+    """MTB_FRAMES_PERM reorders the processing (invalid lists are ignored):
+    every result still lands in its own output."""
+    monkeypatch.setenv("MTB_FRAMES_PERM", perm)
+    frames = [np.ascontiguousarray(np.roll(workloads.cfg2_blur_sp_u8(300, 150), 7 * i, axis=1)) for i in range(7)]
+    radii = [3, 1, 15, 7, 2, 31, 5]
+    outs = mtb.filter_host_frames(frames, radii)
+    for f, r, o in zip(frames, radii, outs):
+        assert np.array_equal(o, O.iot_filter(f, 2 * r + 1)), (perm, r)
+
+
 @pytest.mark.parametrize("bits,r,bands,stream", [(8, 2, None, None), (8, 9, "3", None), (8, 40, None, None),
                                                  (16, 5, None, None), (16, 20, "5", None), (8, 3, "16", None),
                                                  (8, 2, None, "1"), (8, 40, None, "0"), (8, 70, None, "1"),
