@@ -52,8 +52,10 @@ extern "C" {
 #define MTB_E_INVAL (-1)
 #define MTB_E_CUDA (-2)
 
-/* flags */
-#define MTB_FLAG_ADAPTIVE 1u   /* select the adaptive search variant (same result) */
+/* `flags` arguments are reserved: pass 0.  (The reference's adaptive
+ * topology only changes results at max_error > 1, where it enters as the
+ * value map `lut`; the kernels' data layout does not depend on it --
+ * DESIGN.md section 3.7.) */
 
 /* One 8-bit slab.  Replaces run_frame_u/run_frame_a for bit_depth 8. */
 int mtb_median_u8(const uint8_t *src, int64_t src_pitch, int32_t src_row0, int32_t src_rows,
@@ -89,6 +91,19 @@ int mtb_median_batch_u16(const uint16_t *src, int64_t src_image_stride, int64_t 
 int mtb_filter_host(const void *src, void *dst, int32_t bit_depth, int32_t H, int32_t W,
                     int32_t radius, int64_t rank, const void *lut, uint32_t flags);
 
+/* Output rows [row_begin, row_end) of an H x W HOST frame, on GPU `device`
+ * (-1: the calling thread's current device).  `src` is the whole frame
+ * (global row 0); only the rows the windows touch,
+ * [max(0,row_begin-radius), min(H,row_end+radius)), are read, straight from
+ * the host copy -- the reference's band with its n//2 halo rows
+ * (engine.py:243-262), clamped against the global frame.  `dst` receives
+ * rows [row_begin, row_end) (dst row 0 = global row row_begin).  One host
+ * thread per GPU, each with its own slab, filters a frame on several GPUs
+ * with no collective.  Synchronous. */
+int mtb_filter_host_rows(const void *src, void *dst, int32_t bit_depth, int32_t H, int32_t W,
+                         int32_t row_begin, int32_t row_end, int32_t radius, int64_t rank,
+                         const void *lut, uint32_t flags, int32_t device);
+
 /* A sequence of n_frames HOST frames of one geometry (e.g. a video, or one
  * frame at several radii), each filtered as by mtb_filter_host, with the
  * copies of neighbouring frames overlapped: frame i+1 goes host->device and
@@ -111,6 +126,10 @@ int mtb_filter_host_frames(const void *const *srcs, void *const *dsts, const int
 int mtb_rank_bruteforce(const void *src, int64_t src_pitch, void *dst, int64_t dst_pitch,
                         int32_t bit_depth, int32_t H, int32_t W, int32_t radius, int64_t rank,
                         void *stream);
+
+/* Make `device` current for the calling thread in this library's CUDA
+ * runtime (the host-buffer entries run on the current device). */
+int mtb_set_device(int32_t device);
 
 /* Kernel launches issued by this library since load (evidence counter). */
 uint64_t mtb_launch_count(void);

@@ -18,7 +18,6 @@ LIB_PATH = os.path.join(_PKG, "_build", "libmedtree_b200.so")
 MTB_OK = 0
 MTB_E_INVAL = -1
 MTB_E_CUDA = -2
-FLAG_ADAPTIVE = 1
 
 EXPORTS = (
     "mtb_median_u8",
@@ -26,8 +25,10 @@ EXPORTS = (
     "mtb_median_batch_u8",
     "mtb_median_batch_u16",
     "mtb_filter_host",
+    "mtb_filter_host_rows",
     "mtb_filter_host_frames",
     "mtb_rank_bruteforce",
+    "mtb_set_device",
     "mtb_launch_count",
     "mtb_last_kernel",
     "mtb_last_error",
@@ -68,6 +69,8 @@ def load() -> ctypes.CDLL:
             ("mtb_median_batch_u8", batch),
             ("mtb_median_batch_u16", batch),
             ("mtb_filter_host", [p, p, i32, i32, i32, i32, i64, p, u32]),
+            ("mtb_filter_host_rows", [p, p, i32, i32, i32, i32, i32, i32, i64, p, u32, i32]),
+            ("mtb_set_device", [i32]),
             ("mtb_filter_host_frames", [p, p, p, p, i32, i32, i32, i32, p, u32]),
             ("mtb_rank_bruteforce", [p, i64, p, i64, i32, i32, i32, i32, i64, p]),
         ):

@@ -30,7 +30,29 @@ struct SlabParams {
     const unsigned int *in_rows;
     unsigned int *out_px;
     int32_t out_chunk;
+    // set to 1 by a CTA that gave up waiting for its rows (STREAM_TIMEOUT_NS)
+    unsigned int *status;
+    // 16-bit dispatch by value spread (medtree_b200.cu::run_u16_colhist):
+    // spread = device word with the sampled number of distinct high bytes;
+    // gate = GATE_WIDE / GATE_COMPACT: the kernel exits at once unless the
+    // data is widely spread / compact (two launches, one does the work).
+    const int *spread;
+    int32_t gate;
 };
+
+constexpr int SPREAD_WIDE = 24;  // > 24 distinct sampled high bytes: widely spread
+constexpr int GATE_WIDE = 1, GATE_COMPACT = 2;
+constexpr int WK_FROM_SPREAD = 2;  // k_colhist16_u16 wk mode: window-keyed sweep iff compact
+
+__device__ __forceinline__ bool spread_is_wide(const SlabParams &p) {
+    return *reinterpret_cast<const volatile int *>(p.spread) > SPREAD_WIDE;
+}
+
+// true when a gated launch has nothing to do (uniform over the grid)
+__device__ __forceinline__ bool gate_off(const SlabParams &p) {
+    if (!p.gate) return false;
+    return (p.gate == GATE_WIDE) != spread_is_wide(p);
+}
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) {
     return v < lo ? lo : (v > hi ? hi : v);
@@ -49,11 +71,32 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *a) {
     return v;
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// A bound on the wait for source rows.  The host enqueues every copy and
+// "rows arrived" write before the launch, so the wait only ever covers
+// copy-engine time (a few ms per frame); if the rows never come (a broken
+// caller), the CTA records the timeout in p.status and carries on, so the
+// launch ends and the host reports an error instead of hanging.
+constexpr uint64_t STREAM_TIMEOUT_NS = 20ull * 1000 * 1000 * 1000;
+
 // spin (one thread) until source rows [0, need) have arrived
 __device__ __forceinline__ void stream_wait_rows_1(const SlabParams &p, int need) {
     if (!p.in_rows) return;
     need = min(need, p.H);
-    while ((int)ld_acquire(p.in_rows) < need) __nanosleep(256);
+    if ((int)ld_acquire(p.in_rows) >= need) return;
+    const uint64_t t0 = globaltimer_ns();
+    while ((int)ld_acquire(p.in_rows) < need) {
+        __nanosleep(256);
+        if (globaltimer_ns() - t0 > STREAM_TIMEOUT_NS) {
+            if (p.status) atomicExch(p.status, 1u);
+            return;
+        }
+    }
 }
 
 __device__ __forceinline__ void stream_wait_rows(const SlabParams &p, int need) {

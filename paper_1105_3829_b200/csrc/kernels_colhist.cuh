@@ -580,8 +580,10 @@ __global__ void __launch_bounds__(T) k_colhist4_u8(SlabParams p) {
 // rest (marked in the high-byte plane) go through phases A and B, which
 // then skip H0.
 template <int T, int G, int M, int PL, int NF = 0>
-__global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__restrict__ hplane, bool WK) {
+__global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__restrict__ hplane, int wk_mode) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (gate_off(p)) return;
+    const bool WK = wk_mode == WK_FROM_SPREAD ? !spread_is_wide(p) : wk_mode != 0;
     const int tid = threadIdx.x;
     const int r = NF ? NF / 2 : p.radius, W = p.W, n = NF ? NF : 2 * r + 1;
     const int NCOL = T + 2 * r;
@@ -733,6 +735,7 @@ constexpr int CH16S_CMAX = 24;  // low-byte candidates kept per thread (k_colhis
 template <int T, int G, int M, int NF = 0>
 __global__ void __launch_bounds__(T) k_colhist16s_u16(SlabParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (gate_off(p)) return;
     const int tid = threadIdx.x;
     const int r = NF ? NF / 2 : p.radius, H = p.H, W = p.W, n = NF ? NF : 2 * r + 1;
     const int NCOL = T + 2 * r, RS = ch4_stride(NCOL);

@@ -26,7 +26,8 @@ namespace mtb {
 // a wide spread (high byte of the median changes often) favours the
 // sorted-column low byte of k_colhist16s_u16; a compact one the two-phase
 // k_colhist16_u16.  Both are exact.
-__global__ void k_highbyte_spread(const uint16_t *src, int64_t pitch, int rows, int W, int *out) {
+__global__ void k_highbyte_spread(const uint16_t *src, int64_t pitch, int rows, int W, int64_t img_stride,
+                                  int B, int *out) {
     __shared__ int seen[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) seen[i] = 0;
     __syncthreads();
@@ -34,13 +35,15 @@ __global__ void k_highbyte_spread(const uint16_t *src, int64_t pitch, int rows, 
     for (int i = threadIdx.x; i < total; i += blockDim.x) {
         const int y = (int)(((int64_t)i * 7919) % rows);
         const int x = (int)(((int64_t)i * 104729) % W);
-        atomicAdd(&seen[src[(int64_t)y * pitch + x] >> 8], 1);
+        const int b = B > 1 ? i % B : 0;
+        seen[src[b * img_stride + (int64_t)y * pitch + x] >> 8] = 1;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // distinct high bytes
         int d = 0;
-        for (int b = 0; b < 256; ++b) d += seen[b] > 0 ? 1 : 0;  // distinct high bytes
-        *out = d;
+        for (int b = threadIdx.x; b < 256; b += 32) d += seen[b];
+        for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        if (threadIdx.x == 0) *out = d;
     }
 }
 
@@ -99,7 +102,7 @@ static int validate(const SlabParams &p, int B) {
 
 int rows_per_cta(const SlabParams &p, int blocks_x, int B, int ctas_per_sm) {
     const int rows = p.row_end - p.row_begin;
-    const int64_t target = (int64_t)sm_count() * ctas_per_sm * env_int("MTB_RPC_WAVES", 2);
+    const int64_t target = (int64_t)sm_count() * ctas_per_sm * 2;  // two waves
     int64_t slabs = (target + (int64_t)blocks_x * B - 1) / ((int64_t)blocks_x * B);
     if (slabs < 1) slabs = 1;
     int rpc = (int)((rows + slabs - 1) / slabs);
@@ -155,13 +158,6 @@ static int run_sortnet_n(SlabParams p, int B, cudaStream_t s, const char *name) 
     return MTB_OK;
 }
 
-// selection networks: median rank only, n = 3, 5, 7
-template <typename P>
-static bool sortnet_applies(const SlabParams &p) {
-    const int n = 2 * p.radius + 1;
-    return n <= 7 && (uint32_t)((n * n + 1) / 2) == p.rank;
-}
-
 // 3x3 median of 8-bit frames (k_med3_u8): row bands sized so the grid is
 // one wave of resident CTAs
 // TMA-staged variant: 16-byte aligned rows, W % 16 == 0; bands sized for
@@ -169,7 +165,7 @@ static bool sortnet_applies(const SlabParams &p) {
 static int run_med3t(SlabParams p, int B, cudaStream_t s) {
     const int rows = p.row_end - p.row_begin;
     const int bx = (p.W + 1023) / 1024;
-    const int per_sm = env_int("MTB_MED3T_CTAS", 8);
+    const int per_sm = 8;
     const int64_t slots = (int64_t)sm_count() * per_sm;
     int64_t bands = slots / ((int64_t)bx * B);
     if (bands < 1) bands = 1;
@@ -220,7 +216,7 @@ static int run_mednet(SlabParams p, int B, cudaStream_t s, const char *name) {
     if (per_sm < 1) per_sm = 1;
     const int rows = p.row_end - p.row_begin;
     const int bx = (p.W + MN_TX - 1) / MN_TX;
-    const int64_t slots = (int64_t)sm_count() * per_sm * env_int("MTB_MN_WAVES", 2);
+    const int64_t slots = (int64_t)sm_count() * per_sm * 2;
     int64_t bands = slots / ((int64_t)bx * B);
     if (bands < 1) bands = 1;
     int rt = (int)((rows + bands - 1) / bands);
@@ -232,29 +228,26 @@ static int run_mednet(SlabParams p, int B, cudaStream_t s, const char *name) {
     return launch(kern, grid, MN_T, smem, s, p, name);
 }
 
+// small medians: r = 1 (8-bit) -> 3x3 kernels; r = 2, 3 -> sorted packed
+// columns with shared merges; r = 1 (16-bit) -> selection network
 template <typename P>
 static int run_sortnet(SlabParams p, int B, cudaStream_t s) {
-    if ((p.radius == 2 || p.radius == 3) && env_int("MTB_MEDNET", 1) != 0 &&
-        strcmp(forced_kernel(), "sortnet") != 0) {
-        if (p.radius == 2) return run_mednet<5, P>(p, B, s, sizeof(P) == 1 ? "k_mednet<5,u8>" : "k_mednet<5,u16>");
-        return run_mednet<7, P>(p, B, s, sizeof(P) == 1 ? "k_mednet<7,u8>" : "k_mednet<7,u16>");
-    }
-    if (sizeof(P) == 1 && p.radius == 1 && strcmp(forced_kernel(), "sortnet") != 0 &&
-        (int64_t)p.src_rows * p.src_pitch < (1ll << 31))
+    const std::string force = forced_kernel();
+    if (p.radius == 2) return run_mednet<5, P>(p, B, s, sizeof(P) == 1 ? "k_mednet<5,u8>" : "k_mednet<5,u16>");
+    if (p.radius == 3) return run_mednet<7, P>(p, B, s, sizeof(P) == 1 ? "k_mednet<7,u8>" : "k_mednet<7,u16>");
+    if (sizeof(P) == 1 && force != "sortnet" && (int64_t)p.src_rows * p.src_pitch < (1ll << 31))
         return run_med3(p, B, s);
-    switch (p.radius) {
-        case 1: return run_sortnet_n<3, 4, 8, P>(p, B, s, "k_sortnet<3>");
-        case 2:
-            if (env_int("MTB_SN5_K", 2) == 3) return run_sortnet_n<5, 3, 8, P>(p, B, s, "k_sortnet<5,K3>");
-            return run_sortnet_n<5, 2, 8, P>(p, B, s, "k_sortnet<5>");
-        default:
-            if (env_int("MTB_SN7_K", 2) == 2) return run_sortnet_n<7, 2, 8, P>(p, B, s, "k_sortnet<7,K2>");
-            return run_sortnet_n<7, 1, 8, P>(p, B, s, "k_sortnet<7>");
-    }
+    return run_sortnet_n<3, 4, 8, P>(p, B, s, "k_sortnet<3>");
 }
 
-// true when the 16-bit image's high bytes are widely spread (see k_highbyte_spread)
-// host-side decision supplied by the streaming host path (-1: none)
+// 16-bit kernel choice by the spread of the value distribution (distinct
+// high bytes among 2^14 sampled pixels, k_highbyte_spread): a wide spread
+// favours the sorted-column low byte of k_colhist16s_u16 (r <= 16), a
+// compact one the window-keyed two-phase k_colhist16_u16.  Both are exact;
+// the choice only changes speed.  Host paths that hold the frame on the
+// host sample it there (g_spread_hint); device-resident calls sample on the
+// device and let the kernels read the result (SlabParams::spread / gate):
+// no host synchronisation, stream-ordered scratch, graph-capturable.
 static thread_local int g_spread_hint = -1;
 
 static int spread_distinct_host(const uint16_t *src, int64_t pitch, int rows, int W) {
@@ -269,23 +262,37 @@ static int spread_distinct_host(const uint16_t *src, int64_t pitch, int rows, in
     return d;
 }
 
-static bool wide_spread_u16(const SlabParams &p, cudaStream_t s) {
-    if (g_spread_hint >= 0) return g_spread_hint > env_int("MTB_U16_SPREAD", 24);
-    static int *d_out = nullptr;
-    static int h_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!d_out || h_dev != dev) {
-        if (cudaMalloc(&d_out, sizeof(int)) != cudaSuccess) return true;
-        h_dev = dev;
+static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
+    const std::string force = forced_kernel();
+    if (force == "colhist") return run_colhist16_u16(p, B, s, 1);
+    if (force == "colhist16s") return run_colhist16s_u16(p, B, s);
+    const bool small_r = p.radius <= 16;
+    if (g_spread_hint >= 0) {
+        const bool wide = g_spread_hint > SPREAD_WIDE;
+        if (wide && small_r) return run_colhist16s_u16(p, B, s);
+        return run_colhist16_u16(p, B, s, wide ? 0 : 1);
     }
-    const int rows = p.src_rows;
-    k_highbyte_spread<<<1, 256, 0, s>>>(static_cast<const uint16_t *>(p.src), p.src_pitch, rows, p.W, d_out);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    int h = 256;
-    cudaMemcpyAsync(&h, d_out, sizeof(int), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    return h > env_int("MTB_U16_SPREAD", 24);
+    int *d_spread = nullptr;
+    keep_pool_memory();
+    if (cudaMallocAsync(reinterpret_cast<void **>(&d_spread), sizeof(int), s) != cudaSuccess)
+        return fail(MTB_E_CUDA, "k_highbyte_spread: scratch allocation failed");
+    k_highbyte_spread<<<1, 256, 0, s>>>(static_cast<const uint16_t *>(p.src), p.src_pitch, p.src_rows, p.W,
+                                        p.src_img_stride, B, d_spread);
+    cudaError_t e = cudaGetLastError();
+    int rc = e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string("k_highbyte_spread: ") + cudaGetErrorString(e));
+    if (!rc) g_launches.fetch_add(1, std::memory_order_relaxed);
+    p.spread = d_spread;
+    if (!rc && small_r) {
+        p.gate = GATE_WIDE;  // sorted-column kernel runs on widely spread data only
+        rc = run_colhist16s_u16(p, B, s);
+        p.gate = GATE_COMPACT;  // two-phase kernel (window-keyed sweep) otherwise
+        if (!rc) rc = run_colhist16_u16(p, B, s, 1);
+        if (!rc) g_kernel = "k_colhist16s_u16|k_colhist16_u16 (device-selected)";
+    } else if (!rc) {
+        rc = run_colhist16_u16(p, B, s, WK_FROM_SPREAD);  // window-keyed sweep on compact data
+    }
+    cudaFreeAsync(d_spread, s);
+    return rc;
 }
 
 template <typename P>
@@ -302,37 +309,16 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     //   median, r = 1 (16-bit)                    -> selection network (k_sortnet<3>)
     //   8-bit, r <= 32 (any rank)                 -> column-histogram gather
     //   8-bit, 33 <= r <= 127                     -> CTMF tiles (O(1) in r)
-    //   otherwise                                 -> per-column vertical histograms
-    if ((force.empty() || force == "sortnet" || force == "med3" || force == "mednet") && sortnet_applies<P>(p) &&
-        (sizeof(P) == 2 || p.radius <= env_int("MTB_NET_MAX_R_U8", 3) || force == "sortnet" || force == "mednet"))
+    //   16-bit, n <= 255                          -> column histograms (two kernels, by value spread)
+    //   otherwise (n > 255)                       -> per-column vertical histograms
+    // MTB_KERNEL forces a family (tests).
+    const bool median = (uint32_t)((n * n + 1) / 2) == p.rank;
+    if (median && n <= 7 && (force.empty() || force == "sortnet" || force == "med3" || force == "mednet"))
         return run_sortnet<P>(p, B, s);
-    if (sizeof(P) == 1 && p.radius <= 63 && force == "lob") return run_lob_u8_32(p, B, s);
-    if (sizeof(P) == 1 && n <= 255 &&
-        (force == "colhist" || (force.empty() && p.radius <= env_int("MTB_CH_MAX_R", 32))))
+    if (sizeof(P) == 1 && n <= 255 && (force == "colhist" || (force.empty() && p.radius <= 32)))
         return run_colhist_u8(p, B, s);
     if (sizeof(P) == 1 && !wide && (force == "ctmf" || force.empty())) return run_ctmf_u8(p, B, s);
-    // 16-bit: compact high bytes (sampled spread <= MTB_U16_SPREAD) -> the
-    // two-phase column-histogram kernel; widely spread -> high-byte records +
-    // sorted columns for r <= MTB_U16_S_MAX_R, the two-phase kernel above it
-    bool spread = false;
-    if (sizeof(P) == 2 && force.empty()) {
-        spread = wide_spread_u16(p, s);
-        if (n <= 255 && spread && p.radius <= env_int("MTB_U16_S_MAX_R", 16)) return run_colhist16s_u16(p, B, s);
-        if (n <= 255) return run_colhist16_u16(p, B, s, !spread);
-    }
-    if (sizeof(P) == 2 && n <= 255 && force == "colhist") return run_colhist16_u16(p, B, s);
-    if (sizeof(P) == 2 && n <= 255 && force == "colhist16s") return run_colhist16s_u16(p, B, s);
-    if (sizeof(P) == 1 && !wide && force != "vert" && (n * n <= 255 || force == "vert2")) {
-        constexpr int T = 128;
-        const int bx = (p.W + T - 1) / T;
-        const bool small = n * n <= 255;
-        const int spw = (32 + 2 * p.radius + 16 + 15) & ~15;
-        const size_t smem = (size_t)16 * T * 2 + (size_t)256 * T * (small ? 1 : 2) + (size_t)(T / 32) * 2 * spw;
-        p.rows_per_cta = rows_per_cta(p, bx, B, small ? 6 : 3);
-        dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
-        return small ? launch(k_vert2_u8<uint8_t, T>, grid, T, smem, s, p, "k_vert2_u8<u8>")
-                     : launch(k_vert2_u8<uint16_t, T>, grid, T, smem, s, p, "k_vert2_u8<u16>");
-    }
+    if (sizeof(P) == 2 && n <= 255 && force != "vert") return run_u16_colhist(p, B, s);
     if (sizeof(P) == 1) {
         constexpr int T = 128;
         const int bx = (p.W + T - 1) / T;
@@ -341,29 +327,14 @@ static int run(SlabParams p, int B, cudaStream_t s) {
         dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
         return wide ? launch(k_vert_u8<uint32_t, T>, grid, T, smem, s, p, "k_vert_u8<u32>")
                     : launch(k_vert_u8<uint16_t, T>, grid, T, smem, s, p, "k_vert_u8<u16>");
-    } else if (!wide && (force == "vert2" || (force.empty() && spread))) {
-        constexpr int T = 64;
-        const int n16 = (int)n;
-        const size_t smem = (size_t)(16 + 256 + 16) * T * 2 + (size_t)(T + 2 * p.radius) * n16 * 2 +
-                            (size_t)n16 * T;
-        if (smem <= 200 * 1024) {
-            const int bx = (p.W + T - 1) / T;
-            const int occ = (int)((227 * 1024) / (smem + 1024));
-            p.rows_per_cta = rows_per_cta(p, bx, B, occ < 1 ? 1 : occ);
-            if (p.rows_per_cta < 2 * n16) p.rows_per_cta = 2 * n16 < p.row_end - p.row_begin ? 2 * n16 : p.row_end - p.row_begin;
-            dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
-            return launch(k_vert2_u16<uint16_t, T>, grid, T, smem, s, p, "k_vert2_u16<u16>");
-        }
     }
-    {
-        constexpr int T = 64;
-        const int bx = (p.W + T - 1) / T;
-        const size_t smem = (size_t)2 * (16 + 256) * T * (wide ? 4 : 2);
-        p.rows_per_cta = rows_per_cta(p, bx, B, wide ? 1 : 3);
-        dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
-        return wide ? launch(k_vert_u16<uint32_t, T>, grid, T, smem, s, p, "k_vert_u16<u32>")
-                    : launch(k_vert_u16<uint16_t, T>, grid, T, smem, s, p, "k_vert_u16<u16>");
-    }
+    constexpr int T = 64;
+    const int bx = (p.W + T - 1) / T;
+    const size_t smem = (size_t)2 * (16 + 256) * T * (wide ? 4 : 2);
+    p.rows_per_cta = rows_per_cta(p, bx, B, wide ? 1 : 3);
+    dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
+    return wide ? launch(k_vert_u16<uint32_t, T>, grid, T, smem, s, p, "k_vert_u16<u32>")
+                : launch(k_vert_u16<uint16_t, T>, grid, T, smem, s, p, "k_vert_u16<u16>");
 }
 
 static SlabParams make_params(const void *src, int64_t src_pitch, int32_t src_row0,
@@ -404,19 +375,23 @@ struct HostCtx {
     int dev = -1;
     void *dsrc = nullptr, *ddst = nullptr, *dlut = nullptr;
     unsigned int *dflags = nullptr;  // [0] rows arrived, [1..] output pixels per chunk
+    unsigned int *hstatus = nullptr, *dstatus = nullptr;  // mapped pinned word: a CTA timed out waiting for rows
     size_t cap = 0;
     cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
     static constexpr int KMAX = 16;
     cudaEvent_t eh[KMAX], ec[KMAX];
 };
 
-static std::mutex g_host_mu;
+// one context (and one lock) per device: host threads driving different
+// GPUs never serialise on each other
+static std::mutex g_host_mu[64];
 static HostCtx g_host[64];
 
-static int host_ctx(HostCtx *&ctx, size_t bytes) {
+static int host_ctx(HostCtx *&ctx, std::unique_lock<std::mutex> &lock, size_t bytes) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) return fail(MTB_E_CUDA, "device index out of range");
+    lock = std::unique_lock<std::mutex>(g_host_mu[dev]);
     ctx = &g_host[dev];
     auto ok = [](cudaError_t e, const char *what) {
         if (e != cudaSuccess) {
@@ -430,7 +405,9 @@ static int host_ctx(HostCtx *&ctx, size_t bytes) {
             !ok(cudaStreamCreateWithFlags(&ctx->sc, cudaStreamNonBlocking), "cudaStreamCreate") ||
             !ok(cudaStreamCreateWithFlags(&ctx->sd, cudaStreamNonBlocking), "cudaStreamCreate") ||
             !ok(cudaMalloc(&ctx->dlut, 65536 * 2), "cudaMalloc") ||
-            !ok(cudaMalloc(&ctx->dflags, 64 * sizeof(unsigned int)), "cudaMalloc"))
+            !ok(cudaMalloc(&ctx->dflags, 64 * sizeof(unsigned int)), "cudaMalloc") ||
+            !ok(cudaHostAlloc(&ctx->hstatus, sizeof(unsigned int), cudaHostAllocMapped), "cudaHostAlloc") ||
+            !ok(cudaHostGetDevicePointer(&ctx->dstatus, ctx->hstatus, 0), "cudaHostGetDevicePointer"))
             return MTB_E_CUDA;
         for (int i = 0; i < HostCtx::KMAX; ++i)
             if (!ok(cudaEventCreateWithFlags(&ctx->eh[i], cudaEventDisableTiming), "cudaEventCreate") ||
@@ -486,49 +463,60 @@ static bool stream_mem_ops(write32_fn &write32, write32_fn &wait32) {
     return resolved > 0;
 }
 
-static int host_stream(HostCtx *ctx, const void *src, void *dst, int bit_depth, int H, int W, int radius,
-                       int64_t rank, const void *lut, uint32_t flags) {
+// page-locked (or registered) host memory: cudaMemcpyAsync returns at once
+static bool host_pinned(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Output rows [A, B) of an H-row host frame: the device copy holds source
+// rows [top, bot) = [max(0, A-r), min(H, B+r)) -- the rows the windows
+// touch, clamped against the GLOBAL frame (engine.py:252-256) -- and the
+// host destination `dst` holds rows [A, B).
+struct HostRows {
+    const char *src;  // host, global row 0
+    char *dst;        // host, global row A
+    int bit_depth, H, W, A, B, top, bot, radius;
+    int64_t rank;
+    const void *lut;
+    size_t es, row;
+};
+
+static int host_stream(HostCtx *ctx, const HostRows &j) {
     write32_fn write32 = nullptr, wait32 = nullptr;
     if (!stream_mem_ops(write32, wait32)) return 1;  // caller falls back to the banded path
-    const size_t es = bit_depth == 8 ? 1 : 2;
-    const size_t row = (size_t)W * es, total = (size_t)H * row;
-    const int K = std::max(1, std::min(env_int("MTB_HOST_IN_CHUNKS", 4), H / 128));    // input chunks
-    const int KO = std::max(1, std::min(env_int("MTB_HOST_OUT_CHUNKS", 8), std::min(63, H / 128)));  // output
-    const int C = (H + KO - 1) / KO;                                  // rows per output chunk
-    const int nout = (H + C - 1) / C;
+    const int rows = j.B - j.A;
+    const size_t row = j.row, total = (size_t)(j.bot - j.top) * row;
+    const int K = std::max(1, std::min(4, (j.bot - j.top) / 128));   // input chunks
+    const int KO = std::max(1, std::min(8, std::min(63, rows / 128)));  // output chunks
+    const int C = (rows + KO - 1) / KO;                                 // rows per output chunk
+    const int nout = (rows + C - 1) / C;
     auto ok = [](cudaError_t e, const char *what) {
         return e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
     };
+    *ctx->hstatus = 0;
     int rc = ok(cudaMemsetAsync(ctx->dflags, 0, (1 + nout) * sizeof(unsigned int), ctx->sh), "memset");
-    if (!rc && lut)
-        rc = ok(cudaMemcpyAsync(ctx->dlut, lut, ((size_t)1 << bit_depth) * es, cudaMemcpyHostToDevice, ctx->sh),
+    if (!rc && j.lut)
+        rc = ok(cudaMemcpyAsync(ctx->dlut, j.lut, ((size_t)1 << j.bit_depth) * j.es, cudaMemcpyHostToDevice, ctx->sh),
                 "H2D lut");
     if (rc) return rc;
     cudaEventRecord(ctx->eh[0], ctx->sh);
     cudaStreamWaitEvent(ctx->sc, ctx->eh[0], 0);
     cudaStreamWaitEvent(ctx->sd, ctx->eh[0], 0);
-    SlabParams p = make_params(ctx->dsrc, W, 0, H, ctx->ddst, W, H, W, 0, H, radius, rank,
-                               lut ? ctx->dlut : nullptr);
-    p.in_rows = ctx->dflags;
-    p.out_px = ctx->dflags + 1;
-    p.out_chunk = C;
-    if (bit_depth == 16)
-        g_spread_hint = spread_distinct_host(static_cast<const uint16_t *>(src), W, H, W);
-    (void)flags;
-    rc = bit_depth == 8 ? run<uint8_t>(p, 1, ctx->sc) : run<uint16_t>(p, 1, ctx->sc);
-    g_spread_hint = -1;
-    if (rc) {
-        // nothing waits on the flags yet: release any spinning CTAs, then fail
-        write32(ctx->sh, (unsigned long long)ctx->dflags, (unsigned int)H, 0);
-        cudaStreamSynchronize(ctx->sc);
-        cudaStreamSynchronize(ctx->sh);
-        return rc;
-    }
-    const char *s8 = static_cast<const char *>(src);
+    // Every chunk copy and its "rows arrived" write (a global row count) is
+    // enqueued BEFORE the launch (the source is page-locked, so this
+    // returns at once): the kernel's CTAs only ever wait for copy-engine
+    // work already in flight, whatever the launch serialisation
+    // (CUDA_LAUNCH_BLOCKING, profilers, sanitizers).
+    const char *s8 = j.src + (size_t)j.top * row;
     size_t b = 0;
     for (int i = 0; i < K && !rc; ++i) {
-        const int R = (int)((int64_t)H * (i + 1) / K);
-        const size_t e = i == K - 1 ? total : std::min(total, ((size_t)R * row + 127) & ~(size_t)127);
+        const int R = j.top + (int)((int64_t)(j.bot - j.top) * (i + 1) / K);
+        const size_t e = i == K - 1 ? total : std::min(total, ((size_t)(R - j.top) * row + 127) & ~(size_t)127);
         if (e > b) {
             rc = ok(cudaMemcpyAsync(static_cast<char *>(ctx->dsrc) + b, s8 + b, e - b, cudaMemcpyHostToDevice, ctx->sh),
                     "H2D");
@@ -537,62 +525,99 @@ static int host_stream(HostCtx *ctx, const void *src, void *dst, int bit_depth, 
         if (!rc && write32(ctx->sh, (unsigned long long)ctx->dflags, (unsigned int)R, 0) != 0)
             rc = fail(MTB_E_CUDA, "cuStreamWriteValue32 failed");
     }
-    char *d8 = static_cast<char *>(dst);
+    if (!rc) {
+        SlabParams p = make_params(ctx->dsrc, j.W, j.top, j.bot - j.top, ctx->ddst, j.W, j.H, j.W, j.A, j.B,
+                                   j.radius, j.rank, j.lut ? ctx->dlut : nullptr);
+        p.in_rows = ctx->dflags;
+        p.out_px = ctx->dflags + 1;
+        p.out_chunk = C;
+        p.status = ctx->dstatus;
+        rc = j.bit_depth == 8 ? run<uint8_t>(p, 1, ctx->sc) : run<uint16_t>(p, 1, ctx->sc);
+    }
     for (int c = 0; c < nout && !rc; ++c) {
-        const int a = c * C, e = std::min(H, a + C);
-        if (wait32(ctx->sd, (unsigned long long)(ctx->dflags + 1 + c), (unsigned int)((e - a) * W), 0) != 0)
+        const int a = c * C, e = std::min(rows, a + C);
+        if (wait32(ctx->sd, (unsigned long long)(ctx->dflags + 1 + c), (unsigned int)((e - a) * j.W), 0) != 0)
             rc = fail(MTB_E_CUDA, "cuStreamWaitValue32 failed");
         else
-            rc = ok(cudaMemcpyAsync(d8 + (size_t)a * row, static_cast<char *>(ctx->ddst) + (size_t)a * row,
+            rc = ok(cudaMemcpyAsync(j.dst + (size_t)a * row, static_cast<char *>(ctx->ddst) + (size_t)a * row,
                                     (size_t)(e - a) * row, cudaMemcpyDeviceToHost, ctx->sd), "D2H");
     }
-    if (rc) write32(ctx->sh, (unsigned long long)ctx->dflags, (unsigned int)H, 0);  // never leave CTAs spinning
+    if (rc) {
+        // copy-out waits already enqueued can never be met now: release them
+        for (int c = 0; c < nout; ++c)
+            write32(ctx->sh, (unsigned long long)(ctx->dflags + 1 + c), 0xFFFFFFFFu, 0);
+    }
     const int r1 = ok(cudaStreamSynchronize(ctx->sd), "cudaStreamSynchronize");
     const int r2 = ok(cudaStreamSynchronize(ctx->sc), "cudaStreamSynchronize");
     const int r3 = ok(cudaStreamSynchronize(ctx->sh), "cudaStreamSynchronize");
+    if (!rc && *(volatile unsigned int *)ctx->hstatus)
+        rc = fail(MTB_E_CUDA, "streaming launch timed out waiting for source rows");
     return rc ? rc : (r1 ? r1 : (r2 ? r2 : r3));
 }
 
-static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W, int radius, int64_t rank,
-                         const void *lut, uint32_t flags) {
-    std::lock_guard<std::mutex> lock(g_host_mu);
-    const size_t es = bit_depth == 8 ? 1 : 2;
-    const size_t row = (size_t)W * es;
+static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W, int A, int B, int radius,
+                         int64_t rank, const void *lut) {
+    HostRows j;
+    j.src = static_cast<const char *>(src);
+    j.dst = static_cast<char *>(dst);
+    j.bit_depth = bit_depth;
+    j.H = H;
+    j.W = W;
+    j.A = A;
+    j.B = B;
+    j.top = std::max(0, A - radius);
+    j.bot = std::min(H, B + radius);
+    j.radius = radius;
+    j.rank = rank;
+    j.lut = lut;
+    j.es = bit_depth == 8 ? 1 : 2;
+    j.row = (size_t)W * j.es;
+    const size_t row = j.row;
     HostCtx *ctx = nullptr;
-    if (int rc = host_ctx(ctx, (size_t)H * row)) return rc;
+    std::unique_lock<std::mutex> lock;
+    if (int rc = host_ctx(ctx, lock, (size_t)(j.bot - j.top) * row)) return rc;
+    // 16-bit kernel choice from the host copy of the rows this call reads
+    struct HintGuard {
+        ~HintGuard() { g_spread_hint = -1; }
+    } hint_guard;
+    if (bit_depth == 16)
+        g_spread_hint = spread_distinct_host(reinterpret_cast<const uint16_t *>(j.src + (size_t)j.top * row), W,
+                                             j.bot - j.top, W);
     // streaming (one launch, copies overlapped) for compute-heavy radii;
     // row bands below, where the stream-op latencies outweigh the overlap
     // (tools/e2e_probe.py: equal at r = 15, streaming -12% at r = 31, +10%
-    // at r <= 3).  MTB_HOST_STREAM=0/1 forces; lob has no streaming support.
+    // at r <= 3).  Streaming needs a page-locked source (its copies must be
+    // enqueued ahead of the launch without blocking); pageable frames take
+    // the bands, whose launches never wait on copies.  MTB_HOST_STREAM=0/1
+    // forces.
     const int stream_mode = env_int("MTB_HOST_STREAM", -1);
-    const bool want_stream = stream_mode < 0 ? radius >= 12 : stream_mode != 0;
-    if (want_stream && std::string(forced_kernel()) != "lob") {
-        const int rs = host_stream(ctx, src, dst, bit_depth, H, W, radius, rank, lut, flags);
+    const bool want_stream = (stream_mode < 0 ? radius >= 12 : stream_mode != 0) && host_pinned(src);
+    if (want_stream) {
+        const int rs = host_stream(ctx, j);
         if (rs != 1) return rs;
     }
     // bands: enough rows that per-band launch and halo overheads stay small
     // (measured on config 2, tools/e2e_probe.py: 4 bands of 1024 rows for
     // r <= 31, 2 for r = 63 -- shorter bands re-pay the n-row column build)
+    const int rows = B - A;
     const int min_rows = std::max(1024, 32 * radius);
-    int K = env_int("MTB_HOST_BANDS", std::min(8, std::max(1, H / min_rows)));
-    K = std::max(1, std::min(K, std::min(HostCtx::KMAX, H)));
+    int K = env_int("MTB_HOST_BANDS", std::min(8, std::max(1, rows / min_rows)));
+    K = std::max(1, std::min(K, std::min(HostCtx::KMAX, rows)));
     auto cuda_ok = [](cudaError_t e, const char *what) {
         return e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
     };
     if (lut) {
-        if (int rc = cuda_ok(cudaMemcpyAsync(ctx->dlut, lut, ((size_t)1 << bit_depth) * es, cudaMemcpyHostToDevice,
+        if (int rc = cuda_ok(cudaMemcpyAsync(ctx->dlut, lut, ((size_t)1 << bit_depth) * j.es, cudaMemcpyHostToDevice,
                                              ctx->sh), "H2D lut"))
             return rc;
     }
-    const char *s8 = static_cast<const char *>(src);
-    char *d8 = static_cast<char *>(dst);
-    char *ds = static_cast<char *>(ctx->dsrc);
-    char *dd = static_cast<char *>(ctx->ddst);
-    int copied = 0;  // source rows [0, copied) enqueued host->device
+    char *ds = static_cast<char *>(ctx->dsrc);  // global row top
+    char *dd = static_cast<char *>(ctx->ddst);  // global row A
+    int copied = j.top;  // source rows [top, copied) enqueued host->device
     int rc = MTB_OK;
-    auto band = [&](int i, int &a, int &b) {
-        a = (int)((int64_t)H * i / K);
-        b = (int)((int64_t)H * (i + 1) / K);
+    auto band = [&](int i, int &a, int &b) {  // global output rows of band i
+        a = A + (int)((int64_t)rows * i / K);
+        b = A + (int)((int64_t)rows * (i + 1) / K);
     };
     // result rows of band i back to the host (enqueued one band late: with
     // pageable host memory the call blocks until the copy is done, and by
@@ -601,8 +626,8 @@ static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W
         int a, b;
         band(i, a, b);
         cudaStreamWaitEvent(ctx->sd, ctx->ec[i], 0);
-        return cuda_ok(cudaMemcpyAsync(d8 + (size_t)a * row, dd + (size_t)a * row, (size_t)(b - a) * row,
-                                       cudaMemcpyDeviceToHost, ctx->sd), "D2H");
+        return cuda_ok(cudaMemcpyAsync(j.dst + (size_t)(a - A) * row, dd + (size_t)(a - A) * row,
+                                       (size_t)(b - a) * row, cudaMemcpyDeviceToHost, ctx->sd), "D2H");
     };
     int done = 0;
     for (int i = 0; i < K && rc == MTB_OK; ++i) {
@@ -610,18 +635,16 @@ static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W
         band(i, a, b);
         const int need = std::min(H, b + radius);
         if (need > copied) {
-            rc = cuda_ok(cudaMemcpyAsync(ds + copied * row, s8 + copied * row, (size_t)(need - copied) * row,
-                                         cudaMemcpyHostToDevice, ctx->sh), "H2D");
+            rc = cuda_ok(cudaMemcpyAsync(ds + (size_t)(copied - j.top) * row, j.src + (size_t)copied * row,
+                                         (size_t)(need - copied) * row, cudaMemcpyHostToDevice, ctx->sh), "H2D");
             copied = need;
         }
         if (rc) break;
         cudaEventRecord(ctx->eh[i], ctx->sh);
         cudaStreamWaitEvent(ctx->sc, ctx->eh[i], 0);
-        rc = bit_depth == 8
-                 ? mtb_median_u8((const uint8_t *)ds, W, 0, H, (uint8_t *)(dd + (size_t)a * row), W, H, W, a, b,
-                                 radius, rank, lut ? (const uint8_t *)ctx->dlut : nullptr, flags, ctx->sc)
-                 : mtb_median_u16((const uint16_t *)ds, W, 0, H, (uint16_t *)(dd + (size_t)a * row), W, H, W, a,
-                                  b, radius, rank, lut ? (const uint16_t *)ctx->dlut : nullptr, flags, ctx->sc);
+        SlabParams p = make_params(ds, W, j.top, j.bot - j.top, dd + (size_t)(a - A) * row, W, H, W, a, b, radius,
+                                   rank, lut ? ctx->dlut : nullptr);
+        rc = bit_depth == 8 ? run<uint8_t>(p, 1, ctx->sc) : run<uint16_t>(p, 1, ctx->sc);
         if (rc) break;
         cudaEventRecord(ctx->ec[i], ctx->sc);
         if (i >= 1) rc = d2h(i - 1);
@@ -647,16 +670,19 @@ struct FramesCtx {
     int dev = -1;
     void *dsrc[NB] = {}, *ddst[NB] = {}, *dlut = nullptr;
     unsigned int *dflags = nullptr;  // [NB][NFLAGS]
+    unsigned int *hstatus = nullptr, *dstatus = nullptr;  // mapped pinned word: a CTA timed out waiting for rows
     size_t cap = 0;
     cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
     cudaEvent_t ein[NB], ek[NB], eout[NB];
 };
 static FramesCtx g_frames[64];
+static std::mutex g_frames_mu[64];
 
-static int frames_ctx(FramesCtx *&ctx, size_t bytes) {
+static int frames_ctx(FramesCtx *&ctx, std::unique_lock<std::mutex> &lock, size_t bytes) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) return fail(MTB_E_CUDA, "device index out of range");
+    lock = std::unique_lock<std::mutex>(g_frames_mu[dev]);
     ctx = &g_frames[dev];
     auto ok = [](cudaError_t e, const char *what) {
         return e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -667,6 +693,8 @@ static int frames_ctx(FramesCtx *&ctx, size_t bytes) {
         if (!rc) rc = ok(cudaStreamCreateWithFlags(&ctx->sd, cudaStreamNonBlocking), "cudaStreamCreate");
         if (!rc) rc = ok(cudaMalloc(&ctx->dlut, 65536 * 2), "cudaMalloc");
         if (!rc) rc = ok(cudaMalloc(&ctx->dflags, FramesCtx::NB * FramesCtx::NFLAGS * sizeof(unsigned int)), "cudaMalloc");
+        if (!rc) rc = ok(cudaHostAlloc(&ctx->hstatus, sizeof(unsigned int), cudaHostAllocMapped), "cudaHostAlloc");
+        if (!rc) rc = ok(cudaHostGetDevicePointer(&ctx->dstatus, ctx->hstatus, 0), "cudaHostGetDevicePointer");
         for (int j = 0; j < FramesCtx::NB && !rc; ++j) {
             rc = ok(cudaEventCreateWithFlags(&ctx->ein[j], cudaEventDisableTiming), "cudaEventCreate");
             if (!rc) rc = ok(cudaEventCreateWithFlags(&ctx->ek[j], cudaEventDisableTiming), "cudaEventCreate");
@@ -694,15 +722,17 @@ static int frames_ctx(FramesCtx *&ctx, size_t bytes) {
 
 static int host_frames(const void *const *srcs, void *const *dsts, const int32_t *radii, const int64_t *ranks,
                        int n, int bit_depth, int H, int W, const void *lut, uint32_t flags) {
-    std::lock_guard<std::mutex> lock(g_host_mu);
     const size_t es = bit_depth == 8 ? 1 : 2;
     const size_t bytes = (size_t)H * W * es;
     FramesCtx *ctx = nullptr;
-    if (int rc = frames_ctx(ctx, bytes)) return rc;
+    std::unique_lock<std::mutex> lock;
+    if (int rc = frames_ctx(ctx, lock, bytes)) return rc;
     auto ok = [](cudaError_t e, const char *what) {
         return e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
     };
+    (void)flags;
     int rc = MTB_OK;
+    *ctx->hstatus = 0;
     if (lut) {
         rc = ok(cudaMemcpyAsync(ctx->dlut, lut, ((size_t)1 << bit_depth) * es, cudaMemcpyHostToDevice, ctx->sc),
                 "H2D lut");
@@ -719,11 +749,10 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
     // 3: last only (31.7); 0: none.
     write32_fn write32 = nullptr, wait32 = nullptr;
     const int smode = env_int("MTB_FRAMES_STREAM", 4);
-    const bool can_stream = smode != 0 && std::string(forced_kernel()) != "lob" &&
-                            stream_mem_ops(write32, wait32) && H >= 256;  // (lob has no streaming hooks)
+    const bool can_stream = smode != 0 && stream_mem_ops(write32, wait32) && H >= 256;
     const size_t row = (size_t)W * es;
-    const int KI = std::max(1, std::min(env_int("MTB_FRAMES_IN_CHUNKS", 4), H / 128));
-    const int KO = std::max(1, std::min(env_int("MTB_FRAMES_OUT_CHUNKS", 4), std::min(FramesCtx::NFLAGS - 1, H / 128)));
+    const int KI = std::max(1, std::min(4, H / 128));
+    const int KO = std::max(1, std::min(4, std::min(FramesCtx::NFLAGS - 1, H / 128)));
     const int C = (H + KO - 1) / KO, nout = (H + C - 1) / C;
     // Processing order: heavy and light frames alternate (by radius, the
     // filter cost's proxy at one geometry: largest, smallest, second
@@ -732,10 +761,9 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
     // copies.  Results land in dsts[i] whatever the order.  On the
     // config-2 sweep this is within 0.2% of the best of all 720 orders in a
     // copy / filter timeline model (3.16 against 3.52 ms in input order).
-    // MTB_FRAMES_ORDER=0 keeps the input order.
     std::vector<int> order(n);
     for (int i = 0; i < n; ++i) order[i] = i;
-    if (env_int("MTB_FRAMES_ORDER", 1) != 0) {
+    {
         std::vector<int> byr(order);
         std::stable_sort(byr.begin(), byr.end(), [&](int a, int b) { return radii[a] > radii[b]; });
         for (int q = 0, lo = 0, hi = n - 1; q < n; ++q) order[q] = (q & 1) ? byr[hi--] : byr[lo++];
@@ -772,7 +800,10 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
                                               (smode == 3 && q == n - 1) || (smode == 4 && q == 0));
         if (q >= NB) cudaStreamWaitEvent(ctx->sh, ctx->ek[j], 0);  // job i-NB done reading dsrc[j]
         if (streaming) {
-            // counters reset before this frame's kernel or copy-out can look at them
+            // counters reset before this frame's kernel or copy-out can look
+            // at them, and only after job i-NB's copy-out stopped waiting on
+            // them (the same slot's counters)
+            if (q >= NB) cudaStreamWaitEvent(ctx->sh, ctx->eout[j], 0);
             rc = ok(cudaMemsetAsync(fl, 0, (1 + nout) * sizeof(unsigned int), ctx->sh), "memset");
             if (rc) break;
             cudaEventRecord(ctx->ein[j], ctx->sh);
@@ -808,8 +839,8 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
             p.in_rows = fl;
             p.out_px = fl + 1;
             p.out_chunk = C;
+            p.status = ctx->dstatus;
         }
-        (void)flags;
         rc = bit_depth == 8 ? run<uint8_t>(p, 1, ctx->sc) : run<uint16_t>(p, 1, ctx->sc);
         g_spread_hint = -1;
         if (rc) {
@@ -839,6 +870,8 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
     const int r1 = ok(cudaStreamSynchronize(ctx->sd), "cudaStreamSynchronize");
     const int r2 = ok(cudaStreamSynchronize(ctx->sc), "cudaStreamSynchronize");
     const int r3 = ok(cudaStreamSynchronize(ctx->sh), "cudaStreamSynchronize");
+    if (!rc && *(volatile unsigned int *)ctx->hstatus)
+        rc = fail(MTB_E_CUDA, "streaming launch timed out waiting for source rows");
     return rc ? rc : (r1 ? r1 : (r2 ? r2 : r3));
 }
 
@@ -892,7 +925,25 @@ int mtb_filter_host(const void *src, void *dst, int32_t bit_depth, int32_t H, in
         return fail(MTB_E_INVAL, "bit_depth must be 8 or 16, got " + std::to_string(bit_depth));
     if (!src || !dst) return fail(MTB_E_INVAL, "null src/dst pointer");
     if (H < 1 || W < 1) return fail(MTB_E_INVAL, "pixels must be a non-empty 2D array");
-    return host_pipeline(src, dst, bit_depth, H, W, radius, rank, lut, flags);
+    (void)flags;
+    return host_pipeline(src, dst, bit_depth, H, W, 0, H, radius, rank, lut);
+}
+
+int mtb_filter_host_rows(const void *src, void *dst, int32_t bit_depth, int32_t H, int32_t W, int32_t row_begin,
+                         int32_t row_end, int32_t radius, int64_t rank, const void *lut, uint32_t flags,
+                         int32_t device) {
+    (void)flags;
+    if (bit_depth != 8 && bit_depth != 16)
+        return fail(MTB_E_INVAL, "bit_depth must be 8 or 16, got " + std::to_string(bit_depth));
+    if (!src || !dst) return fail(MTB_E_INVAL, "null src/dst pointer");
+    if (H < 1 || W < 1) return fail(MTB_E_INVAL, "pixels must be a non-empty 2D array");
+    if (row_begin < 0 || row_end > H || row_begin > row_end) return fail(MTB_E_INVAL, "bad output row range");
+    if (row_begin == row_end) return MTB_OK;
+    if (device >= 0) {
+        cudaError_t e = cudaSetDevice(device);
+        if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    }
+    return host_pipeline(src, dst, bit_depth, H, W, row_begin, row_end, radius, rank, lut);
 }
 
 int mtb_filter_host_frames(const void *const *srcs, void *const *dsts, const int32_t *radii, const int64_t *ranks,
@@ -932,9 +983,14 @@ int mtb_rank_bruteforce(const void *src, int64_t src_pitch, void *dst, int64_t d
     return MTB_OK;
 }
 
+int mtb_set_device(int32_t device) {
+    cudaError_t e = cudaSetDevice(device);
+    return e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+}
+
 uint64_t mtb_launch_count(void) { return g_launches.load(); }
 const char *mtb_last_kernel(void) { return g_kernel; }
 const char *mtb_last_error(void) { return g_err.c_str(); }
-int mtb_version(void) { return 1; }
+int mtb_version(void) { return 2; }
 
 }  // extern "C"

@@ -5,7 +5,7 @@
 namespace mtb {
 
 template <int T, int G, int PL>
-static int run_colhist16_u16_g(SlabParams p, int B, cudaStream_t s, bool wk) {
+static int run_colhist16_u16_g(SlabParams p, int B, cudaStream_t s, int wk) {
     switch ((2 * p.radius + 1) % G) {
         case 1: return run_colhist16_u16_gm<T, G, (G > 1 ? 1 : 0), PL>(p, B, s, wk);
         case 3: return run_colhist16_u16_gm<T, G, (G > 3 ? 3 : 0), PL>(p, B, s, wk);
@@ -15,15 +15,15 @@ static int run_colhist16_u16_g(SlabParams p, int B, cudaStream_t s, bool wk) {
     }
 }
 
-int run_colhist16_u16(SlabParams p, int B, cudaStream_t s, bool wk) {
+int run_colhist16_u16(SlabParams p, int B, cudaStream_t s, int wk) {
     const int n = 2 * p.radius + 1;
-    if (env_int("MTB_CH16_PL", -1) < 0) {  // compile-time window sides r = 3..31 (run_colhist16_f*.cu)
+    {  // compile-time window sides r = 3..31 (run_colhist16_f*.cu)
         int rc = run_colhist16_fixed_a(p, B, s, wk);
         if (rc == NOT_COVERED) rc = run_colhist16_fixed_b(p, B, s, wk);
         if (rc == NOT_COVERED) rc = run_colhist16_fixed_c(p, B, s, wk);
         if (rc != NOT_COVERED) return rc;
     }
-    const int pl = env_int("MTB_CH16_PL", ch16_pair_levels(p.radius));
+    const int pl = ch16_pair_levels(p.radius);
     if (8 * n <= 255) {
         if (pl == 3) return run_colhist16_u16_g<256, 8, 3>(p, B, s, wk);
         if (pl == 2) return run_colhist16_u16_g<256, 8, 2>(p, B, s, wk);

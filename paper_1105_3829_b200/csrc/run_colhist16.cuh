@@ -11,9 +11,9 @@
 namespace mtb {
 
 template <int T, int G, int M, int PL, int NF = 0>
-inline int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s, bool wk) {
+inline int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s, int wk) {
     // window-keyed first sweep (compact data); MTB_CH16_WK=0/1 forces
-    wk = env_int("MTB_CH16_WK", wk ? 1 : 0) != 0;
+    wk = env_int("MTB_CH16_WK", wk);
     const int ncp = PL > 0 ? colhist4p_ncolp(T, p.radius) : ch4_stride(T + 2 * p.radius);
     const size_t smem = (PL > 0 ? (size_t)colhist4p_bytes(T, p.radius, PL) : (size_t)colhist4_bytes(T, p.radius)) +
                         (size_t)ncp * 4 + (2 * 256 + 2) * sizeof(int);
@@ -51,7 +51,7 @@ constexpr int ch16_pair_levels(int r) {
 // compile-time window sides NLO..NHI (odd); NOT_COVERED when n is outside
 constexpr int NOT_COVERED = 1;  // (MTB status codes are 0 or negative)
 template <int NLO, int NHI>
-inline int run_colhist16_fixed(SlabParams p, int B, cudaStream_t s, bool wk) {
+inline int run_colhist16_fixed(SlabParams p, int B, cudaStream_t s, int wk) {
     const int n = 2 * p.radius + 1;
     if (n < NLO || n > NHI) return NOT_COVERED;
     return with_fixed_n<NLO, NHI>(n, [&](auto nf) {

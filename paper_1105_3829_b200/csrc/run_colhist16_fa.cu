@@ -4,7 +4,7 @@
 
 namespace mtb {
 
-int run_colhist16_fixed_a(SlabParams p, int B, cudaStream_t s, bool wk) {
+int run_colhist16_fixed_a(SlabParams p, int B, cudaStream_t s, int wk) {
     return run_colhist16_fixed<7, 27>(p, B, s, wk);
 }
 

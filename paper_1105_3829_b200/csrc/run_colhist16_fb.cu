@@ -4,7 +4,7 @@
 
 namespace mtb {
 
-int run_colhist16_fixed_b(SlabParams p, int B, cudaStream_t s, bool wk) {
+int run_colhist16_fixed_b(SlabParams p, int B, cudaStream_t s, int wk) {
     return run_colhist16_fixed<29, 45>(p, B, s, wk);
 }
 

@@ -4,7 +4,7 @@
 
 namespace mtb {
 
-int run_colhist16_fixed_c(SlabParams p, int B, cudaStream_t s, bool wk) {
+int run_colhist16_fixed_c(SlabParams p, int B, cudaStream_t s, int wk) {
     return run_colhist16_fixed<47, 63>(p, B, s, wk);
 }
 

@@ -12,7 +12,7 @@ static int run_colhist16s_u16_gm(SlabParams p, int B, cudaStream_t s) {
     const int n = 2 * p.radius + 1, NCOL = T + 2 * p.radius;
     const size_t smem = (size_t)colhist4_bytes(T, p.radius) + 16 * T * 2 + ((size_t)(n * T + 15) & ~(size_t)15) +
                         ((size_t)NCOL * n + 7) / 8 * 16 + (size_t)CH16S_CMAX * T;
-    if (smem > 220 * 1024) return run_colhist16_u16(p, B, s, false);  // sorted columns too large: two-phase kernel
+    if (smem > 220 * 1024) return run_colhist16_u16(p, B, s, 0);  // sorted columns too large: two-phase kernel
     auto kern = k_colhist16s_u16<T, G, M, NF>;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 1;

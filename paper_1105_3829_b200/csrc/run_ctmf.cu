@@ -1,8 +1,6 @@
-// run_ctmf.cu -- launchers of the CTMF tile kernel (kernels_ctmf.cuh) and of
-// the rejected lanes-own-bins kernel (kernels_lob.cuh).
+// run_ctmf.cu -- launcher of the CTMF tile kernel (kernels_ctmf.cuh).
 #include "host.h"
 #include "kernels_ctmf.cuh"
-#include "kernels_lob.cuh"
 
 namespace mtb {
 
@@ -96,34 +94,5 @@ int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
     return run_ctmf_u8_s<16>(p, B, s, pre);
 }
 
-template <int L>
-static int run_lob_u8_l(SlabParams p, int B, cudaStream_t s) {
-    const LobGeom g = lob_geom(L, p.radius);
-    const int rows = p.row_end - p.row_begin;
-    const int tiles_x = (p.W + g.TW - 1) / g.TW;
-    const int per_sm = (220 * 1024) / g.warp_bytes;
-    const int want = sm_count() * (per_sm < 1 ? 1 : per_sm) * 3;
-    int ty = (want + tiles_x * B - 1) / (tiles_x * B);
-    int th = (rows + ty - 1) / ty;
-    const int min_th = env_int("MTB_LOB_MIN_TH", 32);
-    if (th < min_th) th = min_th;
-    th = env_int("MTB_LOB_TH", th);
-    if (th > rows) th = rows;
-    if (th < 1) th = 1;
-    p.rows_per_cta = th;
-    const int tiles_y = (rows + th - 1) / th;
-    dim3 grid(tiles_x * tiles_y, 1, B);
-    const size_t smem = (size_t)g.warp_bytes;
-    auto kern = k_lob_u8<L>;
-    if (int rc = set_smem(kern, smem)) return rc;
-    kern<<<grid, 32, smem, s>>>(p, tiles_x, tiles_y);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_lob_u8: ") + cudaGetErrorString(e));
-    g_kernel = L == 32 ? "k_lob_u8<32>" : "k_lob_u8<64>";
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return MTB_OK;
-}
-
-int run_lob_u8_32(SlabParams p, int B, cudaStream_t s) { return run_lob_u8_l<32>(p, B, s); }
 
 }  // namespace mtb

@@ -27,6 +27,19 @@ def digests():
         return json.load(fh)
 
 
+_FULL = None
+
+
+def fullsize_digests():
+    """SHA-256 of the reference's outputs at the BASELINE sizes
+    (make_fullsize_digests.py)."""
+    global _FULL
+    if _FULL is None:
+        with open(os.path.join(HERE, "fullsize_digests.json")) as fh:
+            _FULL = json.load(fh)
+    return _FULL
+
+
 def topologies():
     data = np.load(os.path.join(HERE, "topologies.npz"))
     names = sorted({k.rsplit("_", 1)[0] for k in data.files})

@@ -3,9 +3,10 @@ the CPU oracle.  Bit-exact everywhere (integer work, no tolerance).
 
 Mirrors the reference's exactness matrix (pkg/tests/test_engine.py:25-99,
 :243-256; pkg/tests/test_acceptance.py:46-93, :186-233) and adds the five
-BASELINE configs: config-shaped digests recorded from the reference, and
-full-size frames checked on sampled bands against the oracle plus
-size-independent properties.
+BASELINE configs: reduced-size digests and FULL-SIZE digests (every config
+at the size BASELINE.json names, every radius of its sweep, config 5 as
+the 64-image batch) recorded from the reference's own filter_image by
+tests/golden/make_golden.py and make_fullsize_digests.py.
 """
 
 import numpy as np
@@ -274,71 +275,113 @@ def test_host_pipeline_bands(bits, r, bands, stream, monkeypatch):
 
 
 # ------------------------------------------------ full-size BASELINE configs
+# Every output byte of every config at its BASELINE size, hashed against the
+# reference's own output (tests/golden/fullsize_digests.json).
 
-def _check_bands(px, out, n, samples, mode="uniform"):
-    H = px.shape[0]
-    for a in samples:
-        b = min(H, a + 24)
-        ref = O.iot_rows(px, n, a, b, mode=mode, threads=1)
-        assert np.array_equal(out[a:b], ref), (n, a)
+_cache = {}
 
 
-def _properties(px, out, n):
-    """Size-independent checks: output values occur in the input, a
-    constant-offset input shifts the output, and the rank filter with
-    rank 1 / n^2 is bounded by the local min / max."""
+def _frame(key):
+    if key not in _cache:
+        _cache.clear()  # one large frame at a time
+        gen = {"cfg2": workloads.cfg2_blur_sp_u8, "cfg3": workloads.cfg3_uniform_u16,
+               "cfg4": workloads.cfg4_three_gauss_u16, "cfg5": workloads.cfg5_batch_u8}[key]
+        _cache[key] = gen()
+    return _cache[key]
+
+
+def _full(name):
+    rec = G.fullsize_digests()[name]
+    return rec
+
+
+@pytest.mark.parametrize("r", workloads.CONFIG_RADII[2])
+def test_cfg2_full_size_digest(r):
+    """Config 2 (4096^2 u8): the drop-in filter_image (pageable frame), the
+    streaming host entry on a page-locked frame, and the device-resident
+    entry -- all equal to the reference's full frame."""
+    px = _frame("cfg2")
+    rec = _full(f"cfg2_4096_r{r}")
+    assert G.sha(px) == rec["input"]
+    out, _ = mtb.filter_image(px, 2 * r + 1)
+    assert G.sha(out.pixels) == rec["output"]
+    pin = torch.from_numpy(px).pin_memory().numpy()
+    pout = torch.empty(px.shape, dtype=torch.uint8).pin_memory().numpy()
+    assert G.sha(mtb.filter_host_buffer(pin, r, out=pout)) == rec["output"]
+    dev = mtb.rank_filter(torch.from_numpy(px).cuda(), r).cpu().numpy()
+    assert G.sha(dev) == rec["output"]
+
+
+@pytest.mark.parametrize("r", workloads.CONFIG_RADII[3])
+def test_cfg3_full_size_digest(r):
+    """Config 3 (4096^2 u16 uniform): host entry and device-resident entry
+    (whose 16-bit kernel choice is sampled on the device)."""
+    px = _frame("cfg3")
+    rec = _full(f"cfg3_4096_r{r}")
+    assert G.sha(px) == rec["input"]
+    out, _ = mtb.filter_image(px, 2 * r + 1)
+    assert G.sha(out.pixels) == rec["output"]
+    dev = mtb.rank_filter(torch.from_numpy(px).cuda(), r).cpu().numpy()
+    assert G.sha(dev) == rec["output"]
+
+
+@pytest.mark.parametrize("r", workloads.CONFIG_RADII[4])
+def test_cfg4_full_size_digest_row_sharded(r):
+    """Config 4 (8192^2 u16, adaptive mode): one device, and row-sharded over
+    2 and 4 'devices' (device 0 listed several times stands in for several
+    GPUs: each slab is a separate mtb_filter_host_rows call with its halo
+    rows read from the host frame)."""
+    px = _frame("cfg4")
+    rec = _full(f"cfg4_8192_r{r}_adaptive")
+    assert G.sha(px) == rec["input"]
+    out, _ = mtb.filter_image(px, 2 * r + 1, mode="adaptive")
+    assert G.sha(out.pixels) == rec["output"]
+    for k in (2, 4):
+        out, _ = mtb.filter_image(px, 2 * r + 1, mode="adaptive", devices=[0] * k)
+        assert G.sha(out.pixels) == rec["output"], k
+
+
+@pytest.mark.parametrize("r", workloads.CONFIG_RADII[5])
+def test_cfg5_full_batch_digest(r):
+    """Config 5 (64 x 2048^2 u8): the one-launch device batch entry, and the
+    host batch spread over 'devices' (plan_images runs through the
+    frame-sequence entry) -- every image and the stacked batch equal the
+    reference."""
+    b5 = _frame("cfg5")
+    rec = _full(f"cfg5_batch_r{r}")
+    assert G.sha(b5) == rec["input"]
+    dev = mtb.rank_filter(torch.from_numpy(b5).cuda(), r).cpu().numpy()
+    bad = [i for i in range(64) if G.sha(dev[i]) != _full(f"cfg5_2048_img{i}_r{r}")["output"]]
+    assert not bad, bad
+    assert G.sha(dev) == rec["output"]
+    del dev
+    outs = mtb.filter_images(b5, 2 * r + 1, devices=[0] * 3)
+    bad = [i for i in range(64) if G.sha(outs[i]) != _full(f"cfg5_2048_img{i}_r{r}")["output"]]
+    assert not bad, bad
+
+
+def _properties(px, out):
+    """Size-independent check: every output value occurs in the input."""
     assert out.shape == px.shape and out.dtype == px.dtype
     present = np.zeros(1 << (8 * px.itemsize), dtype=bool)
     present[px.ravel()] = True
     assert present[out.ravel()].all()
 
 
-@pytest.mark.parametrize("r", workloads.CONFIG_RADII[2])
-def test_cfg2_full_size(r):
-    px = _cfg2()
-    n = 2 * r + 1
-    out, _ = mtb.filter_image(px, n)
-    _properties(px, out.pixels, n)
-    _check_bands(px, out.pixels, n, [0, 2048 - 12, 4096 - 24])
-
-
-@pytest.mark.parametrize("r", workloads.CONFIG_RADII[3])
-def test_cfg3_full_size(r):
-    px = _cfg3()
-    n = 2 * r + 1
-    out, _ = mtb.filter_image(px, n)
-    _properties(px, out.pixels, n)
-    _check_bands(px, out.pixels, n, [0, 4096 - 24])
-
-
-@pytest.mark.parametrize("r", workloads.CONFIG_RADII[4])
-def test_cfg4_full_size_adaptive(r):
-    px = _cfg4()
-    n = 2 * r + 1
-    out, _ = mtb.filter_image(px, n, mode="adaptive")
-    _properties(px, out.pixels, n)
-    _check_bands(px, out.pixels, n, [0, 8192 - 24], mode="uniform")
-
-
-_cache = {}
-
-
-def _cfg2():
-    if "2" not in _cache:
-        _cache["2"] = workloads.cfg2_blur_sp_u8()
-    return _cache["2"]
-
-
-def _cfg3():
-    if "3" not in _cache:
-        _cache["3"] = workloads.cfg3_uniform_u16()
-    return _cache["3"]
-
-
-def _cfg4():
-    if "4" not in _cache:
-        _cache["4"] = workloads.cfg4_three_gauss_u16()
-    return _cache["4"]
+def test_full_size_off_centre_ranks():
+    """Config-2/3 frames at non-median ranks (no reference digest at full
+    size): the outputs occur in the input and are ordered by rank."""
+    for key, r in (("cfg2", 15), ("cfg3", 7)):
+        px = _frame(key)
+        dev = torch.from_numpy(px).cuda()
+        n = 2 * r + 1
+        prev = None
+        for rank in (1, n * n // 4, n * n // 2 + 1, n * n):
+            out = mtb.rank_filter(dev, r, rank=rank).cpu().numpy()
+            _properties(px, out)
+            if prev is not None:
+                assert (out >= prev).all(), (key, rank)
+            prev = out
 
 
 # ------------------------------------------ every kernel family vs the oracle
@@ -346,11 +389,11 @@ def _cfg4():
 _FAMILY_CASES = [c for c in G.small_cases() if c[0]["rank"] is None and c[0]["percentile"] is None]
 
 
-@pytest.mark.parametrize("family", ["vert", "vert2", "ctmf", "lob", "sortnet", "colhist"])
+@pytest.mark.parametrize("family", ["vert", "ctmf", "sortnet", "colhist", "colhist16s"])
 def test_each_kernel_family_is_exact(family, monkeypatch):
     """MTB_KERNEL forces one family; families that do not apply to a case
-    (ctmf/lob: 8-bit only; sortnet: median of n <= 7) fall through to the
-    general kernel, so every case must still be exact."""
+    (ctmf: 8-bit only; sortnet: median of n <= 7) fall through to the
+    default dispatch, so every case must still be exact."""
     from paper_1105_3829_b200 import _lib
 
     monkeypatch.setenv("MTB_KERNEL", family)
@@ -369,19 +412,19 @@ def test_each_kernel_family_is_exact(family, monkeypatch):
         px16 = rng.integers(0, 65536, (70, 90)).astype(np.uint16)
         out16 = mtb.rank_filter(torch.from_numpy(px16).cuda(), min(r, 34)).cpu().numpy()
         assert np.array_equal(out16, O.iot_filter(px16, 2 * min(r, 34) + 1)), (family, r)
-    expect = {"vert": "k_vert_u8", "vert2": "k_vert2_u16", "ctmf": "k_ctmf_u8", "lob": "k_lob_u8",
-              "sortnet": "k_sortnet", "colhist": "k_colhist_u8"}[family]
+    expect = {"vert": "k_vert_u8", "ctmf": "k_ctmf_u8", "sortnet": "k_sortnet", "colhist": "k_colhist_u8",
+              "colhist16s": "k_colhist16s_u16"}[family]
     assert expect in seen, seen
 
 
 @pytest.mark.parametrize("r", [1, 4, 9, 20, 130])
-def test_vert2_u16_ranks_and_counter_widths(r, monkeypatch):
-    """k_vert2_u16 (sorted-column low byte) on wide-spread and compact 16-bit
-    images, at min / max / off-centre ranks.  r=130 (n^2 > 65535, the sorted
-    columns exceed shared memory) must fall back to k_vert_u16, still exact."""
+def test_vert_u16_ranks_and_counter_widths(r, monkeypatch):
+    """k_vert_u16 (the general 16-bit path, any radius) on wide-spread and
+    compact images at min / max / off-centre ranks, u16 and (r = 130,
+    n^2 > 65535) u32 counters."""
     from paper_1105_3829_b200 import _lib
 
-    monkeypatch.setenv("MTB_KERNEL", "vert2")
+    monkeypatch.setenv("MTB_KERNEL", "vert")
     rng = np.random.default_rng(40 + r)
     h, w = (300, 280) if r == 130 else (90, 110)
     n = 2 * r + 1
@@ -390,8 +433,7 @@ def test_vert2_u16_ranks_and_counter_widths(r, monkeypatch):
     for px in imgs:
         for rank in (1, n * n, (n * n) // 3 + 1):
             out = mtb.rank_filter(torch.from_numpy(px).cuda(), r, rank=rank).cpu().numpy()
-            expect = "k_vert_u16" if r == 130 else "k_vert2_u16"
-            assert _lib.last_kernel().startswith(expect), _lib.last_kernel()
+            assert _lib.last_kernel().startswith("k_vert_u16"), _lib.last_kernel()
             assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (r, rank)
 
 
@@ -606,6 +648,85 @@ def test_mednet_shapes_slabs_batch_lut(bits, rt, monkeypatch):
         # value map (reduced precision)
         o, _ = mtb.filter_image(px, n, max_error=16)
         assert np.array_equal(o.pixels, O.iot_filter(px, n, max_error=16)), n
+
+
+_SERIAL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_1105_3829_b200 as mtb, workloads
+from oracle import oracle as O
+torch.cuda.set_device(0)
+px = workloads.cfg2_blur_sp_u8(700, 900)
+pin = torch.from_numpy(px).pin_memory().numpy()
+for r in (7, 15, 31):
+    ref = O.iot_filter(px, 2 * r + 1)
+    out, _ = mtb.filter_image(px, 2 * r + 1)
+    assert np.array_equal(out.pixels, ref), ("pageable", r)
+    assert np.array_equal(mtb.filter_host_buffer(pin, r), ref), ("pinned", r)
+    outs = mtb.filter_host_frames([pin, px], [r, r + 1])
+    assert np.array_equal(outs[0], ref), ("frames", r)
+px16 = workloads.cfg4_three_gauss_u16(600, 500)
+out, _ = mtb.filter_image(torch.from_numpy(px16).pin_memory().numpy(), 31)
+assert np.array_equal(out.pixels, O.iot_filter(px16, 31))
+print("SERIAL_OK")
+"""
+
+
+def test_host_paths_under_serialised_launches():
+    """CUDA_LAUNCH_BLOCKING=1 serialises every launch (as profilers and
+    sanitizers do): the streaming host paths enqueue all their copies and
+    row-arrival writes before the kernel whose CTAs wait on them, so they
+    must still finish (r = 15, 31: the streaming launch) and be exact."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1")
+    res = subprocess.run([sys.executable, "-c", _SERIAL_SCRIPT.format(root=root)], env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0 and "SERIAL_OK" in res.stdout, res.stdout[-2000:] + res.stderr[-4000:]
+
+
+def test_filter_images_over_devices():
+    """filter_images: a batch spread over 'devices' (device 0 listed several
+    times stands in for several GPUs), mixed 8-bit content, ranks and a
+    value map; every image equal to its own filter_image result / oracle."""
+    b = workloads.cfg5_batch_u8(7, 150, 140)
+    for devs in ([0], [0, 0], [0, 0, 0, 0]):
+        outs = mtb.filter_images(b, 15, devices=devs)
+        for i in range(b.shape[0]):
+            assert np.array_equal(outs[i], O.iot_filter(b[i], 15)), (devs, i)
+    outs = mtb.filter_images(list(b[:3]), 9, rank=5, devices=[0, 0])
+    for i in range(3):
+        assert np.array_equal(outs[i], O.iot_filter(b[i], 9, rank=5))
+    outs = mtb.filter_images(b[:4], 5, max_error=16, devices=[0, 0])
+    for i in range(4):
+        assert np.array_equal(outs[i], O.iot_filter(b[i], 5, max_error=16))
+    with pytest.raises(ValueError):
+        mtb.filter_images([b[0], b[0][:10]], 5)
+    assert mtb.filter_images([], 5) == []
+
+
+def test_rank_filter_checks_out_and_device():
+    """rank_filter rejects an `out` of the wrong dtype, device or shape
+    instead of writing out of bounds."""
+    px = torch.from_numpy(np.arange(64 * 80, dtype=np.uint16).reshape(64, 80).copy()).cuda()
+    with pytest.raises(ValueError):
+        mtb.rank_filter(px, 2, out=torch.empty((64, 80), dtype=torch.uint8, device="cuda"))
+    with pytest.raises(ValueError):
+        mtb.rank_filter(px, 2, out=torch.empty((64, 80), dtype=torch.uint16))
+    with pytest.raises(ValueError):
+        mtb.rank_filter(px, 2, out=torch.empty((60, 80), dtype=torch.uint16, device="cuda"))
+    b = px.reshape(4, 16, 80)
+    with pytest.raises(ValueError):
+        mtb.rank_filter(b, 2, out=torch.empty((4, 16, 79), dtype=torch.uint16, device="cuda"))
+    with pytest.raises(ValueError):
+        mtb.filter_host_buffer(px.cpu().numpy(), 2, lut=np.arange(256, dtype=np.uint16))
+    s = torch.cuda.Stream()
+    out = mtb.rank_filter(px, 2, stream=s)
+    s.synchronize()
+    assert np.array_equal(out.cpu().numpy(), O.iot_filter(px.cpu().numpy(), 5))
 
 
 @pytest.mark.parametrize("ndev", [2, 3])
