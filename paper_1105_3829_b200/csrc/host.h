@@ -66,6 +66,7 @@ int run_colhist4p_256(SlabParams p, int B, cudaStream_t s, int pl);
 // wk: window-keyed first sweep (pays off on compact data, see kernel)
 int run_colhist16_u16(SlabParams p, int B, cudaStream_t s, int wk = 1);
 int run_colhist16s_u16(SlabParams p, int B, cudaStream_t s);
+int run_colhist16c_u16(SlabParams p, int B, cudaStream_t s);
 // compile-time window sides of k_colhist16_u16; 1 (NOT_COVERED) when n is outside the range
 int run_colhist16_fixed_a(SlabParams p, int B, cudaStream_t s, int wk);
 int run_colhist16_fixed_b(SlabParams p, int B, cudaStream_t s, int wk);

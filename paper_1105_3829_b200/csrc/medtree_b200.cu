@@ -266,10 +266,11 @@ static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
     const std::string force = forced_kernel();
     if (force == "colhist") return run_colhist16_u16(p, B, s, 1);
     if (force == "colhist16s") return run_colhist16s_u16(p, B, s);
-    const bool small_r = p.radius <= 16;
+    if (force == "colhist16c") return run_colhist16c_u16(p, B, s);
+    const bool small_r = p.radius <= env_int("MTB_U16C_MAX_R", 16);
     if (g_spread_hint >= 0) {
         const bool wide = g_spread_hint > SPREAD_WIDE;
-        if (wide && small_r) return run_colhist16s_u16(p, B, s);
+        if (wide && small_r) return run_colhist16c_u16(p, B, s);
         return run_colhist16_u16(p, B, s, wide ? 0 : 1);
     }
     int *d_spread = nullptr;
@@ -283,11 +284,11 @@ static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
     if (!rc) g_launches.fetch_add(1, std::memory_order_relaxed);
     p.spread = d_spread;
     if (!rc && small_r) {
-        p.gate = GATE_WIDE;  // sorted-column kernel runs on widely spread data only
-        rc = run_colhist16s_u16(p, B, s);
+        p.gate = GATE_WIDE;  // candidate kernel runs on widely spread data only
+        rc = run_colhist16c_u16(p, B, s);
         p.gate = GATE_COMPACT;  // two-phase kernel (window-keyed sweep) otherwise
         if (!rc) rc = run_colhist16_u16(p, B, s, 1);
-        if (!rc) g_kernel = "k_colhist16s_u16|k_colhist16_u16 (device-selected)";
+        if (!rc) g_kernel = "k_colhist16c_u16|k_colhist16_u16 (device-selected)";
     } else if (!rc) {
         rc = run_colhist16_u16(p, B, s, WK_FROM_SPREAD);  // window-keyed sweep on compact data
     }

@@ -389,7 +389,7 @@ def test_full_size_off_centre_ranks():
 _FAMILY_CASES = [c for c in G.small_cases() if c[0]["rank"] is None and c[0]["percentile"] is None]
 
 
-@pytest.mark.parametrize("family", ["vert", "ctmf", "sortnet", "colhist", "colhist16s"])
+@pytest.mark.parametrize("family", ["vert", "ctmf", "sortnet", "colhist", "colhist16s", "colhist16c"])
 def test_each_kernel_family_is_exact(family, monkeypatch):
     """MTB_KERNEL forces one family; families that do not apply to a case
     (ctmf: 8-bit only; sortnet: median of n <= 7) fall through to the
@@ -413,7 +413,7 @@ def test_each_kernel_family_is_exact(family, monkeypatch):
         out16 = mtb.rank_filter(torch.from_numpy(px16).cuda(), min(r, 34)).cpu().numpy()
         assert np.array_equal(out16, O.iot_filter(px16, 2 * min(r, 34) + 1)), (family, r)
     expect = {"vert": "k_vert_u8", "ctmf": "k_ctmf_u8", "sortnet": "k_sortnet", "colhist": "k_colhist_u8",
-              "colhist16s": "k_colhist16s_u16"}[family]
+              "colhist16s": "k_colhist16s_u16", "colhist16c": "k_colhist16c_u16"}[family]
     assert expect in seen, seen
 
 
@@ -509,15 +509,18 @@ def test_colhist16_u16_batch_slab_and_lut(monkeypatch):
     assert np.array_equal(q, ref & ~np.uint16(15))
 
 
-@pytest.mark.parametrize("kind", ["compact", "uniform"])
-def test_colhist16s_u16_sorted_columns(kind, monkeypatch):
-    """k_colhist16s_u16 (high byte from column records, low byte from sorted
-    columns) at radii covering every group size/tail, ragged tiles and
-    min / max / off-centre ranks; r=127 exceeds shared memory and must fall
-    back to the two-phase kernel, still exact."""
+@pytest.mark.parametrize("family", ["colhist16s", "colhist16c"])
+@pytest.mark.parametrize("kind", ["uniform", "compact"])
+def test_colhist16_sorted_span_kernels(kind, family, monkeypatch):
+    """The sorted-span 16-bit kernels -- k_colhist16s_u16 (column records +
+    sorted columns) and k_colhist16c_u16 (pair records + candidate runs,
+    with the crowded-bin counting path that compact data takes) -- at radii
+    covering every group size/tail, ragged tiles and min / max / off-centre
+    ranks; windows past their limits (16s: shared memory at r = 127; 16c:
+    pair counts at n > 127) fall back to the two-phase kernel, still exact."""
     from paper_1105_3829_b200 import _lib
 
-    monkeypatch.setenv("MTB_KERNEL", "colhist16s")
+    monkeypatch.setenv("MTB_KERNEL", family)
     rng = np.random.default_rng(77 if kind == "compact" else 78)
     h, w = 150, 300
     if kind == "compact":
@@ -528,7 +531,8 @@ def test_colhist16s_u16_sorted_columns(kind, monkeypatch):
         n = 2 * r + 1
         for rank in (None, 1, n * n, (n * n) // 3 + 1):
             out = mtb.rank_filter(torch.from_numpy(px).cuda(), r, rank=rank).cpu().numpy()
-            expect = "k_colhist16_u16" if r == 127 else "k_colhist16s_u16"
+            fallback = r == 127 if family == "colhist16s" else n > 127
+            expect = "k_colhist16_u16" if fallback else f"k_{family}_u16"
             assert _lib.last_kernel() == expect, _lib.last_kernel()
             assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (kind, r, rank)
 
