@@ -14,9 +14,9 @@
 //      at the column's count of high bytes below H -- the bytes below H's
 //      digits in the four record words on H's path, one IDP4A per word --
 //      and as long as the count of H in the column (the last word's byte);
-//   3. selects the k'-th smallest low byte of the candidates by two nibble
-//      counts (high nibble over all candidates, then low nibble over those
-//      in the selected high nibble), in registers.
+//   3. selects the k'-th smallest low byte of the candidates: up to 8 by a
+//      sorting network in registers, more by two nibble counts (high nibble
+//      over all candidates, then low nibble over those in the selected one).
 // Bins with more than CMAX values (compact data forced onto this kernel)
 // take two counting passes over the runs instead (u16 counters in shared
 // memory).  Exact for any image.
@@ -224,36 +224,55 @@ __global__ void __launch_bounds__(T) k_colhist16c_u16(SlabParams p) {
         const unsigned sh0 = 8 * d0;
         unsigned lo;
         if (cH <= (uint32_t)CMAX) {
-            // candidates: at most CMAX low bytes; high-nibble counts on the way
-            uint32_t hn[4] = {0, 0, 0, 0};
+            // candidates: the c_H <= CMAX low bytes, stored per thread
             int cnt = 0;
 #pragma unroll 4
             for (int j = 0; j < n; ++j) {
                 const uint32_t w3 = r3[j];
                 const int e0 = (int)__dp4a(r0[j], m0, __dp4a(r1[j], m1, __dp4a(r2[j], m2, __dp4a(w3, m3, 0u))));
                 const int ne = (int)((w3 >> sh0) & 0xffu);
-                const uint16_t *a = wcol + j * n + e0;
-                // the common run lengths 0 / 1 without a branch
-                const unsigned v0 = a[ne ? 0 : -e0] & 0xffu;  // (a valid address either way)
-                const bool on = ne != 0;
-                ch16c_count(hn, v0 >> 4, on);
-                if (on) cand[cnt * T + tid] = (uint8_t)v0;
-                cnt += on ? 1 : 0;
-                for (int e = 1; e < ne; ++e) {  // rare on spread data
-                    const unsigned v = a[e] & 0xffu;
-                    ch16c_count(hn, v >> 4, true);
-                    cand[cnt * T + tid] = (uint8_t)v;
-                    ++cnt;
+                const uint16_t *a = wcol + j * n;
+                // run lengths 0, 1, 2 without a branch (addresses stay inside the column)
+                const unsigned v0 = a[ne > 0 ? e0 : 0], v1 = a[ne > 1 ? e0 + 1 : 0];
+                if (ne > 0) cand[cnt * T + tid] = (uint8_t)v0;
+                if (ne > 1) cand[(cnt + 1) * T + tid] = (uint8_t)v1;
+                cnt += min(ne, 2);
+                if (ne > 2) {  // rare on spread data
+                    for (int e = 2; e < ne; ++e) cand[cnt++ * T + tid] = (uint8_t)a[e0 + e];
                 }
             }
-            // ---- 3. k-th smallest low byte: high nibble, then low nibble
-            const int nh = ch16c_descend16(hn, k);
-            uint32_t ln[4] = {0, 0, 0, 0};
-            for (int i = 0; i < cnt; ++i) {
-                const unsigned v = cand[i * T + tid];
-                ch16c_count(ln, v & 15u, (int)(v >> 4) == nh);
+            // ---- 3. k-th smallest low byte
+            if (cnt <= 8) {
+                // the usual handful: a 19-comparator sorting network on registers
+                uint32_t v[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = i < cnt ? (uint32_t)cand[i * T + tid] : 0x100u;
+                auto cx = [&](int i, int j) {
+                    const uint32_t lo_ = min(v[i], v[j]), hi_ = max(v[i], v[j]);
+                    v[i] = lo_;
+                    v[j] = hi_;
+                };
+                cx(0, 2); cx(1, 3); cx(4, 6); cx(5, 7);
+                cx(0, 4); cx(1, 5); cx(2, 6); cx(3, 7);
+                cx(0, 1); cx(2, 3); cx(4, 5); cx(6, 7);
+                cx(2, 4); cx(3, 5);
+                cx(1, 4); cx(3, 6);
+                cx(1, 2); cx(3, 4); cx(5, 6);
+                lo = v[0];
+#pragma unroll
+                for (int i = 1; i < 8; ++i) lo = (k == (uint32_t)(i + 1)) ? v[i] : lo;
+            } else {
+                // high nibble, then low nibble
+                uint32_t hn[4] = {0, 0, 0, 0};
+                for (int i = 0; i < cnt; ++i) ch16c_count(hn, cand[i * T + tid] >> 4, true);
+                const int nh = ch16c_descend16(hn, k);
+                uint32_t ln[4] = {0, 0, 0, 0};
+                for (int i = 0; i < cnt; ++i) {
+                    const unsigned v = cand[i * T + tid];
+                    ch16c_count(ln, v & 15u, (int)(v >> 4) == nh);
+                }
+                lo = (unsigned)(nh * 16 + ch16c_descend16(ln, k));
             }
-            lo = (unsigned)(nh * 16 + ch16c_descend16(ln, k));
         } else {
             // a crowded bin (compact data): two counting passes over the runs
             auto runs = [&](auto &&visit) {

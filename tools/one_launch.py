@@ -9,7 +9,7 @@ import workloads  # noqa: E402
 import paper_1105_3829_b200 as mtb  # noqa: E402
 
 cfg, r = int(sys.argv[1]), int(sys.argv[2])
-if len(sys.argv) > 3:
+if len(sys.argv) > 3 and sys.argv[3]:
     os.environ["MTB_KERNEL"] = sys.argv[3]
 px = {1: lambda: workloads.cfg1_uniform_u8(4096, 4096), 2: workloads.cfg2_blur_sp_u8,
       3: workloads.cfg3_uniform_u16, 4: workloads.cfg4_three_gauss_u16}[cfg]()
