@@ -25,7 +25,7 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s, bool use_pre) {
     const double per_stripe = (double)warps / ((double)tiles_x * B);  // warps per column stripe
     // (with up-front snapshots a tile's init is two loads per column: from
     // n >= 97 shorter tiles balance better -- r = 63 0.82 -> 0.79 ms)
-    const int target = env_int("MTB_CT_MIN_TH", (use_pre && n >= 97) ? 24 : (n / 3 > 24 ? n / 3 : 24));
+    const int target = (use_pre && n >= 97) ? 24 : (n / 3 > 24 ? n / 3 : 24);
     int th;
     if (per_stripe >= 1.0) {
         int k = (int)((double)rows / (target * per_stripe) + 0.5);
@@ -34,7 +34,6 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s, bool use_pre) {
     } else {
         th = target;
     }
-    th = env_int("MTB_CT_TH", th);
     if (th < 8) th = 8 < rows ? 8 : rows;
     if (th > rows) th = rows;
     p.rows_per_cta = th;
@@ -43,7 +42,7 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s, bool use_pre) {
     // persistent grid: as many CTAs as are resident at once (per image)
     int ctas = (tiles + CT_WARPS - 1) / CT_WARPS;
     const int resident = (int)((sm_count() * per_sm + B - 1) / B);
-    if (env_int("MTB_CT_PERSIST", 1) && ctas > resident) ctas = resident > 0 ? resident : 1;
+    if (ctas > resident) ctas = resident > 0 ? resident : 1;
     dim3 grid(ctas, 1, B);
     // span snapshots of every tile row, computed up front (k_ctmf_pre_u8);
     // MTB_CT_PRE=0: per-warp snapshot scans inside the tiles instead
@@ -55,7 +54,7 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s, bool use_pre) {
             cudaGetLastError();
             return run_ctmf_u8_s<S, MF>(p, B, s, false);
         } else {
-            const int seg = env_int("MTB_CT_PRE_SEG", 2);
+            const int seg = 2;  // tile rows per pre-pass thread segment
             dim3 pg((p.W + CTP_T - 1) / CTP_T, (tiles_y + seg - 1) / seg, B);
             k_ctmf_pre_u8<CTP_T><<<pg, CTP_T, 0, s>>>(p, tiles_y, seg, pre);
             g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -64,14 +63,14 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s, bool use_pre) {
     // per-tile column snapshots (stream-ordered pool allocation, kept cached)
     uint8_t *snap = nullptr;
     const size_t snap_bytes = (size_t)ctas * CT_WARPS * B * ((((size_t)g.NCP * 18 + 15) & ~(size_t)15) + (size_t)g.NCP * 256);
-    if (!pre && env_int("MTB_CT_SNAP", 1)) {
+    if (!pre) {
         keep_pool_memory();
         if (cudaMallocAsync(reinterpret_cast<void **>(&snap), snap_bytes, s) != cudaSuccess) {
             cudaGetLastError();
             snap = nullptr;  // fall back to rescanning the spans
         }
     }
-    kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y, snap, env_int("MTB_CT_SCAN2", 1), pre);
+    kern<<<grid, CT_WARPS * 32, smem, s>>>(p, tiles_x, tiles_y, snap, 1, pre);
     cudaError_t e = cudaGetLastError();
     if (snap) cudaFreeAsync(snap, s);
     if (pre) cudaFreeAsync(pre, s);
@@ -82,16 +81,14 @@ static int run_ctmf_u8_s(SlabParams p, int B, cudaStream_t s, bool use_pre) {
 }
 
 int run_ctmf_u8(SlabParams p, int B, cudaStream_t s) {
+    // MTB_CT_PRE=0: per-tile snapshot scans instead of the up-front pre-pass
     const bool pre = env_int("MTB_CT_PRE", 1) != 0;
-    if (env_int("MTB_CT_S", 8) == 8) {  // n mod 8 as a compile-time constant (n odd)
-        switch ((2 * p.radius + 1) % 8) {
-            case 1: return run_ctmf_u8_s<8, 1>(p, B, s, pre);
-            case 3: return run_ctmf_u8_s<8, 3>(p, B, s, pre);
-            case 5: return run_ctmf_u8_s<8, 5>(p, B, s, pre);
-            default: return run_ctmf_u8_s<8, 7>(p, B, s, pre);
-        }
+    switch ((2 * p.radius + 1) % 8) {  // n mod 8 as a compile-time constant (n odd)
+        case 1: return run_ctmf_u8_s<8, 1>(p, B, s, pre);
+        case 3: return run_ctmf_u8_s<8, 3>(p, B, s, pre);
+        case 5: return run_ctmf_u8_s<8, 5>(p, B, s, pre);
+        default: return run_ctmf_u8_s<8, 7>(p, B, s, pre);
     }
-    return run_ctmf_u8_s<16>(p, B, s, pre);
 }
 
 
