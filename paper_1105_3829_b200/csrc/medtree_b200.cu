@@ -5,7 +5,9 @@
 // or a launch failure is reported as an error.
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -372,16 +374,103 @@ using namespace mtb;
 // device->host on a second copy stream -- so the copies of one band overlap
 // the filtering of its neighbours.  Device buffers and streams are kept per
 // device between calls (the pool grows, never shrinks).
+// Host memcpy workers for pageable frames: the drop-in filter_image gets
+// the caller's pageable numpy array, whose copies the driver would stage
+// through its own bounce buffer at one host thread's memcpy speed.  The
+// host paths instead copy pageable rows into page-locked staging buffers
+// with P threads (the calling thread included), so host memcpy, PCIe and
+// the kernels overlap band by band (host_pipeline).  Persistent workers,
+// one pool per device context; never destroyed (process exit reclaims).
+struct CopyPool {
+    std::mutex mu;
+    std::condition_variable cv, cv_done;
+    char *d = nullptr;
+    const char *s = nullptr;
+    size_t n = 0, piece = 0;
+    int pieces = 0, done = 0, P = 1;
+    std::atomic<int> next{0};
+    uint64_t gen = 0;
+
+    void start(int threads) {
+        P = std::max(1, threads);
+        for (int i = 1; i < P; ++i)
+            std::thread([this] {
+                uint64_t seen = 0;
+                for (;;) {
+                    {
+                        std::unique_lock<std::mutex> lk(mu);
+                        cv.wait(lk, [&] { return gen != seen; });
+                        seen = gen;
+                    }
+                    work();
+                }
+            }).detach();
+    }
+    void work() {
+        for (;;) {
+            const int i = next.fetch_add(1);
+            if (i >= pieces) return;
+            const size_t o = (size_t)i * piece, l = std::min(piece, n - o);
+            memcpy(d + o, s + o, l);
+            std::lock_guard<std::mutex> lk(mu);
+            if (++done == pieces) cv_done.notify_all();
+        }
+    }
+    void copy(void *dst, const void *src, size_t len) {
+        if (len < (1u << 20) || P <= 1) {
+            memcpy(dst, src, len);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            d = static_cast<char *>(dst);
+            s = static_cast<const char *>(src);
+            n = len;
+            pieces = 2 * P;
+            piece = (((len + pieces - 1) / pieces) + 4095) & ~(size_t)4095;
+            pieces = (int)((len + piece - 1) / piece);
+            done = 0;
+            next.store(0);
+            ++gen;
+        }
+        cv.notify_all();
+        work();
+        std::unique_lock<std::mutex> lk(mu);
+        cv_done.wait(lk, [&] { return done == pieces; });
+    }
+};
+
 struct HostCtx {
     int dev = -1;
     void *dsrc = nullptr, *ddst = nullptr, *dlut = nullptr;
     unsigned int *dflags = nullptr;  // [0] rows arrived, [1..] output pixels per chunk
     unsigned int *hstatus = nullptr, *dstatus = nullptr;  // mapped pinned word: a CTA timed out waiting for rows
     size_t cap = 0;
+    void *hin = nullptr, *hout = nullptr;  // page-locked staging for pageable frames
+    size_t hcap = 0;
+    CopyPool *pool = nullptr;
     cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
     static constexpr int KMAX = 16;
-    cudaEvent_t eh[KMAX], ec[KMAX];
+    cudaEvent_t eh[KMAX], ec[KMAX], eo[KMAX];
 };
+
+static int host_staging(HostCtx *ctx, size_t bytes) {
+    if (!ctx->pool) {
+        const unsigned hw = std::thread::hardware_concurrency();
+        ctx->pool = new CopyPool();
+        ctx->pool->start((int)std::min(8u, std::max(1u, hw / 2)));
+    }
+    if (ctx->hcap >= bytes) return MTB_OK;
+    if (ctx->hin) cudaFreeHost(ctx->hin);
+    if (ctx->hout) cudaFreeHost(ctx->hout);
+    ctx->hin = ctx->hout = nullptr;
+    ctx->hcap = 0;
+    cudaError_t e = cudaHostAlloc(&ctx->hin, bytes, cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaHostAlloc(&ctx->hout, bytes, cudaHostAllocDefault);
+    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+    ctx->hcap = bytes;
+    return MTB_OK;
+}
 
 // one context (and one lock) per device: host threads driving different
 // GPUs never serialise on each other
@@ -412,7 +501,8 @@ static int host_ctx(HostCtx *&ctx, std::unique_lock<std::mutex> &lock, size_t by
             return MTB_E_CUDA;
         for (int i = 0; i < HostCtx::KMAX; ++i)
             if (!ok(cudaEventCreateWithFlags(&ctx->eh[i], cudaEventDisableTiming), "cudaEventCreate") ||
-                !ok(cudaEventCreateWithFlags(&ctx->ec[i], cudaEventDisableTiming), "cudaEventCreate"))
+                !ok(cudaEventCreateWithFlags(&ctx->ec[i], cudaEventDisableTiming), "cudaEventCreate") ||
+                !ok(cudaEventCreateWithFlags(&ctx->eo[i], cudaEventDisableTiming), "cudaEventCreate"))
                 return MTB_E_CUDA;
         ctx->dev = dev;
     }
@@ -599,14 +689,19 @@ static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W
     }
     // bands: enough rows that per-band launch and halo overheads stay small
     // (measured on config 2, tools/e2e_probe.py: 4 bands of 1024 rows for
-    // r <= 31, 2 for r = 63 -- shorter bands re-pay the n-row column build)
+    // r <= 31, 2 for r = 63 -- shorter bands re-pay the n-row column build).
+    // Pageable frames are staged through page-locked buffers by the copy
+    // pool, band by band (more, shorter bands: the host memcpy is the
+    // pipeline's slowest stage there).
     const int rows = B - A;
-    const int min_rows = std::max(1024, 32 * radius);
-    int K = env_int("MTB_HOST_BANDS", std::min(8, std::max(1, rows / min_rows)));
+    const bool stage_in = !host_pinned(src), stage_out = !host_pinned(dst);
+    const int min_rows = std::max(stage_in || stage_out ? 512 : 1024, 32 * radius);
+    int K = env_int("MTB_HOST_BANDS", std::min(stage_in || stage_out ? 12 : 8, std::max(1, rows / min_rows)));
     K = std::max(1, std::min(K, std::min(HostCtx::KMAX, rows)));
     auto cuda_ok = [](cudaError_t e, const char *what) {
         return e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
     };
+    if ((stage_in || stage_out) && host_staging(ctx, (size_t)(j.bot - j.top) * row) != MTB_OK) return MTB_E_CUDA;
     if (lut) {
         if (int rc = cuda_ok(cudaMemcpyAsync(ctx->dlut, lut, ((size_t)1 << bit_depth) * j.es, cudaMemcpyHostToDevice,
                                              ctx->sh), "H2D lut"))
@@ -614,6 +709,8 @@ static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W
     }
     char *ds = static_cast<char *>(ctx->dsrc);  // global row top
     char *dd = static_cast<char *>(ctx->ddst);  // global row A
+    char *hin = static_cast<char *>(ctx->hin);    // staging: global row top
+    char *hout = static_cast<char *>(ctx->hout);  // staging: global row A
     int copied = j.top;  // source rows [top, copied) enqueued host->device
     int rc = MTB_OK;
     auto band = [&](int i, int &a, int &b) {  // global output rows of band i
@@ -627,8 +724,20 @@ static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W
         int a, b;
         band(i, a, b);
         cudaStreamWaitEvent(ctx->sd, ctx->ec[i], 0);
-        return cuda_ok(cudaMemcpyAsync(j.dst + (size_t)(a - A) * row, dd + (size_t)(a - A) * row,
-                                       (size_t)(b - a) * row, cudaMemcpyDeviceToHost, ctx->sd), "D2H");
+        char *to = stage_out ? hout : j.dst;
+        const int r2 = cuda_ok(cudaMemcpyAsync(to + (size_t)(a - A) * row, dd + (size_t)(a - A) * row,
+                                               (size_t)(b - a) * row, cudaMemcpyDeviceToHost, ctx->sd), "D2H");
+        cudaEventRecord(ctx->eo[i], ctx->sd);
+        return r2;
+    };
+    // a staged band's rows from the staging buffer to the caller's frame
+    auto unstage = [&](int i) {
+        if (!stage_out) return MTB_OK;
+        int a, b;
+        band(i, a, b);
+        const int r2 = cuda_ok(cudaEventSynchronize(ctx->eo[i]), "cudaEventSynchronize");
+        if (!r2) ctx->pool->copy(j.dst + (size_t)(a - A) * row, hout + (size_t)(a - A) * row, (size_t)(b - a) * row);
+        return r2;
     };
     int done = 0;
     for (int i = 0; i < K && rc == MTB_OK; ++i) {
@@ -636,8 +745,10 @@ static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W
         band(i, a, b);
         const int need = std::min(H, b + radius);
         if (need > copied) {
-            rc = cuda_ok(cudaMemcpyAsync(ds + (size_t)(copied - j.top) * row, j.src + (size_t)copied * row,
-                                         (size_t)(need - copied) * row, cudaMemcpyHostToDevice, ctx->sh), "H2D");
+            const size_t off = (size_t)(copied - j.top) * row, len = (size_t)(need - copied) * row;
+            if (stage_in) ctx->pool->copy(hin + off, j.src + (size_t)copied * row, len);
+            rc = cuda_ok(cudaMemcpyAsync(ds + off, stage_in ? hin + off : j.src + (size_t)copied * row, len,
+                                         cudaMemcpyHostToDevice, ctx->sh), "H2D");
             copied = need;
         }
         if (rc) break;
@@ -649,9 +760,11 @@ static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W
         if (rc) break;
         cudaEventRecord(ctx->ec[i], ctx->sc);
         if (i >= 1) rc = d2h(i - 1);
+        if (!rc && i >= 2) rc = unstage(i - 2);
         done = i;
     }
     if (rc == MTB_OK) rc = d2h(done);
+    for (int i = std::max(0, done - 1); i <= done && rc == MTB_OK; ++i) rc = unstage(i);
     const int rs = cuda_ok(cudaStreamSynchronize(ctx->sd), "cudaStreamSynchronize");
     cudaStreamSynchronize(ctx->sc);
     cudaStreamSynchronize(ctx->sh);
