@@ -61,6 +61,24 @@ def test_abi_rejects_invalid_arguments_without_device():
     rc = lib.mtb_filter_host_frames(None, dummy, dummy, None, 2, 8, 8, 8, None, 0)
     assert rc == _lib.MTB_E_INVAL and b"null" in lib.mtb_last_error()
     assert lib.mtb_filter_host_frames(None, None, None, None, 0, 8, 8, 8, None, 0) == _lib.MTB_OK
+    # host rows entry: its own checks run before any device call
+    rc = lib.mtb_filter_host_rows(dummy, dummy, 12, 8, 8, 0, 8, 1, 5, None, 0, -1)
+    assert rc == _lib.MTB_E_INVAL and b"bit_depth" in lib.mtb_last_error()
+    rc = lib.mtb_filter_host_rows(dummy, dummy, 8, 8, 8, 3, 9, 1, 5, None, 0, -1)
+    assert rc == _lib.MTB_E_INVAL and b"row range" in lib.mtb_last_error()
+    rc = lib.mtb_filter_host_rows(None, dummy, 8, 8, 8, 0, 8, 1, 5, None, 0, -1)
+    assert rc == _lib.MTB_E_INVAL and b"null" in lib.mtb_last_error()
+    assert lib.mtb_filter_host_rows(dummy, dummy, 8, 8, 8, 4, 4, 1, 5, None, 0, -1) == _lib.MTB_OK
+
+
+def test_host_entries_check_lut_length():
+    """A value map must hold 2^bit_depth entries (the C host entries copy
+    that many from the pointer): a short one is rejected in Python."""
+    px16 = np.zeros((8, 8), np.uint16)
+    with pytest.raises(ValueError, match="2\\^16"):
+        mtb.filter_host_buffer(px16, 1, lut=np.arange(256, dtype=np.uint16))
+    with pytest.raises(ValueError, match="2\\^8"):
+        mtb.filter_host_frames([np.zeros((8, 8), np.uint8)], 1, lut=np.arange(16, dtype=np.uint8))
 
 
 def test_host_frames_validates_before_any_device_call():
