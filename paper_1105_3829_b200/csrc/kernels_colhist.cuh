@@ -370,6 +370,32 @@ __device__ __forceinline__ void ch4p_gather(const uint32_t *pr, const uint32_t *
 }
 
 
+// the same with the single column's word supplied by the caller
+template <int GP>
+__device__ __forceinline__ void ch4p_gather_sv(const uint32_t *pr, uint32_t sv, int kp, int np, uint32_t &w0,
+                                               uint32_t &w1) {
+    w0 = __byte_perm(sv, 0, 0x4140);
+    w1 = __byte_perm(sv, 0, 0x4342);
+    const uint32_t *rp = pr + kp;
+    const int full = np - np % GP;
+    int j = 0;
+    for (; j < full; j += GP) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int q = 0; q < GP; q += 2) t += rp[j + q] + (q + 1 < GP ? rp[j + q + 1] : 0u);
+        w0 += __byte_perm(t, 0, 0x4140);
+        w1 += __byte_perm(t, 0, 0x4342);
+    }
+    if (j < np) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int q = 0; q < GP - 1; ++q)
+            if (j + q < np) t += rp[j + q];
+        w0 += __byte_perm(t, 0, 0x4140);
+        w1 += __byte_perm(t, 0, 0x4342);
+    }
+}
+
 // the 4-level selection of the rank-k element (k updated to the rank within
 // the selected value) from the records of the window starting at rp (= record
 // row 0, thread column applied)
@@ -932,17 +958,31 @@ namespace mtb {
 // pair changes with shared-memory atomics (adjacent columns belong to
 // adjacent threads); counts never go below zero, so a per-byte decrement
 // never borrows across bytes.
+// PL = 4: three pair levels, and NO level-2 single records -- the single
+// column of a level-2 pair gather derives its word from its four level-3
+// words (IDP4A each), which frees 64 B per stripe column: three pair levels
+// then fit two 256-thread CTAs per SM up to r = 32 (PL = 2 before), and a
+// row update is 12 shared-memory atomics instead of 14.
+__host__ __device__ constexpr int ch4p_singles(int PL) { return PL == 4 ? 69 : CH4_RECS; }
+__host__ __device__ constexpr int colhist4q_bytes(int T, int r, int PL) {
+    const int ncp = colhist4p_ncolp(T, r);
+    return (ch4p_singles(PL) * ncp + ch4p_recs(PL == 4 ? 3 : PL) * (ncp / 2)) * 4;
+}
+
 template <int T, int G, int M, int PL, bool STREAM, int NF = 0>
 __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
     constexpr int GP = G / 2;
-    constexpr int PR = ch4p_recs(PL);
+    constexpr bool DL2 = PL == 4;           // level-2 singles derived from level 3
+    constexpr int PLP = DL2 ? 3 : PL;        // pair levels
+    constexpr int PR = ch4p_recs(PLP);
+    constexpr int NS = ch4p_singles(PL);     // single record rows
+    constexpr int R3 = DL2 ? 5 : 21;         // first level-3 single row
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int r = NF ? NF / 2 : p.radius, H = p.H, W = p.W, n = NF ? NF : 2 * r + 1;
     const int NCOL = T + 2 * r, NCP = colhist4p_ncolp(T, r), NPR = NCP / 2;
-    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCP] singles
-    uint32_t *prs = rec + CH4_RECS * NCP;                     // [PR][NPR] pairs
-    uint8_t *recb = smem_raw;
+    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [NS][NCP] singles
+    uint32_t *prs = rec + NS * NCP;                           // [PR][NPR] pairs
     const int X0 = blockIdx.x * T;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
     if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
@@ -952,28 +992,45 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
     uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
     const int x = X0 + tid;
+    // single-record updates (one atomic per level kept; the word is the
+    // thread's own column, so there is no contention)
+    auto sbump = [&](int c, unsigned v, int d) {
+        const unsigned one = (unsigned)d;
+        atomicAdd(rec + (0 * NCP + c), one << (8 * (v >> 6)));
+        atomicAdd(rec + ((1 + (v >> 6)) * NCP + c), one << (8 * ((v >> 4) & 3)));
+        if (!DL2) atomicAdd(rec + ((5 + (v >> 4)) * NCP + c), one << (8 * ((v >> 2) & 3)));
+        atomicAdd(rec + ((R3 + (v >> 2)) * NCP + c), one << (8 * (v & 3)));
+    };
 
-    for (int i = tid; i < CH4_RECS * NCP; i += T) rec[i] = 0;
+    for (int i = tid; i < NS * NCP; i += T) rec[i] = 0;
     __syncthreads();
     for (int c = tid; c < NCOL; c += T) {
         const int gx = clampi(X0 - r + c, 0, W - 1);
         // (atomic adds here too: measured r = 15 0.358 -> 0.319 ms, r = 31
         // 0.595 -> 0.530 against byte read-modify-writes)
-        for (int j = -r; j <= r; ++j)
-            ch4_bump_upd(recb, NCP, c, __ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx), 1);
+        for (int j = -r; j <= r; ++j) sbump(c, __ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx), 1);
     }
     __syncthreads();
+    // level-2 word of column c for record p2, from its four level-3 words
+    auto l2_from_l3 = [&](int p2, int c) -> uint32_t {
+        const uint32_t *q = rec + (R3 + 4 * p2) * NCP + c;
+        return __dp4a(q[0], 0x01010101u, 0u) | (__dp4a(q[NCP], 0x01010101u, 0u) << 8) |
+               (__dp4a(q[2 * NCP], 0x01010101u, 0u) << 16) | (__dp4a(q[3 * NCP], 0x01010101u, 0u) << 24);
+    };
     for (int i = tid; i < PR * NPR; i += T) {
         const int row = i / NPR, k = i - row * NPR;
-        prs[i] = rec[row * NCP + 2 * k] + rec[row * NCP + 2 * k + 1];
+        if (DL2 && row >= 5)
+            prs[i] = l2_from_l3(row - 5, 2 * k) + l2_from_l3(row - 5, 2 * k + 1);
+        else
+            prs[i] = rec[row * NCP + 2 * k] + rec[row * NCP + 2 * k + 1];
     }
     // pair updates: levels 0-2 of value v, +-1 in the byte of the next digit
     auto pbump = [&](int c, unsigned v, int d) {
         const int k = c >> 1;
         const unsigned one = (unsigned)d;  // +1 or 0xffffffff (-1)
         atomicAdd(prs + 0 * NPR + k, one << (8 * (v >> 6)));
-        if (PL >= 2) atomicAdd(prs + (1 + (v >> 6)) * NPR + k, one << (8 * ((v >> 4) & 3)));
-        if (PL >= 3) atomicAdd(prs + (5 + (v >> 4)) * NPR + k, one << (8 * ((v >> 2) & 3)));
+        if (PLP >= 2) atomicAdd(prs + (1 + (v >> 6)) * NPR + k, one << (8 * ((v >> 4) & 3)));
+        if (PLP >= 3) atomicAdd(prs + (5 + (v >> 4)) * NPR + k, one << (8 * ((v >> 2) & 3)));
     };
     constexpr int CH_PF = 2;
     int gxs[CH_PF];
@@ -999,8 +1056,8 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
             for (int u = 0; u < CH_PF; ++u) {
                 const int c = tid + u * T;
                 if (c < NCOL) {  // (vo == vi cancels: no data-dependent branch)
-                    ch4_bump_upd(recb, NCP, c, pvo[u], -1);
-                    ch4_bump_upd(recb, NCP, c, pvi[u], 1);
+                    sbump(c, pvo[u], -1);
+                    sbump(c, pvi[u], 1);
                     pbump(c, pvo[u], -1);
                     pbump(c, pvi[u], 1);
                 }
@@ -1012,8 +1069,8 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
                     const int gx = clampi(X0 - r + c, 0, W - 1);
                     const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
                     if (vo == vi) continue;
-                    ch4_bump_upd(recb, NCP, c, vo, -1);
-                    ch4_bump_upd(recb, NCP, c, vi, 1);
+                    sbump(c, vo, -1);
+                    sbump(c, vi, 1);
                     pbump(c, vo, -1);
                     pbump(c, vi, 1);
                 }
@@ -1024,19 +1081,21 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         uint32_t k = p.rank, w0, w1;
         ch4p_gather<GP>(prs, rec, kp, cs, np, w0, w1);
         const int d3 = ch4_descend(w0, w1, k);
-        if (PL >= 2)
+        if (PLP >= 2)
             ch4p_gather<GP>(prs + (1 + d3) * NPR, rec + (1 + d3) * NCP, kp, cs, np, w0, w1);
         else
             ch4_gather<G, M>(rec + (1 + d3) * NCP + tid, n, w0, w1);
         const int d2 = ch4_descend(w0, w1, k);
         const int p2 = d3 * 4 + d2;
-        if (PL >= 3)
+        if (DL2)
+            ch4p_gather_sv<GP>(prs + (5 + p2) * NPR, l2_from_l3(p2, cs), kp, np, w0, w1);
+        else if (PLP >= 3)
             ch4p_gather<GP>(prs + (5 + p2) * NPR, rec + (5 + p2) * NCP, kp, cs, np, w0, w1);
         else
             ch4_gather<G, M>(rec + (5 + p2) * NCP + tid, n, w0, w1);
         const int d1 = ch4_descend(w0, w1, k);
         const int p3 = p2 * 4 + d1;
-        ch4_gather<G, M>(rec + (21 + p3) * NCP + tid, n, w0, w1);
+        ch4_gather<G, M>(rec + (R3 + p3) * NCP + tid, n, w0, w1);
         const int d0 = ch4_descend(w0, w1, k);
         const unsigned v = (unsigned)(p3 * 4 + d0);
         if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;

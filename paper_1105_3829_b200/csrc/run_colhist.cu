@@ -99,14 +99,16 @@ int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
     int var = env_int("MTB_CH_VAR", -1);
     if (var < 0) {
         // measured on config 2 with compile-time window sides and atomic
-        // record updates (tools/probe.py sweep):
-        // 16-bin records for r <= 2; from r = 3 radix-4 records with pair
-        // records for as many upper levels as keep two 256-thread CTAs per
-        // SM (3 levels up to r = 16, 2 above).  Plain radix-4 (var 12/13)
-        // trails them by 3-15% over r = 3..10.
+        // record updates (tools/probe.py sweep, DESIGN.md sections 3.1b,
+        // 3.3): 16-bin records for r <= 2; from r = 3 radix-4 records with
+        // pair records for the three upper levels -- with the level-2
+        // single records (var 30) up to r = 16, derived from level 3
+        // (var 32, PL = 4: two CTAs per SM up to r = 48) above.  Plain
+        // radix-4 (var 12/13) trails by 3-15% over r = 3..10.
         const int r = p.radius, lim = 113 * 1024;
         var = r <= 2 ? 0
               : (r <= 16 && colhist4p_bytes(256, r, 3) <= lim) ? 30
+              : colhist4q_bytes(256, r, 4) <= lim ? 32
               : colhist4p_bytes(256, r, 2) <= lim ? 31
                                                    : 12;
     }
@@ -116,6 +118,7 @@ int run_colhist_u8(SlabParams p, int B, cudaStream_t s) {
         case 30: return run_colhist4p_256(p, B, s, 3);
         case 31: return run_colhist4p_256(p, B, s, 2);
         case 34: return run_colhist4p_256(p, B, s, 1);
+        case 32: return run_colhist4p_256(p, B, s, 4);
         case 13: return run_colhist4_u8<128>(p, B, s, "k_colhist4_u8<128>");
         default: return run_colhist4_u8<256>(p, B, s, "k_colhist4_u8<256>");
     }

@@ -2,38 +2,24 @@
 // pair records (k_colhist4p_u8); see run_colhist.cu for the dispatch.
 #include <algorithm>
 
-#include "host.h"
-#include "kernels_colhist.cuh"
+#include "run_colhist4p.cuh"
 
 namespace mtb {
 
-template <int T, int G, int M, int PL, int NF = 0>
-static int run_colhist4p_u8_gm(SlabParams p, int B, cudaStream_t s, const char *name) {
-    const size_t smem = (size_t)colhist4p_bytes(T, p.radius, PL);
-    auto kern = p.in_rows ? k_colhist4p_u8<T, G, M, PL, true, NF> : k_colhist4p_u8<T, G, M, PL, false, NF>;
-    if (int rc = set_smem(kern, smem)) return rc;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int bx = (p.W + T - 1) / T;
-    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm);
-    dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
-    return launch(kern, grid, T, smem, s, p, name);
-}
+int run_colhist4q_fixed(SlabParams p, int B, cudaStream_t s);
 
 // pair records (G even: n <= 127); PL pair levels
 template <int T, int PL>
 static int run_colhist4p_u8(SlabParams p, int B, cudaStream_t s, const char *name) {
     const int n = 2 * p.radius + 1;
     // compile-time window side for the radii each variant serves (PL = 3:
-    // r = 11..15, PL = 2: r = 16..32; run_colhist.cu)
+    // r = 2..18, PL = 4: r = 16..48; run_colhist.cu)
+    if (PL == 4 && T == 256 && n >= 33 && n <= 97) {  // compile-time window sides r = 16..48 (run_colhist4q.cu)
+        const int rc = run_colhist4q_fixed(p, B, s);
+        if (rc != 1) return rc;
+    }
     if (PL == 3 && n >= 5 && n <= 37)
         return with_fixed_n<5, 37>(n, [&](auto nf) {
-            constexpr int NF = decltype(nf)::value, G = carry_free_group(NF);  // even: n <= 127
-            return run_colhist4p_u8_gm<T, G, NF % G, PL, NF>(p, B, s, name);
-        });
-    if (PL == 2 && n >= 29 && n <= 65)
-        return with_fixed_n<29, 65>(n, [&](auto nf) {
             constexpr int NF = decltype(nf)::value, G = carry_free_group(NF);  // even: n <= 127
             return run_colhist4p_u8_gm<T, G, NF % G, PL, NF>(p, B, s, name);
         });
@@ -53,6 +39,7 @@ static int run_colhist4p_u8(SlabParams p, int B, cudaStream_t s, const char *nam
 
 int run_colhist4p_256(SlabParams p, int B, cudaStream_t s, int pl) {
     switch (pl) {
+        case 4: return run_colhist4p_u8<256, 4>(p, B, s, "k_colhist4p_u8<256,4>");
         case 3: return run_colhist4p_u8<256, 3>(p, B, s, "k_colhist4p_u8<256,3>");
         case 2: return run_colhist4p_u8<256, 2>(p, B, s, "k_colhist4p_u8<256,2>");
         default: return run_colhist4p_u8<256, 1>(p, B, s, "k_colhist4p_u8<256,1>");

@@ -440,7 +440,8 @@ def test_vert_u16_ranks_and_counter_widths(r, monkeypatch):
 @pytest.mark.parametrize("var,name", [(0, "k_colhist_u8<128,1>"), (2, "k_colhist_u8<128,2>"),
                                       (12, "k_colhist4_u8<256>"), (13, "k_colhist4_u8<128>"),
                                       (30, "k_colhist4p_u8<256,3>"),
-                                      (31, "k_colhist4p_u8<256,2>"), (34, "k_colhist4p_u8<256,1>")])
+                                      (31, "k_colhist4p_u8<256,2>"), (32, "k_colhist4p_u8<256,4>"),
+                                      (34, "k_colhist4p_u8<256,1>")])
 def test_colhist_variants_all_group_tails(var, name, monkeypatch):
     """Each column-histogram variant at radii covering every carry-free group
     size G (8/4/2/1) and tail n mod G, ragged tiles (W not a multiple of the
