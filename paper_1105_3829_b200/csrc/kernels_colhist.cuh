@@ -341,6 +341,39 @@ __host__ __device__ constexpr int colhist4p_bytes(int T, int r, int PL) {
     return (CH4_RECS * ncp + ch4p_recs(PL) * (ncp / 2)) * 4;
 }
 
+// PL = 4: three pair levels and NO level-2 single records (see
+// k_colhist4p_u8): singles are level 0 (row 0), level 1 (rows 1-4) and
+// level 3 (rows 5-68); the one single column of a level-2 pair gather
+// derives its word from its four level-3 words.
+__host__ __device__ constexpr int ch4p_singles(int PL) { return PL == 4 ? 69 : CH4_RECS; }
+__host__ __device__ constexpr int ch4p_pair_levels(int PL) { return PL == 4 ? 3 : PL; }
+__host__ __device__ constexpr int colhist4q_bytes(int T, int r, int PL) {
+    const int ncp = colhist4p_ncolp(T, r);
+    return (ch4p_singles(PL) * ncp + ch4p_recs(ch4p_pair_levels(PL)) * (ncp / 2)) * 4;
+}
+
+// level-2 word of column c for record p2 from its four level-3 words (PL = 4)
+__device__ __forceinline__ uint32_t ch4_l2_from_l3(const uint32_t *rec, int NCP, int p2, int c) {
+    const uint32_t *q = rec + (5 + 4 * p2) * NCP + c;
+    return __dp4a(q[0], 0x01010101u, 0u) | (__dp4a(q[NCP], 0x01010101u, 0u) << 8) |
+           (__dp4a(q[2 * NCP], 0x01010101u, 0u) << 16) | (__dp4a(q[3 * NCP], 0x01010101u, 0u) << 24);
+}
+
+// record updates for the PL = 4 layout: byte read-modify-writes (builds)
+// and shared-memory atomics (row updates)
+__device__ __forceinline__ void ch4q_bump(uint8_t *recb, int NCOL, int c, unsigned v, int d) {
+    recb[(0 * NCOL + c) * 4 + (v >> 6)] += d;
+    recb[((1 + (v >> 6)) * NCOL + c) * 4 + ((v >> 4) & 3)] += d;
+    recb[((5 + (v >> 2)) * NCOL + c) * 4 + (v & 3)] += d;
+}
+__device__ __forceinline__ void ch4q_bump_upd(uint8_t *recb, int NCOL, int c, unsigned v, int d) {
+    uint32_t *rw = reinterpret_cast<uint32_t *>(recb);
+    const unsigned one = (unsigned)d;
+    atomicAdd(rw + (0 * NCOL + c), one << (8 * (v >> 6)));
+    atomicAdd(rw + ((1 + (v >> 6)) * NCOL + c), one << (8 * ((v >> 4) & 3)));
+    atomicAdd(rw + ((5 + (v >> 2)) * NCOL + c), one << (8 * (v & 3)));
+}
+
 // window of one level from pair records (np = (n-1)/2 pairs from kp) plus
 // the single column cs; GP pairs per carry-free group, runtime tail
 template <int GP>
@@ -419,23 +452,27 @@ __device__ __forceinline__ unsigned ch4_select_p(const uint32_t *rec, const uint
         return (unsigned)(p3 * 4 + d0);
     }
     constexpr int GP = G / 2;
+    constexpr bool DL2 = PL == 4;
+    constexpr int PLP = ch4p_pair_levels(PL), R3 = DL2 ? 5 : 21;
     const int kp = (tid + 1) >> 1, cs = (tid & 1) ? tid : tid + n - 1, np = (n - 1) >> 1;
     uint32_t w0, w1;
     ch4p_gather<GP>(prs, rec, kp, cs, np, w0, w1);
     const int d3 = ch4_descend(w0, w1, k);
-    if (PL >= 2)
+    if (PLP >= 2)
         ch4p_gather<GP>(prs + (1 + d3) * NPR, rec + (1 + d3) * NCP, kp, cs, np, w0, w1);
     else
         ch4_gather<G, M>(rec + (1 + d3) * NCP + tid, n, w0, w1);
     const int d2 = ch4_descend(w0, w1, k);
     const int p2 = d3 * 4 + d2;
-    if (PL >= 3)
+    if (DL2)
+        ch4p_gather_sv<GP>(prs + (5 + p2) * NPR, ch4_l2_from_l3(rec, NCP, p2, cs), kp, np, w0, w1);
+    else if (PLP >= 3)
         ch4p_gather<GP>(prs + (5 + p2) * NPR, rec + (5 + p2) * NCP, kp, cs, np, w0, w1);
     else
         ch4_gather<G, M>(rec + (5 + p2) * NCP + tid, n, w0, w1);
     const int d1 = ch4_descend(w0, w1, k);
     const int p3 = p2 * 4 + d1;
-    ch4_gather<G, M>(rec + (21 + p3) * NCP + tid, n, w0, w1);
+    ch4_gather<G, M>(rec + (R3 + p3) * NCP + tid, n, w0, w1);
     const int d0 = ch4_descend(w0, w1, k);
     return (unsigned)(p3 * 4 + d0);
 }
@@ -478,29 +515,37 @@ __device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uin
     const int r = p.radius, H = p.H, W = p.W;
     const int RS = PL > 0 ? NCP : ch4_stride(NCOL);  // record row stride
     const int NPR = RS / 2;
+    constexpr bool DL2 = PL == 4;  // no level-2 singles (ch4p_singles)
+    constexpr int PLP = ch4p_pair_levels(PL);
     uint8_t *recb = reinterpret_cast<uint8_t *>(rec);
     auto pbump = [&](int c, unsigned v, int d) {
         const int kk = c >> 1;
         const unsigned one = (unsigned)d;
         atomicAdd(prs + kk, one << (8 * (v >> 6)));
-        if (PL >= 2) atomicAdd(prs + (1 + (v >> 6)) * NPR + kk, one << (8 * ((v >> 4) & 3)));
-        if (PL >= 3) atomicAdd(prs + (5 + (v >> 4)) * NPR + kk, one << (8 * ((v >> 2) & 3)));
+        if (PLP >= 2) atomicAdd(prs + (1 + (v >> 6)) * NPR + kk, one << (8 * ((v >> 4) & 3)));
+        if (PLP >= 3) atomicAdd(prs + (5 + (v >> 4)) * NPR + kk, one << (8 * ((v >> 2) & 3)));
     };
     auto bump2 = [&](int c, unsigned vo, unsigned vi) {
         extra(c, vo, -1);
         extra(c, vi, 1);
         const int ko = key(vo), ki = key(vi);  // (ko == ki cancels: no data-dependent branch)
         if (ko >= 0) {
-            ch4_bump_upd(recb, RS, c, (unsigned)ko, -1);
+            if (DL2)
+                ch4q_bump_upd(recb, RS, c, (unsigned)ko, -1);
+            else
+                ch4_bump_upd(recb, RS, c, (unsigned)ko, -1);
             if (PL > 0) pbump(c, (unsigned)ko, -1);
         }
         if (ki >= 0) {
-            ch4_bump_upd(recb, RS, c, (unsigned)ki, 1);
+            if (DL2)
+                ch4q_bump_upd(recb, RS, c, (unsigned)ki, 1);
+            else
+                ch4_bump_upd(recb, RS, c, (unsigned)ki, 1);
             if (PL > 0) pbump(c, (unsigned)ki, 1);
         }
     };
     __syncthreads();  // previous users of rec are done
-    for (int i = tid; i < CH4_RECS * RS; i += T) rec[i] = 0;
+    for (int i = tid; i < ch4p_singles(PL) * RS; i += T) rec[i] = 0;
     __syncthreads();
     for (int c = tid; c < NCOL; c += T) {
         const int gx = clampi(X0 - r + c, 0, W - 1);
@@ -508,14 +553,22 @@ __device__ __forceinline__ void ch4_sweep(const SlabParams &p, const P *src, uin
             const unsigned v = src_row(p, src, clampi(ya + j, 0, H - 1))[gx];
             extra(c, v, 1);
             const int kv = key(v);
-            if (kv >= 0) ch4_bump(recb, RS, c, (unsigned)kv, 1);
+            if (kv >= 0) {
+                if (DL2)
+                    ch4q_bump(recb, RS, c, (unsigned)kv, 1);
+                else
+                    ch4_bump(recb, RS, c, (unsigned)kv, 1);
+            }
         }
     }
     __syncthreads();
     if (PL > 0) {
-        for (int i = tid; i < ch4p_recs(PL) * NPR; i += T) {
+        for (int i = tid; i < ch4p_recs(PLP) * NPR; i += T) {
             const int row = i / NPR, kk = i - row * NPR;
-            prs[i] = rec[row * RS + 2 * kk] + rec[row * RS + 2 * kk + 1];
+            if (DL2 && row >= 5)
+                prs[i] = ch4_l2_from_l3(rec, RS, row - 5, 2 * kk) + ch4_l2_from_l3(rec, RS, row - 5, 2 * kk + 1);
+            else
+                prs[i] = rec[row * RS + 2 * kk] + rec[row * RS + 2 * kk + 1];
         }
         __syncthreads();
     }
@@ -615,9 +668,9 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
     const int NCOL = T + 2 * r;
     const int NCP = PL > 0 ? colhist4p_ncolp(T, r) : ch4_stride(NCOL);  // record row stride
     const int NPR = NCP / 2;
-    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85][NCP]
-    uint32_t *prs = rec + CH4_RECS * NCP;                     // [PR][NPR] (PL > 0)
-    uint32_t *rec3 = prs + (PL > 0 ? ch4p_recs(PL) * NPR : 0);  // [NCP] below/equal/above H0 (WK)
+    uint32_t *rec = reinterpret_cast<uint32_t *>(smem_raw);  // [85 or 69][NCP] singles
+    uint32_t *prs = rec + ch4p_singles(PL) * NCP;             // [PR][NPR] (PL > 0)
+    uint32_t *rec3 = prs + (PL > 0 ? ch4p_recs(ch4p_pair_levels(PL)) * NPR : 0);  // [NCP] below/equal/above H0 (WK)
     int *hfirst = reinterpret_cast<int *>(rec3 + NCP);             // [256]
     int *hlast = hfirst + 256;                                      // [256]
     int *flags = hlast + 256;                                       // [0]: H0, [1]: any miss
@@ -963,11 +1016,6 @@ namespace mtb {
 // words (IDP4A each), which frees 64 B per stripe column: three pair levels
 // then fit two 256-thread CTAs per SM up to r = 32 (PL = 2 before), and a
 // row update is 12 shared-memory atomics instead of 14.
-__host__ __device__ constexpr int ch4p_singles(int PL) { return PL == 4 ? 69 : CH4_RECS; }
-__host__ __device__ constexpr int colhist4q_bytes(int T, int r, int PL) {
-    const int ncp = colhist4p_ncolp(T, r);
-    return (ch4p_singles(PL) * ncp + ch4p_recs(PL == 4 ? 3 : PL) * (ncp / 2)) * 4;
-}
 
 template <int T, int G, int M, int PL, bool STREAM, int NF = 0>
 __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {

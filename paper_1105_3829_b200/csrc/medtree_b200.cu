@@ -292,7 +292,11 @@ static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
         if (!rc) rc = run_colhist16_u16(p, B, s, 1);
         if (!rc) g_kernel = "k_colhist16c_u16|k_colhist16_u16 (device-selected)";
     } else if (!rc) {
-        rc = run_colhist16_u16(p, B, s, WK_FROM_SPREAD);  // window-keyed sweep on compact data
+        p.gate = GATE_WIDE;  // spread data: per-H phase-B sweeps
+        rc = run_colhist16_u16(p, B, s, 0);
+        p.gate = GATE_COMPACT;  // compact data: the window-keyed sweep
+        if (!rc) rc = run_colhist16_u16(p, B, s, 1);
+        if (!rc) g_kernel = "k_colhist16_u16 (device-selected)";
     }
     cudaFreeAsync(d_spread, s);
     return rc;

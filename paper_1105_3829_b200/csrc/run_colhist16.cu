@@ -23,13 +23,16 @@ int run_colhist16_u16(SlabParams p, int B, cudaStream_t s, int wk) {
         if (rc == NOT_COVERED) rc = run_colhist16_fixed_c(p, B, s, wk);
         if (rc != NOT_COVERED) return rc;
     }
-    const int pl = ch16_pair_levels(p.radius);
+    const int pl = ch16_pair_levels(p.radius, wk == 1);
     if (8 * n <= 255) {
         if (pl == 3) return run_colhist16_u16_g<256, 8, 3>(p, B, s, wk);
+        if (pl == 4) return run_colhist16_u16_g<256, 8, 4>(p, B, s, wk);
         if (pl == 2) return run_colhist16_u16_g<256, 8, 2>(p, B, s, wk);
         return run_colhist16_u16_g<256, 8, 0>(p, B, s, wk);
     }
-    if (4 * n <= 255) return pl >= 2 ? run_colhist16_u16_g<256, 4, 2>(p, B, s, wk) : run_colhist16_u16_g<256, 4, 0>(p, B, s, wk);
+    if (4 * n <= 255)
+        return pl == 4 ? run_colhist16_u16_g<256, 4, 4>(p, B, s, wk)
+                       : (pl >= 2 ? run_colhist16_u16_g<256, 4, 2>(p, B, s, wk) : run_colhist16_u16_g<256, 4, 0>(p, B, s, wk));
     if (2 * n <= 255) return run_colhist16_u16_g<256, 2, 0>(p, B, s, wk);
     return run_colhist16_u16_g<256, 1, 0>(p, B, s, wk);
 }

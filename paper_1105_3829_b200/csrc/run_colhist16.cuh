@@ -15,7 +15,7 @@ inline int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s, int wk) {
     // window-keyed first sweep (compact data); MTB_CH16_WK=0/1 forces
     wk = env_int("MTB_CH16_WK", wk);
     const int ncp = PL > 0 ? colhist4p_ncolp(T, p.radius) : ch4_stride(T + 2 * p.radius);
-    const size_t smem = (PL > 0 ? (size_t)colhist4p_bytes(T, p.radius, PL) : (size_t)colhist4_bytes(T, p.radius)) +
+    const size_t smem = (PL > 0 ? (size_t)colhist4q_bytes(T, p.radius, PL) : (size_t)colhist4_bytes(T, p.radius)) +
                         (size_t)ncp * 4 + (2 * 256 + 2) * sizeof(int);
     auto kern = k_colhist16_u16<T, G, M, PL, NF>;
     if (int rc = set_smem(kern, smem)) return rc;
@@ -42,10 +42,18 @@ inline int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s, int wk) {
 }
 
 // pair-record levels where two 256-thread CTAs per SM still fit (the
-// window-keyed sweep's per-column word and the H bookkeeping included)
-constexpr int ch16_pair_levels(int r) {
+// window-keyed sweep's per-column word and the H bookkeeping included).
+// allow4: three pair levels with derived level-2 singles (PL = 4) -- for
+// the window-keyed sweep on compact data (one or two sweeps per tile:
+// config 4 r = 31 3.84 -> 3.72 ms); on spread data the per-H phase-B
+// sweeps (~10 per tile) each re-derive the level-2 pairs, and PL = 2 stays
+// faster (config 3 r = 31 8.31 against 9.66 ms).
+constexpr int ch16_pair_levels(int r, bool allow4 = false) {
     const int lim = 113 * 1024 - (2 * 256 + 2) * (int)sizeof(int) - ch4_stride(256 + 2 * r) * 4;
-    return colhist4p_bytes(256, r, 3) <= lim ? 3 : (colhist4p_bytes(256, r, 2) <= lim ? 2 : 0);
+    return colhist4p_bytes(256, r, 3) <= lim                 ? 3
+           : (allow4 && colhist4q_bytes(256, r, 4) <= lim) ? 4
+           : colhist4p_bytes(256, r, 2) <= lim              ? 2
+                                                             : 0;
 }
 
 // compile-time window sides NLO..NHI (odd); NOT_COVERED when n is outside
@@ -59,8 +67,13 @@ inline int run_colhist16_fixed(SlabParams p, int B, cudaStream_t s, int wk) {
         if constexpr (NF == 0) {
             return NOT_COVERED;
         } else {
-            constexpr int G = carry_free_group(NF), pl = ch16_pair_levels(NF / 2);
+            constexpr int G = carry_free_group(NF);
+            constexpr int pl = ch16_pair_levels(NF / 2), pl4 = ch16_pair_levels(NF / 2, true);
             constexpr int PL = G == 8 ? pl : (G == 4 && pl >= 2 ? 2 : 0);
+            constexpr int PL4 = G == 8 ? pl4 : (G == 4 && pl4 >= 2 ? (pl4 == 4 ? 4 : 2) : 0);
+            if constexpr (PL4 != PL) {
+                if (wk == 1) return run_colhist16_u16_gm<256, G, NF % G, PL4, NF>(p, B, s, wk);
+            }
             return run_colhist16_u16_gm<256, G, NF % G, PL, NF>(p, B, s, wk);
         }
     });
