@@ -782,21 +782,24 @@ static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W
 // to release the destination buffer; its device->host copy waits for its
 // filter.  So frame i+1 arrives and frame i-1 leaves while frame i is being
 // filtered: the copy engines and the SMs stay busy across the sequence.
+// NB = one buffer pair per frame of the call, 3 to NBMAX, within a device
+// memory budget (round 1 kept 3: the ring's reuse waits then serialised the
+// config-2 sweep's six frames behind the copies of the frames 3 back).
 struct FramesCtx {
-    static constexpr int NB = 3;
+    static constexpr int NBMAX = 8;
     static constexpr int NFLAGS = 64;  // per slot: [0] rows arrived, [1..] output pixels per chunk
-    int dev = -1;
-    void *dsrc[NB] = {}, *ddst[NB] = {}, *dlut = nullptr;
-    unsigned int *dflags = nullptr;  // [NB][NFLAGS]
+    int dev = -1, nb = 0;
+    void *dsrc[NBMAX] = {}, *ddst[NBMAX] = {}, *dlut = nullptr;
+    unsigned int *dflags = nullptr;  // [NBMAX][NFLAGS]
     unsigned int *hstatus = nullptr, *dstatus = nullptr;  // mapped pinned word: a CTA timed out waiting for rows
     size_t cap = 0;
     cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
-    cudaEvent_t ein[NB], ek[NB], eout[NB];
+    cudaEvent_t ein[NBMAX], ek[NBMAX], eout[NBMAX];
 };
 static FramesCtx g_frames[64];
 static std::mutex g_frames_mu[64];
 
-static int frames_ctx(FramesCtx *&ctx, std::unique_lock<std::mutex> &lock, size_t bytes) {
+static int frames_ctx(FramesCtx *&ctx, std::unique_lock<std::mutex> &lock, size_t bytes, int want_nb) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) return fail(MTB_E_CUDA, "device index out of range");
@@ -810,10 +813,10 @@ static int frames_ctx(FramesCtx *&ctx, std::unique_lock<std::mutex> &lock, size_
         if (!rc) rc = ok(cudaStreamCreateWithFlags(&ctx->sc, cudaStreamNonBlocking), "cudaStreamCreate");
         if (!rc) rc = ok(cudaStreamCreateWithFlags(&ctx->sd, cudaStreamNonBlocking), "cudaStreamCreate");
         if (!rc) rc = ok(cudaMalloc(&ctx->dlut, 65536 * 2), "cudaMalloc");
-        if (!rc) rc = ok(cudaMalloc(&ctx->dflags, FramesCtx::NB * FramesCtx::NFLAGS * sizeof(unsigned int)), "cudaMalloc");
+        if (!rc) rc = ok(cudaMalloc(&ctx->dflags, FramesCtx::NBMAX * FramesCtx::NFLAGS * sizeof(unsigned int)), "cudaMalloc");
         if (!rc) rc = ok(cudaHostAlloc(&ctx->hstatus, sizeof(unsigned int), cudaHostAllocMapped), "cudaHostAlloc");
         if (!rc) rc = ok(cudaHostGetDevicePointer(&ctx->dstatus, ctx->hstatus, 0), "cudaHostGetDevicePointer");
-        for (int j = 0; j < FramesCtx::NB && !rc; ++j) {
+        for (int j = 0; j < FramesCtx::NBMAX && !rc; ++j) {
             rc = ok(cudaEventCreateWithFlags(&ctx->ein[j], cudaEventDisableTiming), "cudaEventCreate");
             if (!rc) rc = ok(cudaEventCreateWithFlags(&ctx->ek[j], cudaEventDisableTiming), "cudaEventCreate");
             if (!rc) rc = ok(cudaEventCreateWithFlags(&ctx->eout[j], cudaEventDisableTiming), "cudaEventCreate");
@@ -821,19 +824,28 @@ static int frames_ctx(FramesCtx *&ctx, std::unique_lock<std::mutex> &lock, size_
         if (rc) return rc;
         ctx->dev = dev;
     }
+    // buffer pairs: one per frame (3..NBMAX), at most 2 GiB of them
+    const size_t budget = 2ull << 30;
+    int nb = std::max(3, std::min(FramesCtx::NBMAX, want_nb));
+    while (nb > 3 && (size_t)nb * 2 * bytes > budget) --nb;
     if (ctx->cap < bytes) {
         cudaDeviceSynchronize();
-        for (int j = 0; j < FramesCtx::NB; ++j) {
+        for (int j = 0; j < FramesCtx::NBMAX; ++j) {
             if (ctx->dsrc[j]) cudaFree(ctx->dsrc[j]);
             if (ctx->ddst[j]) cudaFree(ctx->ddst[j]);
             ctx->dsrc[j] = ctx->ddst[j] = nullptr;
         }
-        ctx->cap = 0;
-        for (int j = 0; j < FramesCtx::NB; ++j) {
-            if (int rc = ok(cudaMalloc(&ctx->dsrc[j], bytes), "cudaMalloc")) return rc;
-            if (int rc = ok(cudaMalloc(&ctx->ddst[j], bytes), "cudaMalloc")) return rc;
-        }
         ctx->cap = bytes;
+        ctx->nb = 0;
+    }
+    for (int j = ctx->nb; j < nb; ++j) {
+        if (int rc = ok(cudaMalloc(&ctx->dsrc[j], ctx->cap), "cudaMalloc")) return j >= 3 ? (ctx->nb = j, MTB_OK) : rc;
+        if (int rc = ok(cudaMalloc(&ctx->ddst[j], ctx->cap), "cudaMalloc")) {
+            cudaFree(ctx->dsrc[j]);
+            ctx->dsrc[j] = nullptr;
+            return j >= 3 ? (ctx->nb = j, MTB_OK) : rc;
+        }
+        ctx->nb = j + 1;
     }
     return MTB_OK;
 }
@@ -844,7 +856,7 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
     const size_t bytes = (size_t)H * W * es;
     FramesCtx *ctx = nullptr;
     std::unique_lock<std::mutex> lock;
-    if (int rc = frames_ctx(ctx, lock, bytes)) return rc;
+    if (int rc = frames_ctx(ctx, lock, bytes, n)) return rc;
     auto ok = [](cudaError_t e, const char *what) {
         return e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
     };
@@ -855,7 +867,7 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
         rc = ok(cudaMemcpyAsync(ctx->dlut, lut, ((size_t)1 << bit_depth) * es, cudaMemcpyHostToDevice, ctx->sc),
                 "H2D lut");
     }
-    constexpr int NB = FramesCtx::NB;
+    const int NB = std::min(ctx->nb, std::max(3, n));  // buffer pairs this call rotates through
     // Streaming frames: a frame's rows arrive in chunks (CTAs wait on a row
     // counter) and its results leave in chunks (the copy-out stream waits on
     // per-chunk pixel counters), so the frame also overlaps its OWN copies.
