@@ -1042,12 +1042,15 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
     const int x = X0 + tid;
     // single-record updates (one atomic per level kept; the word is the
     // thread's own column, so there is no contention)
-    auto sbump = [&](int c, unsigned v, int d) {
+    auto sbump_upper = [&](int c, unsigned v, int d) {  // levels 1-3
         const unsigned one = (unsigned)d;
-        atomicAdd(rec + (0 * NCP + c), one << (8 * (v >> 6)));
         atomicAdd(rec + ((1 + (v >> 6)) * NCP + c), one << (8 * ((v >> 4) & 3)));
         if (!DL2) atomicAdd(rec + ((5 + (v >> 4)) * NCP + c), one << (8 * ((v >> 2) & 3)));
         atomicAdd(rec + ((R3 + (v >> 2)) * NCP + c), one << (8 * (v & 3)));
+    };
+    auto sbump = [&](int c, unsigned v, int d) {
+        atomicAdd(rec + (0 * NCP + c), (unsigned)d << (8 * (v >> 6)));
+        sbump_upper(c, v, d);
     };
 
     for (int i = tid; i < NS * NCP; i += T) rec[i] = 0;
@@ -1072,13 +1075,25 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         else
             prs[i] = rec[row * NCP + 2 * k] + rec[row * NCP + 2 * k + 1];
     }
-    // pair updates: levels 0-2 of value v, +-1 in the byte of the next digit
+    // pair updates: levels 1-2 of value v, +-1 in the byte of the next digit
     auto pbump = [&](int c, unsigned v, int d) {
         const int k = c >> 1;
         const unsigned one = (unsigned)d;  // +1 or 0xffffffff (-1)
-        atomicAdd(prs + 0 * NPR + k, one << (8 * (v >> 6)));
         if (PLP >= 2) atomicAdd(prs + (1 + (v >> 6)) * NPR + k, one << (8 * ((v >> 4) & 3)));
         if (PLP >= 3) atomicAdd(prs + (5 + (v >> 4)) * NPR + k, one << (8 * ((v >> 2) & 3)));
+    };
+    // one column's row step (vo leaves, vi enters).  Level 0 is one record
+    // per column (and per pair): its two changes go in as ONE atomic add of
+    // the combined delta -- exact in modular arithmetic, since every byte's
+    // final count is in [0, 255].
+    auto move = [&](int c, unsigned vo, unsigned vi) {
+        const unsigned d0 = (1u << (8 * (vi >> 6))) - (1u << (8 * (vo >> 6)));
+        atomicAdd(rec + c, d0);
+        atomicAdd(prs + (c >> 1), d0);
+        sbump_upper(c, vo, -1);
+        sbump_upper(c, vi, 1);
+        pbump(c, vo, -1);
+        pbump(c, vi, 1);
     };
     constexpr int CH_PF = 2;
     int gxs[CH_PF];
@@ -1103,12 +1118,7 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
 #pragma unroll
             for (int u = 0; u < CH_PF; ++u) {
                 const int c = tid + u * T;
-                if (c < NCOL) {  // (vo == vi cancels: no data-dependent branch)
-                    sbump(c, pvo[u], -1);
-                    sbump(c, pvi[u], 1);
-                    pbump(c, pvo[u], -1);
-                    pbump(c, pvi[u], 1);
-                }
+                if (c < NCOL) move(c, pvo[u], pvi[u]);  // (vo == vi cancels: no data-dependent branch)
             }
             if (NCOL > CH_PF * T) {
                 const uint8_t *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
@@ -1117,10 +1127,7 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
                     const int gx = clampi(X0 - r + c, 0, W - 1);
                     const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
                     if (vo == vi) continue;
-                    sbump(c, vo, -1);
-                    sbump(c, vi, 1);
-                    pbump(c, vo, -1);
-                    pbump(c, vi, 1);
+                    move(c, vo, vi);
                 }
             }
             if (y + 1 < y1) prefetch(y + 1);
