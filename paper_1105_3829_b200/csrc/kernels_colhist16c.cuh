@@ -128,20 +128,30 @@ __global__ void __launch_bounds__(T) k_colhist16c_u16(SlabParams p) {
         const int row = i / NPR, k = i - row * NPR;
         prs[i] = rec[row * NCP + 2 * k] + rec[row * NCP + 2 * k + 1];
     }
-    auto pbump = [&](int c, unsigned v, int d) {
+    auto pbump_upper = [&](int c, unsigned v, int d) {  // pair levels 1-2
         const int k = c >> 1;
         const unsigned one = (unsigned)d;
-        atomicAdd(prs + 0 * NPR + k, one << (8 * (v >> 6)));
         if (PL >= 2) atomicAdd(prs + (1 + (v >> 6)) * NPR + k, one << (8 * ((v >> 4) & 3)));
         if (PL >= 3) atomicAdd(prs + (5 + (v >> 4)) * NPR + k, one << (8 * ((v >> 2) & 3)));
     };
     // one column's row step: records of the high bytes (the -1 and +1 cancel
     // when they agree: no data-dependent branch), then the sorted span
     auto col_step = [&](int c, unsigned vo, unsigned vi) {
-        ch4_bump_upd(recb, NCP, c, vo >> 8, -1);
-        ch4_bump_upd(recb, NCP, c, vi >> 8, 1);
-        pbump(c, vo >> 8, -1);
-        pbump(c, vi >> 8, 1);
+        // level 0 (one record per column and per pair): one combined atomic
+        // each; levels 1-3 one per value
+        const unsigned ho = vo >> 8, hi = vi >> 8;
+        const unsigned d0 = (1u << (8 * (hi >> 6))) - (1u << (8 * (ho >> 6)));
+        atomicAdd(rec + c, d0);
+        atomicAdd(prs + (c >> 1), d0);
+        uint32_t *rw = rec;
+        atomicAdd(rw + ((1 + (ho >> 6)) * NCP + c), 0xffffffffu << (8 * ((ho >> 4) & 3)));
+        atomicAdd(rw + ((1 + (hi >> 6)) * NCP + c), 1u << (8 * ((hi >> 4) & 3)));
+        atomicAdd(rw + ((5 + (ho >> 4)) * NCP + c), 0xffffffffu << (8 * ((ho >> 2) & 3)));
+        atomicAdd(rw + ((5 + (hi >> 4)) * NCP + c), 1u << (8 * ((hi >> 2) & 3)));
+        atomicAdd(rw + ((21 + (ho >> 2)) * NCP + c), 0xffffffffu << (8 * (ho & 3)));
+        atomicAdd(rw + ((21 + (hi >> 2)) * NCP + c), 1u << (8 * (hi & 3)));
+        pbump_upper(c, ho, -1);
+        pbump_upper(c, hi, 1);
         if (vo == vi) return;
         uint16_t *a = scol + c * n;
         const uint16_t *const aa[2] = {a, a};
