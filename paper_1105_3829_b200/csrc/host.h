@@ -18,7 +18,7 @@ extern std::atomic<uint64_t> g_launches;
 
 int fail(int code, const std::string &msg);
 int sm_count();
-int rows_per_cta(const SlabParams &p, int blocks_x, int B, int ctas_per_sm);
+int rows_per_cta(const SlabParams &p, int blocks_x, int B, int ctas_per_sm, int waves = 2);
 int env_int(const char *name, int dflt);
 const char *forced_kernel();
 void keep_pool_memory();

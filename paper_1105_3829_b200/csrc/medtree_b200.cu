@@ -102,9 +102,9 @@ static int validate(const SlabParams &p, int B) {
     return MTB_OK;
 }
 
-int rows_per_cta(const SlabParams &p, int blocks_x, int B, int ctas_per_sm) {
+int rows_per_cta(const SlabParams &p, int blocks_x, int B, int ctas_per_sm, int waves) {
     const int rows = p.row_end - p.row_begin;
-    const int64_t target = (int64_t)sm_count() * ctas_per_sm * 2;  // two waves
+    const int64_t target = (int64_t)sm_count() * ctas_per_sm * waves;
     int64_t slabs = (target + (int64_t)blocks_x * B - 1) / ((int64_t)blocks_x * B);
     if (slabs < 1) slabs = 1;
     int rpc = (int)((rows + slabs - 1) / slabs);

@@ -23,7 +23,10 @@ inline int run_colhist16_u16_gm(SlabParams p, int B, cudaStream_t s, int wk) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
     if (per_sm < 1) per_sm = 1;
     const int bx = (p.W + T - 1) / T;
-    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm);
+    // four waves of shorter slabs: the tiles' phase-B / window-keyed work
+    // varies with the data, and shorter slabs balance it (config 4 r = 15
+    // 2.53 -> 1.92 ms, r = 31 3.73 -> 2.83; config 3 r = 31 8.3 -> 6.8)
+    p.rows_per_cta = rows_per_cta(p, bx, B, per_sm, 4);
     dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
     // per-pixel high-byte plane (stream-ordered pool allocation, kept cached)
     uint8_t *hplane = nullptr;

@@ -27,7 +27,7 @@ static int run_colhist16c_gm(SlabParams p, int B, cudaStream_t s) {
     // data from CTA to CTA, and short slabs even it out -- config 3 r = 15
     // 3.17 -> 2.66 ms, r = 7 1.72 -> 1.46 ms against two waves of ~150-row
     // slabs, despite the extra span builds
-    p.rows_per_cta = std::max(rows_per_cta(p, bx, B, per_sm) / 8, std::min(2 * n, p.row_end - p.row_begin));
+    p.rows_per_cta = std::max(rows_per_cta(p, bx, B, per_sm, 16), std::min(2 * n, p.row_end - p.row_begin));
     dim3 grid(bx, (p.row_end - p.row_begin + p.rows_per_cta - 1) / p.rows_per_cta, B);
     return launch(kern, grid, T, smem, s, p, "k_colhist16c_u16");
 }
