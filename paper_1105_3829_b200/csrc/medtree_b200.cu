@@ -269,7 +269,7 @@ static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
     if (force == "colhist") return run_colhist16_u16(p, B, s, 1);
     if (force == "colhist16s") return run_colhist16s_u16(p, B, s);
     if (force == "colhist16c") return run_colhist16c_u16(p, B, s);
-    const bool small_r = p.radius <= env_int("MTB_U16C_MAX_R", 16);
+    const bool small_r = p.radius <= env_int("MTB_U16C_MAX_R", 23);
     if (g_spread_hint >= 0) {
         const bool wide = g_spread_hint > SPREAD_WIDE;
         if (wide && small_r) return run_colhist16c_u16(p, B, s);

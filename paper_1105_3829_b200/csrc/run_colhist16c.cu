@@ -51,8 +51,8 @@ static int run_colhist16c_pl(SlabParams p, int B, cudaStream_t s) {
 int run_colhist16c_u16(SlabParams p, int B, cudaStream_t s) {
     const int n = 2 * p.radius + 1;
     if (n > 127) return run_colhist16_u16(p, B, s, 0);
-    if (n >= 5 && n <= 33) {  // compile-time window side for the radii this kernel serves (r <= 16)
-        return with_fixed_n<5, 33>(n, [&](auto nf) {
+    if (n >= 5 && n <= 47) {  // compile-time window side for the radii this kernel serves (r <= 23)
+        return with_fixed_n<5, 47>(n, [&](auto nf) {
             constexpr int NF = decltype(nf)::value, G = carry_free_group(NF);
             constexpr int PL = ch16c_pair_levels(CH16C_T, NF / 2, CH16C_CMAX);
             return run_colhist16c_gm<G, NF % G, PL, NF>(p, B, s);
