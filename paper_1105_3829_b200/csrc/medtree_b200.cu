@@ -322,6 +322,7 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     const bool median = (uint32_t)((n * n + 1) / 2) == p.rank;
     if (median && n <= 7 && (force.empty() || force == "sortnet" || force == "med3" || force == "mednet"))
         return run_sortnet<P>(p, B, s);
+    if (sizeof(P) == 1 && n <= 255 && p.radius >= 1 && force == "bandmma") return run_bandmma_u8(p, B, s);
     if (sizeof(P) == 1 && n <= 255 && (force == "colhist" || (force.empty() && p.radius <= 48)))
         return run_colhist_u8(p, B, s);
     if (sizeof(P) == 1 && !wide && (force == "ctmf" || force.empty())) return run_ctmf_u8(p, B, s);
