@@ -21,32 +21,33 @@
 // and k-tile.  No O(n) gathers per pixel on the CUDA cores, no prefix scans,
 // no sliding windows: the gather is the tensor core's k-loop.
 //
-// Keyed windows.  A warp resolves 32 output pixels (two groups of 16, 32
-// columns apart so that they share k-tiles) with ONE product over 8*NT planes:
-// the cumulative plane cum[B] ("below 16 B") and the 8*NT-1 value planes
-// 16B .. 16B+8NT-2.  B is predicted from the same pixels' results one row up
-// (the median of a large window moves slowly: on the benchmark frame the
-// prediction misses 0.05% of the time at r = 63 with NT = 4 and 0.5% at
-// r = 31 with NT = 6).  A pixel whose rank falls outside the keyed window
-// is a miss: the warp then takes the coarse bin of every unresolved pixel from
-// the 16 cumulative planes (one product) and repeats the keyed product from
-// the lowest one, until every pixel is resolved -- exact for any image, the
-// prediction only decides the speed.  The accumulator fragments are
-// transposed through a per-warp buffer so that each lane descends one pixel's
-// packed u16 counts (the reference's extract_u, 16-ary).
+// Keyed windows.  A warp resolves 16 adjacent output pixels with ONE product
+// over 32 planes: the cumulative plane cum[B] ("below 16 B") and the 31 value
+// planes 16B .. 16B+30.  B is predicted from the same pixels' results one row
+// up (the median of a large window moves slowly: on the benchmark frame the
+// prediction misses 0.3% of the time at r = 31 and never at r = 63).  A pixel
+// whose rank falls outside the keyed window is a miss: the warp then takes
+// the coarse bin of every unresolved pixel from the 16 cumulative planes (one
+// product) and repeats the keyed product from the lowest one, until every
+// pixel is resolved -- exact for any image, the prediction only decides the
+// speed.  The accumulator fragments are transposed through a per-warp buffer
+// so that a pair of lanes descends one pixel's 32 packed u16 counts, 16 bins
+// each (the reference's extract_u, 16-ary).
 //
 // All arithmetic is exact integer counting; window counts fit u16 because
 // n^2 <= 65535 is required (r <= 127).
 #pragma once
+#include <cstdio>
 #include "common.cuh"
 
 namespace mtb {
 
 constexpr int BM_PLANES = 272;  // 16 cumulative coarse planes, then one plane per value
-constexpr int BM_MAXT = 512;    // threads per CTA (128 registers per thread)
-constexpr int BM_TPITCH = 34;   // 16-byte units between the rows of a transpose buffer
+constexpr int BM_MAXT = 1024;   // threads per CTA: one warp per 16 output columns
+constexpr int BM_REC = 80;      // bytes between pixel records of a transpose buffer (64 used)
+constexpr int BM_TBUF = 16 * BM_REC;
 
-// stripe geometry for a radius: TW output columns (multiple of 64), NP plane
+// stripe geometry for a radius: TW output columns (multiple of 16), NP plane
 // pitch in bytes (>= halo'd columns and the last k-tile a warp reads; NP mod
 // 64 == 32 keeps the four plane rows of a half-warp's B-fragment load in
 // distinct bank groups)
@@ -56,10 +57,9 @@ __host__ __device__ constexpr int bm_pitch(int TW, int r) {
     const int need = a > b ? a : b;
     return ((need + 31) / 64) * 64 + 32;  // smallest value >= need with value mod 64 == 32
 }
-__host__ __device__ constexpr int bm_tbuf_bytes(int NT) { return NT * BM_TPITCH * 16; }
-__host__ __device__ constexpr size_t bm_smem(int TW, int r, int warps, int NT) {
+__host__ __device__ constexpr size_t bm_smem(int TW, int r) {
     // planes | per-warp transpose buffers
-    return (size_t)BM_PLANES * bm_pitch(TW, r) + (size_t)warps * bm_tbuf_bytes(NT);
+    return (size_t)BM_PLANES * bm_pitch(TW, r) + (size_t)(TW / 16) * BM_TBUF;
 }
 
 __device__ __forceinline__ void bm_mma(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -80,8 +80,8 @@ __device__ __forceinline__ uint32_t bm_mask4(int col0, int m, int r2) {
 __device__ __forceinline__ uint32_t bm_hsum16(uint32_t w) { return (w * 0x10001u) >> 16; }
 
 // smallest bin b with cumsum(bins[0..b]) >= k (16 u16 bins packed in w[0..7],
-// bins 2i | 2i+1 << 16; the caller guarantees sum >= k); leaves in k the rank
-// within bin b
+// bins 2i | 2i+1 << 16); leaves in k the rank within bin b.  If the 16 bins
+// hold fewer than k, the result is bin 15 with k above that bin's count.
 __device__ __forceinline__ int bm_descend(const uint32_t (&w)[8], uint32_t &k) {
     uint32_t s = bm_hsum16(w[0] + w[1] + w[2] + w[3]);
     const bool r1 = s < k;
@@ -102,94 +102,55 @@ __device__ __forceinline__ int bm_descend(const uint32_t (&w)[8], uint32_t &k) {
     return (r1 ? 8 : 0) | (r2 ? 4 : 0) | (r3 ? 2 : 0) | (r4 ? 1 : 0);
 }
 
-// One product: 8*NTL planes for the two groups of 16 pixels whose windows
-// start at stripe columns xa and xa + 32.  Plane of bin i: row(i).  Results
-// transposed through tb: lane l gets pixel (l >> 4) * 32 + (l & 15) of the
-// pair as 8*NTL u16 counts packed in w[0 .. 4*NTL) (bins 2i | 2i+1 << 16).
+// One product: 8*NTL planes (plane of bin i: row(i)) for the 16 pixels whose
+// windows start at stripe columns xa .. xa+15.  n-tile t holds bins 8t..8t+7
+// and lane (g, q)'s B-fragment column is bin 8t+g: the four plane rows a
+// half-warp reads are consecutive, so with the pitch = 32 (mod 64) they sit
+// in distinct bank groups.  After the k-loop lane (g, q) holds bins 8t+2q and
+// 8t+2q+1 of pixels g and g+8: record word 4t+q (bins 2i | 2i+1 << 16 in word
+// i) of the two pixels' records in tb.
 template <int NK, int NTL, typename RowOf>
 __device__ __forceinline__ void bm_product(const uint8_t *planes, int NP, int xa, int lane,
-                                           const uint32_t (&af)[3][4], unsigned char *tb, RowOf row,
-                                           uint32_t (&w)[4 * NTL], int dbg = 0) {
+                                           const uint32_t (&af)[3][4], unsigned char *tb, RowOf row) {
     const int g = lane >> 2, q = lane & 3;
-    int acc[2][NTL][4];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int t = 0; t < NTL; ++t)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc[a][t][i] = 0;
     const uint32_t ones[4] = {0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u};
+    __syncwarp();  // the previous product's records have been read
 #pragma unroll
     for (int t = 0; t < NTL; ++t) {
-        // n-tile t holds bins 8t .. 8t+7, this lane's B-fragment column is bin
-        // 8t + g: the four plane rows a half-warp reads are consecutive, so with
-        // the pitch = 32 (mod 64) they sit in distinct bank groups
         const uint8_t *rp = planes + (size_t)row(8 * t + g) * NP + xa + 8 * q;
+        int acc[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int j = 0; j <= NK; ++j) {
-            const uint2 b = *reinterpret_cast<const uint2 *>(rp + 32 * j);
-#pragma unroll
-            for (int a = 0; a < 2; ++a) {
-                const int kt = j - a;  // group a's k-tile held by this load
-                if (kt < 0 || kt >= NK) continue;
-                if (kt == 0)
-                    bm_mma(acc[a][t], af[0], b.x, b.y);
-                else if (kt == NK - 1)
-                    bm_mma(acc[a][t], af[2], b.x, b.y);
-                else if (kt == NK - 2)
-                    bm_mma(acc[a][t], af[1], b.x, b.y);
-                else
-                    bm_mma(acc[a][t], ones, b.x, b.y);
-            }
+        for (int kt = 0; kt < NK; ++kt) {
+            const uint2 b = *reinterpret_cast<const uint2 *>(rp + 32 * kt);
+            if (kt == 0)
+                bm_mma(acc, af[0], b.x, b.y);
+            else if (kt == NK - 1)
+                bm_mma(acc, af[2], b.x, b.y);
+            else if (kt == NK - 2)
+                bm_mma(acc, af[1], b.x, b.y);
+            else
+                bm_mma(acc, ones, b.x, b.y);
         }
-    }
-    // lane (g, q) holds, per n-tile t, bins 8t+2q and 8t+2q+1 of pixels g (regs
-    // 0, 1) and g + 8 (regs 2, 3) of each group.  It writes its NTL packed words
-    // as 8-byte half-units q NTL/2 .. of the pixel's record (record word
-    // q NTL + t = bins 8t+2q | 8t+2q+1); half-unit h of pixel p lives at
-    // ((h >> 1) * PITCH + p) * 16 + (h & 1) * 8
-    __syncwarp();
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-#pragma unroll
-        for (int hh = 0; hh < NTL / 2; ++hh) {
-            const int h = q * (NTL / 2) + hh;
-            unsigned char *dst = tb + ((h >> 1) * BM_TPITCH) * 16 + (h & 1) * 8;
-            const uint2 lo = make_uint2(__byte_perm(acc[a][2 * hh][0], acc[a][2 * hh][1], 0x5410),
-                                        __byte_perm(acc[a][2 * hh + 1][0], acc[a][2 * hh + 1][1], 0x5410));
-            const uint2 hi = make_uint2(__byte_perm(acc[a][2 * hh][2], acc[a][2 * hh][3], 0x5410),
-                                        __byte_perm(acc[a][2 * hh + 1][2], acc[a][2 * hh + 1][3], 0x5410));
-            *reinterpret_cast<uint2 *>(dst + (16 * a + g) * 16) = lo;
-            *reinterpret_cast<uint2 *>(dst + (16 * a + g + 8) * 16) = hi;
-        }
+        *reinterpret_cast<uint32_t *>(tb + g * BM_REC + (4 * t + q) * 4) = __byte_perm(acc[0], acc[1], 0x5410);
+        *reinterpret_cast<uint32_t *>(tb + (g + 8) * BM_REC + (4 * t + q) * 4) = __byte_perm(acc[2], acc[3], 0x5410);
     }
     __syncwarp();
-    // record word qq NTL + t -> w[4t + qq] (bins 2i | 2i+1 << 16 in w[i])
-    uint32_t rec[4 * NTL];
-#pragma unroll
-    for (int u = 0; u < NTL; ++u) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(tb + (u * BM_TPITCH + lane) * 16);
-        rec[4 * u] = v.x; rec[4 * u + 1] = v.y; rec[4 * u + 2] = v.z; rec[4 * u + 3] = v.w;
-    }
-#pragma unroll
-    for (int t = 0; t < NTL; ++t)
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) w[4 * t + qq] = rec[qq * NTL + t];
 }
 
-// NK: k-tiles per group of 16 pixels; NT: n-tiles of the keyed window (8 NT
-// planes: cum[B] and 8 NT - 1 values).  Block = 32 * warps threads; grid =
-// (stripes, row slabs, images).
-template <int NK, int NT, bool STREAM>
+// NK: k-tiles of a group of 16 pixels.  Block = 32 * (TW / 16) threads (one
+// warp per 16 output columns); grid = (stripes, row slabs, images).
+template <int NK, bool STREAM>
 __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW) {
-    static_assert(NT == 4 || NT == 6, "keyed window of 32 or 48 planes");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NTH = blockDim.x;
     const int r = p.radius, r2 = 2 * r, H = p.H, W = p.W;
     const int NC = TW + r2, NP = bm_pitch(TW, r), NPW = NP >> 2;
     uint8_t *planes = smem_raw;
     uint32_t *planew = reinterpret_cast<uint32_t *>(smem_raw);
-    unsigned char *tb = smem_raw + (size_t)BM_PLANES * NP + (size_t)warp * bm_tbuf_bytes(NT);
+    unsigned char *tb = smem_raw + (size_t)BM_PLANES * NP + (size_t)warp * BM_TBUF;
+#ifdef BM_TIMING
+    const long long tstart = clock64();
+#endif
     const int X0 = blockIdx.x * TW;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
     if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
@@ -249,30 +210,22 @@ __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW)
         af[s][3] = bm_mask4(c0 + 4, g + 8, r2);
     }
 
-    // ---- row updates: slot s = tid + u NTH, leaving / entering pixels a row
-    // ahead; running row pointers (a clamped row index repeats the edge row)
-    constexpr int PF = 2;
-    uint32_t *pw[PF];       // plane word of the slot (row 0), nullptr: no slot
-    uint32_t pone[PF];
-    const uint8_t *pin[PF];  // the slot's column in source row 0 of this image
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-        const int s = tid + u * NTH;
-        const int bl = s / nwords, wd = s - bl * nwords, c = 4 * wd + bl;
-        pw[u] = (s < nslots && c < NC) ? planew + wd : nullptr;
-        pin[u] = src_row(p, src, p.src_row0) + clampi(X0 - r + min(c, NC - 1), 0, W - 1);
-        pone[u] = 1u << (8 * (bl & 3));
+    // ---- row updates: one slot per thread (more: a loop), leaving / entering
+    // pixels loaded a row ahead
+    uint32_t *pw = nullptr;  // plane word of the slot (row 0), nullptr: no slot
+    uint32_t pone = 0;
+    const uint8_t *pin = src;  // the slot's column in source row 0 of this image
+    {
+        const int bl = tid / nwords, wd = tid - bl * nwords, c = 4 * wd + bl;
+        if (tid < nslots && c < NC) pw = planew + wd;
+        pin = src_row(p, src, p.src_row0) + clampi(X0 - r + min(c, NC - 1), 0, W - 1);
+        pone = 1u << (8 * (bl & 3));
     }
-    unsigned pvo[PF], pvi[PF];
+    unsigned pvo = 0, pvi = 0;
     auto prefetch = [&](int yn) {
-        const int64_t oo = (int64_t)(clampi(yn - r - 1, 0, H - 1) - p.src_row0) * p.src_pitch;
-        const int64_t oi = (int64_t)(clampi(yn + r, 0, H - 1) - p.src_row0) * p.src_pitch;
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-            if (pw[u]) {
-                pvo[u] = __ldg(pin[u] + oo);
-                pvi[u] = __ldg(pin[u] + oi);
-            }
+        if (pw) {
+            pvo = __ldg(pin + (int64_t)(clampi(yn - r - 1, 0, H - 1) - p.src_row0) * p.src_pitch);
+            pvi = __ldg(pin + (int64_t)(clampi(yn + r, 0, H - 1) - p.src_row0) * p.src_pitch);
         }
     };
     auto move = [&](uint32_t *wp, uint32_t one, unsigned vo, unsigned vi) {
@@ -285,26 +238,27 @@ __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW)
         for (int j = min(a, b) + 1; j <= max(a, b); ++j) atomicAdd(wp + j * NPW, d);
     };
 
-    // ---- the warp's 32 output pixels (one pair of groups per warp: the
-    // launcher starts TW / 32 warps)
-    const int xa = 64 * (warp >> 1) + 16 * (warp & 1);    // first pixel of group 0; group 1 at xa + 32
-    const int xl = xa + 32 * (lane >> 4) + (lane & 15);   // this lane's pixel (stripe-relative)
-    const bool valid = X0 + xl < W;
-    const bool live = X0 + xa < W;                         // (warp-uniform) something of the pair is in the image
-    uint8_t *dpx = dst + (int64_t)(y0 - p.row_begin) * p.dst_pitch + X0 + xl;
+    // ---- the warp's 16 output pixels; lanes l and l + 16 share pixel l & 15:
+    // each descends one half (16 bins) of the pixel's record
+    const int xa = 16 * warp;                 // first pixel (stripe-relative) = first window column
+    const int px = lane & 15, half = lane >> 4;
+    const bool valid = X0 + xa + px < W;
+    const bool live = X0 + xa < W;            // (warp-uniform) some pixel of the warp is in the image
+    const unsigned char *myrec = tb + px * BM_REC + half * 32;
+    uint8_t *dpx = dst + (int64_t)(y0 - p.row_begin) * p.dst_pitch + X0 + xa + px;
     int Bp = 0xff;  // predicted window base (coarse bin); 0xff: none yet
     const uint32_t rank = p.rank;
-    const int dbg = p.gate;
 
+#ifdef BM_TIMING
+    long long tA = 0, tB1 = 0, tB = 0, tB2 = 0, t0 = clock64(), tinit = t0 - tstart;
+#endif
     for (int y = y0; y < y1; ++y, dpx += p.dst_pitch) {
-        if (y > y0 && !(dbg & 2)) {
-#pragma unroll
-            for (int u = 0; u < PF; ++u)
-                if (pw[u]) move(pw[u], pone[u], pvo[u], pvi[u]);
-            if (nslots > PF * NTH) {
+        if (y > y0) {
+            if (pw) move(pw, pone, pvo, pvi);
+            if (nslots > NTH) {
                 const uint8_t *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
                 const uint8_t *ri = src_row(p, src, clampi(y + r, 0, H - 1));
-                for (int s = tid + PF * NTH; s < nslots; s += NTH) {
+                for (int s = tid + NTH; s < nslots; s += NTH) {
                     const int bl = s / nwords, wd = s - bl * nwords, c = 4 * wd + bl;
                     if (c >= NC) continue;
                     const int gx = clampi(X0 - r + c, 0, W - 1);
@@ -313,16 +267,24 @@ __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW)
             }
         }
         if (y + 1 < y1) prefetch(y + 1);
+#ifdef BM_TIMING
+        { const long long t = clock64(); tA += t - t0; t0 = t; }
+#endif
         __syncthreads();
-        if (live && !(dbg & 4)) {
+#ifdef BM_TIMING
+        { const long long t = clock64(); tB1 += t - t0; t0 = t; }
+#endif
+        if (live) {
             int B = Bp;
-            uint32_t open = 0xffffffffu;  // lanes not yet resolved
+            uint32_t open = 0xffffffffu;  // lanes whose pixel is not yet resolved
             unsigned val = 0;
             for (int pass = 0;; ++pass) {
                 if (pass > 0 || B == 0xff) {
                     // coarse bin of every open pixel from the 16 cumulative planes
-                    uint32_t cw[8];
-                    bm_product<NK, 2>(planes, NP, xa, lane, af, tb, [](int bin) { return bin; }, cw);
+                    bm_product<NK, 2>(planes, NP, xa, lane, af, tb, [](int bin) { return bin; });
+                    const uint4 u = *reinterpret_cast<const uint4 *>(tb + px * BM_REC);
+                    const uint4 v = *reinterpret_cast<const uint4 *>(tb + px * BM_REC + 16);
+                    const uint32_t cw[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
                     int cb = 0;  // number of j in 1..15 with cum[j] < rank = the coarse bin
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
@@ -333,51 +295,47 @@ __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW)
                     B = __reduce_min_sync(0xffffffffu, (((open >> lane) & 1u) && valid) ? cb : 255);
                     if (B == 255) break;  // only lanes past the edge were open
                 }
-                uint32_t w[4 * NT];
-                bm_product<NK, NT>(planes, NP, xa, lane, af, tb,
-                                   [B](int bin) {
-                                       const int v = 16 * B + bin - 1;  // value plane; bin 0: cum[B]
-                                       return bin == 0 ? B : (v <= 255 ? 16 + v : 0);  // past 255: the zero plane
-                                   },
-                                   w, dbg);
-                // chunk of 16 bins holding the rank, then the 16-ary descent;
-                // a rank above the window's total ends in the last bin with
-                // more left than the bin holds
-                uint32_t k = rank;
-                uint32_t c8[8];
-                int base;
-                const uint32_t s0 = bm_hsum16(w[0] + w[1] + w[2] + w[3] + w[4] + w[5] + w[6] + w[7]);
-                const bool p1 = s0 < k;
-                if constexpr (NT == 4) {
-                    k -= p1 ? s0 : 0u;
-                    base = p1 ? 16 : 0;
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) c8[i] = p1 ? w[8 + i] : w[i];
-                } else {
-                    const uint32_t s1 = bm_hsum16(w[8] + w[9] + w[10] + w[11] + w[12] + w[13] + w[14] + w[15]);
-                    const bool p2 = s0 + s1 < k;
-                    k -= p2 ? s0 + s1 : (p1 ? s0 : 0u);
-                    base = p2 ? 32 : (p1 ? 16 : 0);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) c8[i] = p2 ? w[(16 + i) % (4 * NT)] : (p1 ? w[8 + i] : w[i]);
-                }
-                int b16 = 1;
-                if (!(dbg & 8)) b16 = bm_descend(c8, k); else k = 0;
-                const uint32_t cl = c8[7] >> 16;  // count of a chunk's last bin
-                const int bin = base + b16;
-                // bin 0 is "below the window": a miss, like a rank above the window's total
-                const bool hit = bin > 0 && !(b16 == 15 && k > cl);
-                if (hit && ((open >> lane) & 1u)) val = (unsigned)(16 * B + bin - 1);
+                bm_product<NK, 4>(planes, NP, xa, lane, af, tb, [B](int bin) {
+                    const int v = 16 * B + bin - 1;  // value plane; bin 0: cum[B]
+                    return bin == 0 ? B : (v <= 255 ? 16 + v : 0);  // past 255: the zero plane
+                });
+                // this lane's 16 bins: 0..15 (half 0, bin 0 = below the window) or 16..31
+                const uint4 u = *reinterpret_cast<const uint4 *>(myrec);
+                const uint4 v = *reinterpret_cast<const uint4 *>(myrec + 16);
+                const uint32_t c8[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
+                const uint32_t mine = bm_hsum16(c8[0] + c8[1] + c8[2] + c8[3] + c8[4] + c8[5] + c8[6] + c8[7]);
+                const uint32_t other = __shfl_xor_sync(0xffffffffu, mine, 16);
+                // rank within this half; the upper half only counts when the lower holds fewer than rank
+                uint32_t k = half ? rank - min(other, rank) : rank;
+                const bool here = half ? (other < rank && k <= mine) : (rank <= mine);
+                const int b16 = bm_descend(c8, k);
+                const int bin = 16 * half + b16;
+                // (bin 0 is "below the window": a miss, like a rank above the window's total)
+                const unsigned cand = (here && bin > 0) ? (unsigned)(16 * B + bin - 1) : 0xffffu;
+                const unsigned both = min(cand, __shfl_xor_sync(0xffffffffu, cand, 16));  // the pair's result
+                const bool hit = both != 0xffffu;
+                if (hit && ((open >> lane) & 1u)) val = both;
                 open &= ~__ballot_sync(0xffffffffu, hit || !valid);
                 if (!open) break;
             }
-            // prediction for the next row: the lowest result of the pair, one below for drift
+            // prediction for the next row: the lowest result of the warp, one below for drift
             const int lo = __reduce_min_sync(0xffffffffu, valid ? (int)val : 255);
-            Bp = max(lo - 1, 0) >> 4;
-            if (valid) *dpx = lut ? __ldg(lut + val) : (uint8_t)val;
+            Bp = min(max(lo - 1, 0) >> 4, 15);
+            if (valid && half == 0) *dpx = lut ? __ldg(lut + val) : (uint8_t)val;
         }
+#ifdef BM_TIMING
+        { const long long t = clock64(); tB += t - t0; t0 = t; }
+#endif
         __syncthreads();
+#ifdef BM_TIMING
+        { const long long t = clock64(); tB2 += t - t0; t0 = t; }
+#endif
     }
+#ifdef BM_TIMING
+    if ((p.gate & 32) && lane == 0 && (warp == 0 || warp == 17) && blockIdx.x == 3 && blockIdx.y == 5)
+        printf("warp %d rows %d: init %lld, A %lld, bar1 %lld, B %lld, bar2 %lld (cycles per row: A %lld bar1 %lld B %lld bar2 %lld)\n",
+               warp, y1 - y0, tinit, tA, tB1, tB, tB2, tA / (y1 - y0), tB1 / (y1 - y0), tB / (y1 - y0), tB2 / (y1 - y0));
+#endif
     if (STREAM) stream_signal(p, y0, y1, X0, X0 + TW);
 }
 

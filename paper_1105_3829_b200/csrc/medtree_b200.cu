@@ -302,6 +302,10 @@ static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
     return rc;
 }
 
+// smallest radius sent to k_bandmma_u8 (config 2: 0.51 ms at r = 31 against 0.50 for the pair
+// records, 0.47 against 0.71 at r = 40)
+constexpr int BANDMMA_MIN_R = 32;
+
 template <typename P>
 static int run(SlabParams p, int B, cudaStream_t s) {
     int rc = validate(p, B);
@@ -314,18 +318,20 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     //   median, r = 1 (8-bit)                     -> 3x3 kernels (k_med3t / k_med3)
     //   median, r = 2, 3                          -> sorted packed columns + shared merges (k_mednet)
     //   median, r = 1 (16-bit)                    -> selection network (k_sortnet<3>)
-    //   8-bit, r <= 48 (any rank)                 -> column-histogram gather
-    //   8-bit, 49 <= r <= 127                     -> CTMF tiles (O(1) in r)
+    //   8-bit, r < 32 (any rank)                  -> column-histogram gather
+    //   8-bit, 32 <= r <= 127                     -> band-matrix products on the tensor cores (k_bandmma_u8)
+    //   (CTMF tiles, O(1) in r: MTB_KERNEL=ctmf only -- superseded by k_bandmma_u8)
     //   16-bit, n <= 255                          -> column histograms (two kernels, by value spread)
     //   otherwise (n > 255)                       -> per-column vertical histograms
     // MTB_KERNEL forces a family (tests).
     const bool median = (uint32_t)((n * n + 1) / 2) == p.rank;
     if (median && n <= 7 && (force.empty() || force == "sortnet" || force == "med3" || force == "mednet"))
         return run_sortnet<P>(p, B, s);
-    if (sizeof(P) == 1 && n <= 255 && p.radius >= 1 && force == "bandmma") return run_bandmma_u8(p, B, s);
-    if (sizeof(P) == 1 && n <= 255 && (force == "colhist" || (force.empty() && p.radius <= 48)))
+    if (sizeof(P) == 1 && n <= 255 && (force == "colhist" || (force.empty() && p.radius < BANDMMA_MIN_R)))
         return run_colhist_u8(p, B, s);
-    if (sizeof(P) == 1 && !wide && (force == "ctmf" || force.empty())) return run_ctmf_u8(p, B, s);
+    if (sizeof(P) == 1 && n <= 255 && p.radius >= 1 && (force == "bandmma" || force.empty()))
+        return run_bandmma_u8(p, B, s);
+    if (sizeof(P) == 1 && !wide && force == "ctmf") return run_ctmf_u8(p, B, s);
     if (sizeof(P) == 2 && n <= 255 && force != "vert") return run_u16_colhist(p, B, s);
     if (sizeof(P) == 1) {
         constexpr int T = 128;

@@ -389,7 +389,7 @@ def test_full_size_off_centre_ranks():
 _FAMILY_CASES = [c for c in G.small_cases() if c[0]["rank"] is None and c[0]["percentile"] is None]
 
 
-@pytest.mark.parametrize("family", ["vert", "ctmf", "sortnet", "colhist", "colhist16s", "colhist16c"])
+@pytest.mark.parametrize("family", ["vert", "ctmf", "bandmma", "sortnet", "colhist", "colhist16s", "colhist16c"])
 def test_each_kernel_family_is_exact(family, monkeypatch):
     """MTB_KERNEL forces one family; families that do not apply to a case
     (ctmf: 8-bit only; sortnet: median of n <= 7) fall through to the
@@ -412,7 +412,7 @@ def test_each_kernel_family_is_exact(family, monkeypatch):
         px16 = rng.integers(0, 65536, (70, 90)).astype(np.uint16)
         out16 = mtb.rank_filter(torch.from_numpy(px16).cuda(), min(r, 34)).cpu().numpy()
         assert np.array_equal(out16, O.iot_filter(px16, 2 * min(r, 34) + 1)), (family, r)
-    expect = {"vert": "k_vert_u8", "ctmf": "k_ctmf_u8", "sortnet": "k_sortnet", "colhist": "k_colhist_u8",
+    expect = {"vert": "k_vert_u8", "ctmf": "k_ctmf_u8", "bandmma": "k_bandmma_u8", "sortnet": "k_sortnet", "colhist": "k_colhist_u8",
               "colhist16s": "k_colhist16s_u16", "colhist16c": "k_colhist16c_u16"}[family]
     assert expect in seen, seen
 
@@ -777,6 +777,52 @@ def test_ctmf_slabs_batch_lut(pre, ctb4, monkeypatch):
         assert np.array_equal(out[i], O.iot_filter(bt[i], 81)), i
     o, _ = mtb.filter_image(px, 99, max_error=8)
     assert np.array_equal(o.pixels, O.iot_filter(px, 99, max_error=8))
+
+
+@pytest.mark.parametrize("tw", ["512", "208", "64"])
+def test_bandmma_slabs_batch_lut_ranks(tw, monkeypatch):
+    """The band-matrix tensor-core kernel (k_bandmma_u8) at several stripe
+    widths: every k-tile count (r = 1 .. 127), ranks at both ends and off
+    centre, slab calls with row_begin > 0, a batch of images, a value map,
+    ragged stripes -- on smooth frames (keyed windows predicted from the row
+    above hit) and on frames whose medians jump between rows and columns
+    (every prediction misses: the coarse fallback resolves them) -- all vs the
+    oracle."""
+    from paper_1105_3829_b200 import _lib
+
+    monkeypatch.setenv("MTB_KERNEL", "bandmma")
+    monkeypatch.setenv("MTB_BM_TW", tw)
+    rng = np.random.default_rng(int(tw))
+    smooth = workloads.cfg2_blur_sp_u8(140, 333, seed=12)
+    noise = rng.integers(0, 256, (140, 333), dtype=np.uint8)
+    # bands of very different levels, 9 rows / 21 columns wide: the median jumps
+    jumpy = ((np.arange(140)[:, None] // 9 * 83 + np.arange(333)[None, :] // 21 * 57) % 256).astype(np.uint8)
+    jumpy[rng.random(jumpy.shape) < 0.1] = 255
+    for name, px in (("smooth", smooth), ("noise", noise), ("jumpy", jumpy)):
+        dev = torch.from_numpy(px).cuda()
+        for r in (1, 8, 9, 24, 25, 40, 41, 56, 57, 63, 69):
+            n = 2 * r + 1
+            for rank in (None, 1, n * n, (n * n) // 3 + 1):
+                out = mtb.rank_filter(dev, r, rank=rank).cpu().numpy()
+                assert _lib.last_kernel().startswith("k_bandmma_u8"), _lib.last_kernel()
+                assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (name, r, rank)
+    tall = workloads.cfg2_blur_sp_u8(300, 150, seed=13)
+    for r in (73, 88, 89, 104, 105, 120, 127):  # k-tile counts 6 .. 9
+        out = mtb.rank_filter(torch.from_numpy(tall).cuda(), r).cpu().numpy()
+        assert np.array_equal(out, O.iot_filter(tall, 2 * r + 1)), r
+    H = smooth.shape[0]
+    ref = O.iot_filter(smooth, 81)
+    dev = torch.from_numpy(smooth).cuda()
+    for a, b in [(0, 57), (57, 130), (130, 140)]:
+        top, bot = max(0, a - 40), min(H, b + 40)
+        out = mtb.rank_filter(dev[top:bot], 40, rows=(a, b), src_row0=top, height=H)
+        assert np.array_equal(out.cpu().numpy(), ref[a:b]), (a, b)
+    bt = workloads.cfg5_batch_u8(3, 150, 290)
+    out = mtb.rank_filter(torch.from_numpy(bt).cuda(), 33).cpu().numpy()
+    for i in range(3):
+        assert np.array_equal(out[i], O.iot_filter(bt[i], 67)), i
+    o, _ = mtb.filter_image(smooth, 99, max_error=8)
+    assert np.array_equal(o.pixels, O.iot_filter(smooth, 99, max_error=8))
 
 
 # ------------------------------------------ every radius through the default dispatch
