@@ -222,11 +222,19 @@ __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW)
         pone = 1u << (8 * (bl & 3));
     }
     unsigned pvo = 0, pvi = 0;
+    // running pointers to the slot's column in the leaving / entering row of
+    // the next update (a clamped row index repeats the edge row: no step)
+    const uint8_t *pout = pin + (int64_t)(clampi(y0 - r, 0, H - 1) - p.src_row0) * p.src_pitch;
+    const uint8_t *pent = pin + (int64_t)(clampi(y0 + 1 + r, 0, H - 1) - p.src_row0) * p.src_pitch;
+    // rows of the update y-1 -> y: leaving y-r-1, entering y+r; called for yn = y0+1, y0+2, ...
     auto prefetch = [&](int yn) {
         if (pw) {
-            pvo = __ldg(pin + (int64_t)(clampi(yn - r - 1, 0, H - 1) - p.src_row0) * p.src_pitch);
-            pvi = __ldg(pin + (int64_t)(clampi(yn + r, 0, H - 1) - p.src_row0) * p.src_pitch);
+            pvo = __ldg(pout);
+            pvi = __ldg(pent);
         }
+        // next update (yn + 1): leaving row yn - r, entering row yn + 1 + r
+        if (yn - r > 0 && yn - r <= H - 1) pout += p.src_pitch;
+        if (yn + 1 + r <= H - 1) pent += p.src_pitch;
     };
     auto move = [&](uint32_t *wp, uint32_t one, unsigned vo, unsigned vi) {
         atomicAdd(wp + (16 + vo) * NPW, 0u - one);
