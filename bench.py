@@ -319,6 +319,20 @@ def _issue_profile():
         return {}
 
 
+IMMA_PER_SM_CLK = 1.79  # measured: tools/micro/imma_lat.cu, profiles/r2_micro_imma.txt
+
+
+def _tensor_share(r, npx, ms, sm_mhz, nsm):
+    """Tensor-core work of one k_bandmma_u8 launch: one product of 4 n-tiles x
+    NK k-tiles (mma.sync m16n8k32 u8, 8192 MACs x 2 ops) per 16 output pixels,
+    against the measured IMMA issue rate."""
+    nk = (16 + 2 * r + 31) // 32
+    imma = npx / 16 * 4 * nk
+    bound_ms = imma / (nsm * IMMA_PER_SM_CLK * (sm_mhz or 1965.0) * 1e6) * 1e3
+    return {"imma_per_launch": int(imma), "int8_tops": round(imma * 16 * 8 * 32 * 2 / (ms * 1e-3) / 1e12, 1),
+            "imma_bound_ms": round(bound_ms, 4), "frac": round(bound_ms / ms, 4)}
+
+
 def _issue_ceiling(key, npx, ms, sm_mhz, nsm):
     """The second ceiling: the kernel's warp-instructions per
     output pixel (ncu) against the chip's issue rate.  issue_bound_ms = the
@@ -495,7 +509,7 @@ def run_ours(args):
                "h2d_bytes_per_step": len(RADII) * H * W, "d2h_bytes_per_step": len(RADII) * H * W,
                "api": "paper_1105_3829_b200.filter_host_frames -> mtb_filter_host_frames (C ABI, six pinned "
                       "host frames per step, one per radius; copies of neighbouring frames overlapped with "
-                      "filtering on a ring of 3 device buffer pairs)",
+                      "filtering, one device buffer pair per frame)",
                "single_frame_calls": {"value": v_single, "api": "filter_host_buffer -> mtb_filter_host_rows per "
                                       "radius on pinned frames (synchronous; row bands for r < 12, streaming "
                                       "launch for r >= 12)"},
@@ -519,6 +533,9 @@ def run_ours(args):
                               "mpix_s": round(H * W / (ms_r[r] * 1e-3) / 1e6, 1),
                               "hbm_frac": round(alg_bytes / (ms_r[r] * 1e-3) / 1e9 / peak, 5),
                               "issue": _issue_ceiling(f"cfg2_r{r}", H * W, ms_r[r], clocks.get("sm_mhz"), nsm)}
+    for r in RADII:  # the tensor-core share of the band-matrix kernel (k_bandmma_u8)
+        if kernels[r].startswith("k_bandmma"):
+            per_radius[str(r)]["tensor"] = _tensor_share(r, H * W, ms_r[r], clocks.get("sm_mhz"), nsm)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
