@@ -13,7 +13,7 @@ import argparse
 import itertools
 
 # config-2 kernel times per radius (ms, bench.py per-radius events)
-KERNEL_MS = {1: 0.02, 3: 0.17, 7: 0.23, 15: 0.32, 31: 0.53, 63: 1.07}
+KERNEL_MS = {1: 0.023, 3: 0.170, 7: 0.226, 15: 0.323, 31: 0.499, 63: 0.534}
 
 
 def simulate(order, nb, copy_ms, stream_first=True):
