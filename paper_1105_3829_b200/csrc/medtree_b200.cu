@@ -20,6 +20,10 @@
 #include "kernels_mednet.cuh"
 #include "kernels_select.cuh"
 #include <cstdlib>
+#if defined(__x86_64__) || defined(_M_X64)
+#include <emmintrin.h>
+#define MTB_HAVE_SSE2 1
+#endif
 
 namespace mtb {
 
@@ -392,6 +396,38 @@ using namespace mtb;
 // with P threads (the calling thread included), so host memcpy, PCIe and
 // the kernels overlap band by band (host_pipeline).  Persistent workers,
 // one pool per device context; never destroyed (process exit reclaims).
+// Staging copy between a pageable frame and a page-locked buffer with
+// non-temporal stores: the destination is either read next by the DMA engine
+// (from DRAM) or is the caller's result frame, so filling the cache with it
+// (and reading the lines first, as plain stores do) only costs memory
+// bandwidth -- the host memcpy is the slowest stage of the pageable path.
+// MTB_COPY_NT=0: plain memcpy.
+static void stage_copy(char *d, const char *s, size_t n) {
+#ifdef MTB_HAVE_SSE2
+    static const bool nt = env_int("MTB_COPY_NT", 1) != 0;
+    if (nt && n >= 4096) {
+        const size_t head = (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15;
+        memcpy(d, s, head);
+        d += head, s += head, n -= head;
+        size_t i = 0;
+        for (; i + 64 <= n; i += 64) {
+            const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i));
+            const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 16));
+            const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 32));
+            const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 48));
+            _mm_stream_si128(reinterpret_cast<__m128i *>(d + i), a);
+            _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 16), b);
+            _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 32), c);
+            _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 48), e);
+        }
+        _mm_sfence();
+        memcpy(d + i, s + i, n - i);
+        return;
+    }
+#endif
+    memcpy(d, s, n);
+}
+
 struct CopyPool {
     std::mutex mu;
     std::condition_variable cv, cv_done;
@@ -422,14 +458,14 @@ struct CopyPool {
             const int i = next.fetch_add(1);
             if (i >= pieces) return;
             const size_t o = (size_t)i * piece, l = std::min(piece, n - o);
-            memcpy(d + o, s + o, l);
+            stage_copy(d + o, s + o, l);
             std::lock_guard<std::mutex> lk(mu);
             if (++done == pieces) cv_done.notify_all();
         }
     }
     void copy(void *dst, const void *src, size_t len) {
         if (len < (1u << 20) || P <= 1) {
-            memcpy(dst, src, len);
+            stage_copy(static_cast<char *>(dst), static_cast<const char *>(src), len);
             return;
         }
         {
@@ -469,7 +505,7 @@ static int host_staging(HostCtx *ctx, size_t bytes) {
     if (!ctx->pool) {
         const unsigned hw = std::thread::hardware_concurrency();
         ctx->pool = new CopyPool();
-        ctx->pool->start((int)std::min(8u, std::max(1u, hw / 2)));
+        ctx->pool->start(env_int("MTB_COPY_THREADS", (int)std::min(8u, std::max(1u, hw / 2))));
     }
     if (ctx->hcap >= bytes) return MTB_OK;
     if (ctx->hin) cudaFreeHost(ctx->hin);
