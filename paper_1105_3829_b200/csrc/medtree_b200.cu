@@ -333,6 +333,7 @@ static int run(SlabParams p, int B, cudaStream_t s) {
         return run_sortnet<P>(p, B, s);
     if (sizeof(P) == 1 && n <= 255 && (force == "colhist" || (force.empty() && p.radius < BANDMMA_MIN_R)))
         return run_colhist_u8(p, B, s);
+    if (sizeof(P) == 1 && n <= 255 && p.radius >= 1 && force == "bandtc") return run_bandtc_u8(p, B, s);
     if (sizeof(P) == 1 && n <= 255 && p.radius >= 1 && (force == "bandmma" || force.empty()))
         return run_bandmma_u8(p, B, s);
     if (sizeof(P) == 1 && !wide && force == "ctmf") return run_ctmf_u8(p, B, s);
