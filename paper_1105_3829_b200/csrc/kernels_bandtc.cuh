@@ -24,12 +24,15 @@
 //   * D = s32 accumulators in tensor memory; each thread reads ITS pixel's
 //     counts with tcgen05.ld (lane = pixel, registers = bins): no transpose
 //     through shared memory, one thread descends one pixel.
-// Per row and 128-pixel tile: one N = 16 product over the cumulative planes
-// (every pixel's exact coarse bin and the count below it) and one N = NF
-// product over the value planes of NF / 16 coarse bins from a base predicted
-// one row up.  A pixel whose coarse bin lies outside that window is a miss: the
-// tile repeats the value product from the lowest missed bin (its planes are
-// still those of this row) -- exact for any image.
+// Bins of 15 values: bin j = values 15j .. 15j+14 owns 16 consecutive planes
+// (two groups): the cumulative plane "pixels below 15j", then its 15 value
+// planes -- so the planes of NB consecutive bins are ONE contiguous B operand
+// and a row costs one product (N = 16 NB) per k-step and 128-pixel tile; its
+// result holds, per bin, the count below the bin and the bin's 15 counts.  The
+// window base is predicted from the bins the tile used one row up.  A pixel
+// whose rank lies below or above the window is a miss: the tile repeats the
+// product from a window on that side (its planes are still those of this row)
+// until every pixel is resolved -- exact for any image.
 //
 // All arithmetic is exact integer counting (r <= 127: u8 column counts).
 #pragma once
@@ -41,11 +44,11 @@ constexpr int BT_M = 128;          // pixels per product (tensor-memory lanes)
 constexpr int BT_MAXTILES = 4;     // 128-pixel tiles per CTA (512 threads)
 constexpr int BT_TMEM_COLS = 512;  // the whole tensor memory (one CTA per SM)
 constexpr int BT_ACOL0 = 416;      // band tiles: columns 416 .. 416 + 8 NKA (NKA <= 12)
-constexpr int BT_CUMG = 0, BT_FINEG = 2;  // plane groups: cum[0..15] = groups 0, 1; fine[v] = group 2 + v / 8
+constexpr int BT_BINS = 18;         // bins of 15 values (18 x 15 >= 256), 16 planes = 2 groups each
 
 __host__ __device__ constexpr int bt_nka(int r) { return (BT_M + 2 * r + 31) / 32; }
 __host__ __device__ constexpr int bt_ncols(int TW, int r) { return TW - BT_M + 32 * bt_nka(r); }
-__host__ __device__ constexpr int bt_groups(int NF) { return 32 + NF / 8 + 2; }  // cum, fine, zero tail of a window from bin 15
+__host__ __device__ constexpr int bt_groups(int) { return 2 * BT_BINS; }
 __host__ __device__ constexpr size_t bt_smem(int TW, int r, int NF) {
     const size_t planes = (size_t)bt_groups(NF) * (bt_ncols(TW, r) / 16) * 128;
     return planes > 120 * 1024 ? planes : 120 * 1024;  // (at least 120 KB: one CTA per SM, it owns all of tensor memory)
@@ -107,14 +110,15 @@ __device__ __forceinline__ int bt_descend16(const int (&f)[16], int k) {
     return (p8 ? 8 : 0) + (p4 ? 4 : 0) + (p2 ? 2 : 0) + (p1 ? 1 : 0);
 }
 
-// NF: value planes of the keyed product (32: two coarse bins, 64: four).
-// Block = TW threads (TW = 128 MT output columns, thread = pixel); grid =
+// NF: planes of the keyed product (32: two bins of 15 values, 64: four).
+// Block = 2 TW threads: thread t < TW = pixel t of the stripe (TW = 128 MT
+// output columns); the others only help with the row updates.  Grid =
 // (stripes, row slabs, images).
 template <int NF, bool STREAM>
-__global__ void __launch_bounds__(BT_M * BT_MAXTILES, 1) k_bandtc_u8(SlabParams p, int TW) {
-    static_assert(NF == 32 || NF == 64, "two or four coarse bins per keyed window");
-    constexpr int NB = NF / 16;             // coarse bins of the keyed window
-    constexpr int DST = NF + 32;            // tensor-memory columns per tile: NF value bins | 16 cumulative | pad
+__global__ void __launch_bounds__(2 * BT_M * BT_MAXTILES, 1) k_bandtc_u8(SlabParams p, int TW) {
+    static_assert(NF == 32 || NF == 64, "two or four bins per keyed window");
+    constexpr int NB = NF / 16;  // bins of the keyed window
+    constexpr int DST = NF;      // tensor-memory columns per tile
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t s_bar[BT_MAXTILES];
     __shared__ uint32_t s_tmem;
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(BT_M * BT_MAXTILES, 1) k_bandtc_u8(SlabParams 
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&s_bar[tid])) : "memory");
         s_lo[0][tid] = s_lo[1][tid] = 255;
         s_hi[0][tid] = s_hi[1][tid] = -1;
-        s_minv[0][tid] = s_minv[1][tid] = 255;
+        s_minv[0][tid] = s_minv[1][tid] = 4096;
         s_retry[tid] = 255;
     }
     if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -173,6 +177,9 @@ __global__ void __launch_bounds__(BT_M * BT_MAXTILES, 1) k_bandtc_u8(SlabParams 
     }
     // word of (plane pl, word column wc = c >> 2) in the blocked layout
     auto pword = [&](int pl, int wc) { return ((pl >> 3) * GSZ + (wc >> 2) * 128 + (pl & 7) * 16 + (wc & 3) * 4) >> 2; };
+    // plane of value v: bin v / 15 (exact for v < 256), plane 1 + v % 15 of the bin's 16
+    auto vplane = [](unsigned v) { const unsigned j = (v * 137u) >> 11; return (int)(v + j + 1u); };  // 16 j + 1 + (v - 15 j)
+    auto vbin = [](unsigned v) { return (int)((v * 137u) >> 11); };
     // Slot s = (byte lane, word column): the lanes of a warp hit distinct words.
     const int nwords = (NC + 3) >> 2, nslots = 4 * nwords;
     for (int s = tid; s < nslots; s += NTH) {
@@ -186,19 +193,20 @@ __global__ void __launch_bounds__(BT_M * BT_MAXTILES, 1) k_bandtc_u8(SlabParams 
 #pragma unroll
             for (int u = 0; u < 8; ++u) v[u] = __ldg(src_row(p, src, clampi(y0 + j + u, 0, H - 1)) + gx);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) atomicAdd(planew + pword(16 + (int)v[u], wc), one);
+            for (int u = 0; u < 8; ++u) atomicAdd(planew + pword(vplane(v[u]), wc), one);
         }
         for (; j <= r; ++j)
-            atomicAdd(planew + pword(16 + (int)__ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx), wc), one);
+            atomicAdd(planew + pword(vplane(__ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx)), wc), one);
     }
     __syncthreads();
-    // cumulative planes from the value planes (bytewise; a column's total is n <= 255)
+    // cumulative planes (plane 16 j: pixels below 15 j) from the value planes (bytewise; a
+    // column's total is n <= 255)
     for (int wc = tid; wc < nwords; wc += NTH) {
         uint32_t run = 0;
-        for (int j = 0; j < 16; ++j) {
-            planew[pword(j, wc)] = run;
+        for (int j = 0; j < BT_BINS; ++j) {
+            planew[pword(16 * j, wc)] = run;
 #pragma unroll
-            for (int v = 0; v < 16; ++v) run += planew[pword(16 + 16 * j + v, wc)];
+            for (int v = 1; v < 16; ++v) run += planew[pword(16 * j + v, wc)];
         }
     }
 
@@ -224,59 +232,75 @@ __global__ void __launch_bounds__(BT_M * BT_MAXTILES, 1) k_bandtc_u8(SlabParams 
         if (yn + 1 + r <= H - 1) pent += p.src_pitch;
     };
     auto move = [&](int wc, uint32_t one, unsigned vo, unsigned vi) {
-        atomicAdd(planew + pword(16 + (int)vo, wc), 0u - one);
-        atomicAdd(planew + pword(16 + (int)vi, wc), one);
-        // cum[j] counts the pixels below 16 j
-        const int a = (int)(vo >> 4), b = (int)(vi >> 4);
+        atomicAdd(planew + pword(vplane(vo), wc), 0u - one);
+        atomicAdd(planew + pword(vplane(vi), wc), one);
+        // plane 16 j counts the pixels below 15 j
+        const int a = vbin(vo), b = vbin(vi);
         const uint32_t d = b > a ? 0u - one : one;
-        for (int j = min(a, b) + 1; j <= max(a, b); ++j) atomicAdd(planew + pword(j, wc), d);
+        for (int j = min(a, b) + 1; j <= max(a, b); ++j) atomicAdd(planew + pword(16 * j, wc), d);
     };
 
-    // ---- products: thread 0 of every tile issues; all 128 threads of the tile read
-    const bool issuer = m == 0;                     // the tile's bookkeeping thread
-    const bool issue_warp = (warp & 3) == 0;        // the tile's first warp issues its products (one elected lane)
-    const uint32_t bar = bt_smem_u32(&s_bar[tile]);
+    // ---- products: the first warp of every tile issues (one elected lane); the tile's 128
+    // threads read their pixels' counts
+    const bool worker = tid < TW;                    // a pixel thread (the others only move the planes)
+    const bool issuer = worker && m == 0;            // the tile's bookkeeping thread
+    const bool issue_warp = worker && (warp & 3) == 0;
+    const uint32_t utile = (uint32_t)__shfl_sync(0xffffffffu, tile, 0);  // (warp-uniform for the compiler)
+    const uint32_t bar = bt_smem_u32(&s_bar[worker ? tile : 0]);
     uint32_t parity = 0;
     const uint32_t dcol = (uint32_t)tile * DST;                       // the tile's accumulator columns
-    const uint32_t tlane = tm + ((uint32_t)(32 * (warp & 3)) << 16);  // this warp's lane quadrant
-    const uint32_t idesc_f = (2u << 4) | ((uint32_t)(NF >> 3) << 17) | ((uint32_t)(BT_M >> 4) << 24);
-    const uint32_t idesc_c = (2u << 4) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(BT_M >> 4) << 24);
-    const uint32_t utile = (uint32_t)__shfl_sync(0xffffffffu, tile, 0);  // (warp-uniform for the compiler)
-    const uint32_t sbase = bt_smem_u32(smem_raw) + utile * 8 * 128;  // the tile's first column chunk
     const uint32_t udcol = utile * DST;
-    auto issue = [&](int B, bool with_cum) {
+    const uint32_t tlane = tm + ((uint32_t)(32 * (warp & 3)) << 16);  // this warp's lane quadrant
+    const uint32_t idesc = (2u << 4) | ((uint32_t)(NF >> 3) << 17) | ((uint32_t)(BT_M >> 4) << 24);
+    const uint32_t sbase = bt_smem_u32(smem_raw) + utile * 8 * 128;   // the tile's first column chunk
+    auto issue = [&](int B) {
         // generic-proxy plane writes (atomics) of all threads are ordered by the barrier; make them
         // visible to the tensor core's async-proxy reads
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t uB = (uint32_t)__shfl_sync(0xffffffffu, B, 0);
-        const uint64_t df = bt_desc(sbase + (BT_FINEG + 2 * uB) * (uint32_t)GSZ, 128, GSZ);
-        const uint64_t dc = bt_desc(sbase + (uint32_t)BT_CUMG * GSZ, 128, GSZ);
+        const uint64_t db = bt_desc(sbase + 2 * uB * (uint32_t)GSZ, 128, GSZ);
 #pragma unroll 4
-        for (int s = 0; s < NKA; ++s) {
-            const uint32_t ta = tm + BT_ACOL0 + 8 * s;
-            bt_mma(tm + udcol, ta, df + (uint64_t)(16 * s), idesc_f, s > 0);             // + 256 bytes per k-step
-            if (with_cum) bt_mma(tm + udcol + NF, ta, dc + (uint64_t)(16 * s), idesc_c, s > 0);
-        }
+        for (int s = 0; s < NKA; ++s) bt_mma(tm + udcol, tm + BT_ACOL0 + 8 * s, db + (uint64_t)(16 * s), idesc, s > 0);  // + 256 bytes per k-step
         bt_commit(bt_smem_u32(&s_bar[utile]));
     };
 
     const int xl = tile * BT_M + m;
-    const bool valid = X0 + xl < W;
+    const bool valid = worker && X0 + xl < W;
     uint8_t *dpx = dst + (int64_t)(y0 - p.row_begin) * p.dst_pitch + X0 + xl;
     const int rank = (int)p.rank;
-    // value chunks of the pixels whose coarse bin lies in [B, B + NB): the chunk's 16 counts, then the descent
-    auto resolve = [&](int B, int cb, int kf, bool want, int &val, bool &miss) {
-        const int d = cb - B;
-        const bool inwin = want && d >= 0 && d < NB;
+    // After a product from base B: the pixel's bin if the window holds its rank value.  lob / hib
+    // bound the bin from what the misses told (below the window / above it).
+    auto resolve = [&](int B, bool want, int &val, int &bin, bool &miss, int &lob, int &hib) {
+        int bl[NB];  // counts below each bin of the window
+#pragma unroll
+        for (int i = 0; i < NB; ++i)
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(bl[i]) : "r"(tlane + dcol + 16 * i) : "memory");
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        int ci = 0;
+#pragma unroll
+        for (int i = 1; i < NB; ++i) ci += bl[i] < rank ? 1 : 0;
+        const bool low = rank <= bl[0];  // the rank value lies below the window
+        if (want && low) hib = min(hib, B - 1);
+        const bool look = want && !low;
 #pragma unroll
         for (int dd = 0; dd < NB; ++dd) {
-            if (__any_sync(0xffffffffu, inwin && d == dd)) {  // (the load's address is warp-uniform)
+            if (__any_sync(0xffffffffu, look && ci == dd)) {  // (the load's address is warp-uniform)
                 int f[16];
                 bt_ld16(tlane + dcol + 16 * dd, f);
-                if (inwin && d == dd) {
-                    val = 16 * cb + bt_descend16(f, kf);
-                    miss = false;
+                if (look && ci == dd) {
+                    const int k = rank - f[0];
+                    f[0] = 0;
+                    int tot = 0;
+#pragma unroll
+                    for (int i = 1; i < 16; ++i) tot += f[i];
+                    if (k <= tot) {
+                        bin = B + dd;
+                        val = 15 * bin + bt_descend16(f, k) - 1;
+                        miss = false;
+                    } else {
+                        lob = max(lob, B + NB);  // above the window (only its last bin can say so)
+                    }
                 }
             }
         }
@@ -288,79 +312,64 @@ __global__ void __launch_bounds__(BT_M * BT_MAXTILES, 1) k_bandtc_u8(SlabParams 
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();  // the planes are those of row y; last row's accumulators have been read
-        // the tile's window base from the coarse bins of the row above (every thread of the tile
-        // computes the same): the bins the tile used, centred in the window
-        int Bt = 0;
-        if (y > y0) {
-            const int lo = s_lo[cur ^ 1][tile], hi = s_hi[cur ^ 1][tile], nib = s_minv[cur ^ 1][tile] & 15;
-            if (lo <= hi) {
-                const int slack = NB - (hi - lo + 1);
-                const int under = slack <= 0 ? 0 : slack / 2 + (((slack & 1) && nib < 8) ? 1 : 0);
-                Bt = max(lo - under, 0);
+        int val = 0, bin = 0, lob = 0, hib = BT_BINS - 1;
+        bool miss = worker;
+        int Bt = (BT_BINS - NB) / 2;
+        if (worker) {
+            // the tile's window base from the bins of the row above (every thread of the tile
+            // computes the same): the bins the tile used, centred in the window
+            if (y > y0) {
+                const int lo = s_lo[cur ^ 1][tile], hi = s_hi[cur ^ 1][tile], pos = s_minv[cur ^ 1][tile];
+                if (lo <= hi) {
+                    const int slack = NB - (hi - lo + 1);
+                    const int under = slack <= 0 ? 0 : slack / 2 + (((slack & 1) && pos - 15 * lo < 7) ? 1 : 0);
+                    Bt = min(max(lo - under, 0), BT_BINS - NB);
+                }
             }
+            if (issue_warp) issue(Bt);
+            bt_wait(bar, parity);
+            parity ^= 1;
+            resolve(Bt, true, val, bin, miss, lob, hib);
         }
-        if (issue_warp) issue(Bt, true);
-        bt_wait(bar, parity);
-        parity ^= 1;
-        // every pixel's coarse bin and the count below it from the 16 cumulative counts
-        int c[16];
-        bt_ld16(tlane + dcol + NF, c);
-        const bool p8 = c[8] < rank;
-        const int a4 = p8 ? c[12] : c[4];
-        int cb = p8 ? 8 : 0, below = p8 ? c[8] : 0;
-        const bool p4 = a4 < rank;
-        cb += p4 ? 4 : 0;
-        below = p4 ? a4 : below;
-        const int a2 = p8 ? (p4 ? c[14] : c[10]) : (p4 ? c[6] : c[2]);
-        const bool p2 = a2 < rank;
-        cb += p2 ? 2 : 0;
-        below = p2 ? a2 : below;
-        const int q0 = p2 ? c[3] : c[1], q1 = p2 ? c[7] : c[5], q2 = p2 ? c[11] : c[9], q3 = p2 ? c[15] : c[13];
-        const int a1 = p8 ? (p4 ? q3 : q2) : (p4 ? q1 : q0);
-        const bool p1 = a1 < rank;
-        cb += p1 ? 1 : 0;
-        below = p1 ? a1 : below;
-        const int kf = rank - below;  // rank within coarse bin cb
-        bool miss = cb < Bt || cb >= Bt + NB;
         // every product of this row is done once all threads are here; any pixel outside its window?
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         int anymiss = __syncthreads_or(miss && valid);
         if (issuer && y > y0) {  // the row above's statistics have been read by the whole tile
             s_lo[cur ^ 1][tile] = 255;
             s_hi[cur ^ 1][tile] = -1;
-            s_minv[cur ^ 1][tile] = 255;
+            s_minv[cur ^ 1][tile] = 4096;
         }
-        int val = 0;
-        miss = true;
-        resolve(Bt, cb, kf, true, val, miss);
         while (anymiss) {
-            // the tile repeats the value product from its lowest missed coarse bin (the planes are
-            // still those of this row: no thread has left the loop)
-            if (miss && valid) atomicMin(&s_retry[tile], cb);
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncthreads();  // (also: every value chunk of the last product has been read)
-            const int nb = s_retry[tile];
-            if (nb != 255) {
-                if (issue_warp) issue(nb, false);
-                bt_wait(bar, parity);
-                parity ^= 1;
-                resolve(nb, cb, kf, miss, val, miss);
+            // the tile repeats the product from a window on the side its lowest missed pixel asked
+            // for (the planes are still those of this row: no thread has left the loop)
+            if (miss && valid) atomicMin(&s_retry[tile], hib < BT_BINS - 1 ? max(hib - NB + 1, 0) : min(lob, BT_BINS - NB));
+            __syncthreads();
+            if (worker) {
+                const int nb = s_retry[tile];
+                if (nb != 255) {
+                    if (issue_warp) issue(nb);
+                    bt_wait(bar, parity);
+                    parity ^= 1;
+                    resolve(nb, miss, val, bin, miss, lob, hib);
+                }
             }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncthreads();
             if (issuer) s_retry[tile] = 255;
             anymiss = __syncthreads_or(miss && valid);
         }
-        // coarse bins and lowest value of this row's pixels: the next row's base
-        {
-            const int wlo = __reduce_min_sync(0xffffffffu, valid ? cb : 255);
-            const int whi = __reduce_max_sync(0xffffffffu, valid ? cb : -1);
-            const int wmv = __reduce_min_sync(0xffffffffu, valid ? val : 255);
+        if (worker) {
+            // bins and lowest value of this row's pixels: the next row's base
+            const int wlo = __reduce_min_sync(0xffffffffu, valid ? bin : 255);
+            const int whi = __reduce_max_sync(0xffffffffu, valid ? bin : -1);
+            const int wmv = __reduce_min_sync(0xffffffffu, valid ? val : 4096);
             if (lane == 0) {
                 atomicMin(&s_lo[cur][tile], wlo);
                 atomicMax(&s_hi[cur][tile], whi);
                 atomicMin(&s_minv[cur][tile], wmv);
             }
+            if (valid) *dpx = lut ? __ldg(lut + val) : (uint8_t)val;
         }
-        if (valid) *dpx = lut ? __ldg(lut + val) : (uint8_t)val;
         // the planes move on to row y+1 (other warps may still be descending: they read tensor memory only)
         if (y + 1 < y1) {
             if (pwc >= 0) move(pwc, pone, pvo, pvi);

@@ -32,7 +32,7 @@ static int run_bandtc_nf(SlabParams p, int B, cudaStream_t s) {
     rpc = std::max(rpc, std::min(rows, r / 2 + 8));
     p.rows_per_cta = rpc;
     dim3 grid(bx, (rows + rpc - 1) / rpc, B);
-    kern<<<grid, TW, smem, s>>>(p, TW);
+    kern<<<grid, 2 * TW, smem, s>>>(p, TW);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_bandtc_u8: ") + cudaGetErrorString(e));
     g_kernel = NF == 32 ? "k_bandtc_u8<32>" : "k_bandtc_u8<64>";
