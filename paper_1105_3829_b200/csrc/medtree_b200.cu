@@ -309,6 +309,9 @@ static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
 // smallest radius sent to k_bandmma_u8 (config 2: 0.51 ms at r = 31 against 0.50 for the pair
 // records, 0.47 against 0.71 at r = 40)
 constexpr int BANDMMA_MIN_R = 32;
+// smallest radius sent to the tcgen05 kernel k_bandtc_u8 (config 2: 0.58 ms against 0.63 for
+// k_bandmma_u8 at r = 80, 0.58 against 0.77 at r = 127; 0.59 against 0.54 at r = 72)
+constexpr int BANDTC_MIN_R = 76;
 
 template <typename P>
 static int run(SlabParams p, int B, cudaStream_t s) {
@@ -323,7 +326,8 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     //   median, r = 2, 3                          -> sorted packed columns + shared merges (k_mednet)
     //   median, r = 1 (16-bit)                    -> selection network (k_sortnet<3>)
     //   8-bit, r < 32 (any rank)                  -> column-histogram gather
-    //   8-bit, 32 <= r <= 127                     -> band-matrix products on the tensor cores (k_bandmma_u8)
+    //   8-bit, 32 <= r <= 75                      -> band-matrix products on the tensor cores, mma.sync (k_bandmma_u8)
+    //   8-bit, 76 <= r <= 127                     -> the same with tcgen05.mma / tensor memory (k_bandtc_u8)
     //   (CTMF tiles, O(1) in r: MTB_KERNEL=ctmf only -- superseded by k_bandmma_u8)
     //   16-bit, n <= 255                          -> column histograms (two kernels, by value spread)
     //   otherwise (n > 255)                       -> per-column vertical histograms
@@ -333,7 +337,9 @@ static int run(SlabParams p, int B, cudaStream_t s) {
         return run_sortnet<P>(p, B, s);
     if (sizeof(P) == 1 && n <= 255 && (force == "colhist" || (force.empty() && p.radius < BANDMMA_MIN_R)))
         return run_colhist_u8(p, B, s);
-    if (sizeof(P) == 1 && n <= 255 && p.radius >= 1 && force == "bandtc") return run_bandtc_u8(p, B, s);
+    if (sizeof(P) == 1 && n <= 255 && p.radius >= 1 &&
+        (force == "bandtc" || (force.empty() && p.radius >= BANDTC_MIN_R)))
+        return run_bandtc_u8(p, B, s);
     if (sizeof(P) == 1 && n <= 255 && p.radius >= 1 && (force == "bandmma" || force.empty()))
         return run_bandmma_u8(p, B, s);
     if (sizeof(P) == 1 && !wide && force == "ctmf") return run_ctmf_u8(p, B, s);

@@ -389,7 +389,7 @@ def test_full_size_off_centre_ranks():
 _FAMILY_CASES = [c for c in G.small_cases() if c[0]["rank"] is None and c[0]["percentile"] is None]
 
 
-@pytest.mark.parametrize("family", ["vert", "ctmf", "bandmma", "sortnet", "colhist", "colhist16s", "colhist16c"])
+@pytest.mark.parametrize("family", ["vert", "ctmf", "bandmma", "bandtc", "sortnet", "colhist", "colhist16s", "colhist16c"])
 def test_each_kernel_family_is_exact(family, monkeypatch):
     """MTB_KERNEL forces one family; families that do not apply to a case
     (ctmf: 8-bit only; sortnet: median of n <= 7) fall through to the
@@ -412,7 +412,7 @@ def test_each_kernel_family_is_exact(family, monkeypatch):
         px16 = rng.integers(0, 65536, (70, 90)).astype(np.uint16)
         out16 = mtb.rank_filter(torch.from_numpy(px16).cuda(), min(r, 34)).cpu().numpy()
         assert np.array_equal(out16, O.iot_filter(px16, 2 * min(r, 34) + 1)), (family, r)
-    expect = {"vert": "k_vert_u8", "ctmf": "k_ctmf_u8", "bandmma": "k_bandmma_u8", "sortnet": "k_sortnet", "colhist": "k_colhist_u8",
+    expect = {"vert": "k_vert_u8", "ctmf": "k_ctmf_u8", "bandmma": "k_bandmma_u8", "bandtc": "k_bandtc_u8", "sortnet": "k_sortnet", "colhist": "k_colhist_u8",
               "colhist16s": "k_colhist16s_u16", "colhist16c": "k_colhist16c_u16"}[family]
     assert expect in seen, seen
 
@@ -823,6 +823,59 @@ def test_bandmma_slabs_batch_lut_ranks(tw, monkeypatch):
         assert np.array_equal(out[i], O.iot_filter(bt[i], 67)), i
     o, _ = mtb.filter_image(smooth, 99, max_error=8)
     assert np.array_equal(o.pixels, O.iot_filter(smooth, 99, max_error=8))
+
+
+@pytest.mark.parametrize("tiles,nf", [("4", "32"), ("2", "64"), ("1", "32")])
+def test_bandtc_slabs_batch_lut_ranks(tiles, nf, monkeypatch):
+    """The tcgen05 band-matrix kernel (k_bandtc_u8: band tiles in tensor
+    memory, planes through shared-memory matrix descriptors, accumulators
+    read back per pixel) with 1, 2 and 4 tiles of 128 pixels per CTA and both
+    window widths: small and large radii, ranks at both ends and off centre,
+    slabs, a batch, a value map, ragged stripes, smooth frames (the window
+    predicted from the row above holds) and frames whose medians jump (the
+    retry from the missed side resolves them), the streaming host entry --
+    all vs the oracle."""
+    from paper_1105_3829_b200 import _lib
+
+    monkeypatch.setenv("MTB_KERNEL", "bandtc")
+    monkeypatch.setenv("MTB_BT_TILES", tiles)
+    monkeypatch.setenv("MTB_BT_NF", nf)
+    rng = np.random.default_rng(int(tiles) * 100 + int(nf))
+    smooth = workloads.cfg2_blur_sp_u8(140, 333, seed=14)
+    noise = rng.integers(0, 256, (140, 333), dtype=np.uint8)
+    jumpy = ((np.arange(140)[:, None] // 9 * 83 + np.arange(333)[None, :] // 21 * 57) % 256).astype(np.uint8)
+    jumpy[rng.random(jumpy.shape) < 0.1] = 255
+    flat = np.full((140, 333), 255, dtype=np.uint8)  # the top bin
+    flat[::7, ::5] = 0
+    for name, px in (("smooth", smooth), ("noise", noise), ("jumpy", jumpy), ("flat", flat)):
+        dev = torch.from_numpy(px).cuda()
+        for r in (1, 9, 31, 48, 63, 69):
+            n = 2 * r + 1
+            for rank in (None, 1, n * n, (n * n) // 3 + 1):
+                out = mtb.rank_filter(dev, r, rank=rank).cpu().numpy()
+                assert _lib.last_kernel().startswith("k_bandtc_u8"), _lib.last_kernel()
+                assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (name, r, rank)
+    tall = workloads.cfg2_blur_sp_u8(300, 150, seed=15)
+    for r in (76, 97, 112, 127):
+        out = mtb.rank_filter(torch.from_numpy(tall).cuda(), r).cpu().numpy()
+        assert np.array_equal(out, O.iot_filter(tall, 2 * r + 1)), r
+    H = smooth.shape[0]
+    ref = O.iot_filter(smooth, 81)
+    dev = torch.from_numpy(smooth).cuda()
+    for a, b in [(0, 57), (57, 130), (130, 140)]:
+        top, bot = max(0, a - 40), min(H, b + 40)
+        out = mtb.rank_filter(dev[top:bot], 40, rows=(a, b), src_row0=top, height=H)
+        assert np.array_equal(out.cpu().numpy(), ref[a:b]), (a, b)
+    bt = workloads.cfg5_batch_u8(3, 150, 290)
+    out = mtb.rank_filter(torch.from_numpy(bt).cuda(), 33).cpu().numpy()
+    for i in range(3):
+        assert np.array_equal(out[i], O.iot_filter(bt[i], 67)), i
+    o, _ = mtb.filter_image(smooth, 99, max_error=8)
+    assert np.array_equal(o.pixels, O.iot_filter(smooth, 99, max_error=8))
+    big = workloads.cfg2_blur_sp_u8(700, 900, seed=16)
+    pinned = torch.from_numpy(big).pin_memory()
+    got = mtb.filter_host_buffer(pinned.numpy(), 80)  # page-locked source, r >= 12: the streaming launch
+    assert np.array_equal(got, O.iot_filter(big, 161))
 
 
 # ------------------------------------------ every radius through the default dispatch
