@@ -1,5 +1,5 @@
 """Parity of a forced kernel family against the CPU oracle on small ragged frames.
-usage: python tools/check_bandmma.py [kernel] [radii]"""
+usage: python tools/check_family.py [kernel] [radii]"""
 import os
 import sys
 
