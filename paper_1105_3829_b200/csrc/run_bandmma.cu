@@ -19,7 +19,7 @@ static int run_bandmma_nk(SlabParams p, int B, cudaStream_t s, int TW) {
     if (per_sm < 1) per_sm = 1;
     // row slabs: as many CTAs as fit `waves` whole rounds of the resident slots
     // (never one more: a straggler round would double the time)
-    const int waves = env_int("MTB_BM_WAVES", 1), rows = p.row_end - p.row_begin;
+    const int waves = env_int("MTB_BM_WAVES", 2), rows = p.row_end - p.row_begin;  // (two: evens out data-dependent rows, costs nothing)
     int64_t slabs = (int64_t)sm_count() * per_sm * waves / ((int64_t)bx * B);
     slabs = std::max<int64_t>(1, std::min<int64_t>(slabs, rows));
     int rpc = (int)((rows + slabs - 1) / slabs);
