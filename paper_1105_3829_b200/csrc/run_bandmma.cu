@@ -26,7 +26,7 @@ static int run_bandmma_nk(SlabParams p, int B, cudaStream_t s, int TW) {
     rpc = std::max(rpc, std::min(rows, p.radius / 2 + 8));  // keep the column build a small share
     p.rows_per_cta = rpc;
     dim3 grid(bx, (rows + rpc - 1) / rpc, B);
-    p.gate = env_int("MTB_BM_DBG", 0);
+    p.gate = env_int("MTB_BM_DBG", 0);  // (only read by a -DBM_TIMING build)
     kern<<<grid, threads, smem, s>>>(p, TW);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_bandmma_u8: ") + cudaGetErrorString(e));
