@@ -7,6 +7,12 @@
 
 namespace mtb {
 
+// the geometry the dispatch relies on: 512-column stripes fit one SM up to r = 72, every radius has a stripe
+static_assert(bm_smem(512, 63) <= 227 * 1024 && bm_smem(512, 72) <= 227 * 1024, "512-column stripes at r <= 72");
+static_assert(bm_smem(16, 127) <= 227 * 1024, "a stripe at the largest radius");
+static_assert(bm_pitch(512, 63) % 64 == 32 && bm_pitch(512, 63) >= 512 + 126 && bm_pitch(512, 63) >= 512 + 32 * bm_nk(63) - 16,
+              "plane pitch: bank rule, halo'd columns, last k-tile");
+
 template <int NK>
 static int run_bandmma_nk(SlabParams p, int B, cudaStream_t s, int TW) {
     const size_t smem = bm_smem(TW, p.radius);

@@ -6,6 +6,11 @@
 
 namespace mtb {
 
+// four 128-pixel tiles fit one SM at every radius; the band tiles (8 columns per k-step) and the
+// accumulators (NF columns per tile) fit tensor memory
+static_assert(bt_smem(512, 127, 32) <= 227 * 1024 - 256 && bt_smem(512, 127, 64) <= 227 * 1024 - 256, "planes at r = 127");
+static_assert(BT_ACOL0 + 8 * bt_nka(127) <= BT_TMEM_COLS && BT_MAXTILES * 64 <= BT_ACOL0, "tensor-memory columns");
+
 template <int NF>
 static int run_bandtc_nf(SlabParams p, int B, cudaStream_t s) {
     const int r = p.radius;
