@@ -47,6 +47,10 @@ _FRAMES: dict = {}
 _TOPO: dict = {}
 
 
+# beyond BASELINE's sweep: the radii of the tcgen05 kernel (k_bandtc_u8, r >= 76) on the config-2 frame
+EXTRA_RADII_CFG2 = (80, 127)
+
+
 def sha(a: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
@@ -88,7 +92,7 @@ def main():
     jobs = []  # (name, key, n, mode, bands)
     if not only or "cfg2" in only:
         _FRAMES["cfg2"] = workloads.cfg2_blur_sp_u8()
-        for r in workloads.CONFIG_RADII[2]:
+        for r in workloads.CONFIG_RADII[2] + EXTRA_RADII_CFG2:
             jobs.append((f"cfg2_4096_r{r}", "cfg2", 2 * r + 1, "uniform", 32))
     if not only or "cfg3" in only:
         _FRAMES["cfg3"] = workloads.cfg3_uniform_u16()

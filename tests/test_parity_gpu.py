@@ -312,6 +312,23 @@ def test_cfg2_full_size_digest(r):
     assert G.sha(dev) == rec["output"]
 
 
+@pytest.mark.parametrize("r", [80, 127])
+def test_cfg2_full_size_digest_large_radii(r):
+    """The config-2 frame beyond BASELINE's sweep, where the tcgen05 kernel
+    (k_bandtc_u8) takes over: device-resident and streaming host entries
+    against the reference's own full frame."""
+    from paper_1105_3829_b200 import _lib
+
+    px = _frame("cfg2")
+    rec = _full(f"cfg2_4096_r{r}")
+    assert G.sha(px) == rec["input"]
+    dev = mtb.rank_filter(torch.from_numpy(px).cuda(), r).cpu().numpy()
+    assert _lib.last_kernel().startswith("k_bandtc_u8"), _lib.last_kernel()
+    assert G.sha(dev) == rec["output"]
+    pin = torch.from_numpy(px).pin_memory().numpy()
+    assert G.sha(mtb.filter_host_buffer(pin, r)) == rec["output"]
+
+
 @pytest.mark.parametrize("r", workloads.CONFIG_RADII[3])
 def test_cfg3_full_size_digest(r):
     """Config 3 (4096^2 u16 uniform): host entry and device-resident entry
