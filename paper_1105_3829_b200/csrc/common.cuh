@@ -38,6 +38,13 @@ struct SlabParams {
     // data is widely spread / compact (two launches, one does the work).
     const int *spread;
     int32_t gate;
+    // 16-bit candidate-list path (kernels_lowsel16.cuh): one byte per block of
+    // 32 x todo_bh output pixels ([image][block row][block column], todo_nbx
+    // block columns), non-zero where the list kernel left the block to the
+    // two-phase kernel.  With todo set, k_colhist16_u16 only works on tiles
+    // that contain such a block.  nullptr elsewhere.
+    unsigned char *todo;
+    int32_t todo_bh, todo_nbx, todo_nby;
 };
 
 constexpr int SPREAD_WIDE = 24;  // > 24 distinct sampled high bytes: widely spread
@@ -52,6 +59,18 @@ __device__ __forceinline__ bool spread_is_wide(const SlabParams &p) {
 __device__ __forceinline__ bool gate_off(const SlabParams &p) {
     if (!p.gate) return false;
     return (p.gate == GATE_WIDE) != spread_is_wide(p);
+}
+
+// CTA-uniform: does the tile [x0, x0 + tw) x rows [y0, y1) contain a block
+// the list kernel left undone?  (Every thread gets the same answer.)
+__device__ __forceinline__ bool todo_any(const SlabParams &p, int x0, int tw, int y0, int y1) {
+    const int bx0 = x0 >> 5, bx1 = min((x0 + tw + 31) >> 5, p.todo_nbx);
+    const int by0 = (y0 - p.row_begin) / p.todo_bh, by1 = min((y1 - p.row_begin + p.todo_bh - 1) / p.todo_bh, p.todo_nby);
+    const unsigned char *f = p.todo + (size_t)blockIdx.z * p.todo_nbx * p.todo_nby;
+    const int nx = bx1 - bx0, cells = nx * (by1 - by0);
+    int any = 0;
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) any |= f[(size_t)(by0 + i / nx) * p.todo_nbx + bx0 + i % nx];
+    return __syncthreads_or(any) != 0;
 }
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) {

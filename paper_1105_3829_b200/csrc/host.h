@@ -67,6 +67,11 @@ int run_colhist4p_256(SlabParams p, int B, cudaStream_t s, int pl);
 int run_colhist16_u16(SlabParams p, int B, cudaStream_t s, int wk = 1);
 int run_colhist16s_u16(SlabParams p, int B, cudaStream_t s);
 int run_colhist16c_u16(SlabParams p, int B, cudaStream_t s);
+// 16-bit, widely spread data: high byte by pair records, low byte from per-block candidate lists,
+// leftovers by the two-phase kernel (run_lowsel16.cu); device-resident launches, r = 3..63
+constexpr int LOWSEL_MIN_R = 3, LOWSEL_MAX_R = 63;
+bool lowsel16_applies(const SlabParams &p);
+int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s);
 // compile-time window sides of k_colhist16_u16; 1 (NOT_COVERED) when n is outside the range
 int run_colhist16_fixed_a(SlabParams p, int B, cudaStream_t s, int wk);
 int run_colhist16_fixed_b(SlabParams p, int B, cudaStream_t s, int wk);

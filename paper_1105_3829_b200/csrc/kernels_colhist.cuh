@@ -678,6 +678,7 @@ __global__ void __launch_bounds__(T) k_colhist16_u16(SlabParams p, uint8_t *__re
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
     if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
     const int y1 = min(y0 + p.rows_per_cta, p.row_end);
+    if (p.todo && !todo_any(p, X0, T, y0, y1)) return;  // (CTA-uniform) nothing left over in this tile
     const uint16_t *src = static_cast<const uint16_t *>(p.src) + blockIdx.z * p.src_img_stride;
     uint16_t *dst = static_cast<uint16_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint16_t *lut = static_cast<const uint16_t *>(p.lut);
@@ -1017,8 +1018,15 @@ namespace mtb {
 // then fit two 256-thread CTAs per SM up to r = 32 (PL = 2 before), and a
 // row update is 12 shared-memory atomics instead of 14.
 
-template <int T, int G, int M, int PL, bool STREAM, int NF = 0>
+// PX = uint16_t: the same kernel keyed by the HIGH byte of 16-bit pixels
+// (first pass of the 16-bit candidate-list path, kernels_lowsel16.cuh):
+// instead of a result pixel it writes H << 16 | k' per pixel to a u32 plane
+// (p.dst, pitch in words), H = the result's high byte, k' = the rank of the
+// result among the window values with that high byte.
+template <int T, int G, int M, int PL, bool STREAM, int NF = 0, typename PX = uint8_t>
 __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
+    constexpr bool HI16 = sizeof(PX) == 2;
+    constexpr int KS = HI16 ? 8 : 0;  // key = pixel >> KS
     constexpr int GP = G / 2;
     constexpr bool DL2 = PL == 4;           // level-2 singles derived from level 3
     constexpr int PLP = DL2 ? 3 : PL;        // pair levels
@@ -1034,10 +1042,11 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
     const int X0 = blockIdx.x * T;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
     if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
+    if (HI16 && gate_off(p)) return;
     const int y1 = min(y0 + p.rows_per_cta, p.row_end);
     if (STREAM) stream_wait_rows(p, y1 + r);
-    const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
-    uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
+    const PX *src = static_cast<const PX *>(p.src) + blockIdx.z * p.src_img_stride;
+    uint8_t *dst = static_cast<uint8_t *>(p.dst) + (HI16 ? 4 : 1) * blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
     const int x = X0 + tid;
     // single-record updates (one atomic per level kept; the word is the
@@ -1059,7 +1068,7 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         const int gx = clampi(X0 - r + c, 0, W - 1);
         // (atomic adds here too: measured r = 15 0.358 -> 0.319 ms, r = 31
         // 0.595 -> 0.530 against byte read-modify-writes)
-        for (int j = -r; j <= r; ++j) sbump(c, __ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx), 1);
+        for (int j = -r; j <= r; ++j) sbump(c, (unsigned)__ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx) >> KS, 1);
     }
     __syncthreads();
     // level-2 word of column c for record p2, from its four level-3 words
@@ -1101,12 +1110,12 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
     for (int u = 0; u < CH_PF; ++u) gxs[u] = clampi(X0 - r + min(tid + u * T, NCOL - 1), 0, W - 1);
     unsigned pvo[CH_PF], pvi[CH_PF];
     auto prefetch = [&](int yn) {
-        const uint8_t *ro = src_row(p, src, clampi(yn - r - 1, 0, H - 1));
-        const uint8_t *ri = src_row(p, src, clampi(yn + r, 0, H - 1));
+        const PX *ro = src_row(p, src, clampi(yn - r - 1, 0, H - 1));
+        const PX *ri = src_row(p, src, clampi(yn + r, 0, H - 1));
 #pragma unroll
         for (int u = 0; u < CH_PF; ++u) {
-            pvo[u] = __ldg(ro + gxs[u]);
-            pvi[u] = __ldg(ri + gxs[u]);
+            pvo[u] = (unsigned)__ldg(ro + gxs[u]) >> KS;
+            pvi[u] = (unsigned)__ldg(ri + gxs[u]) >> KS;
         }
     };
     if (y0 + 1 < y1) prefetch(y0 + 1);
@@ -1121,11 +1130,11 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
                 if (c < NCOL) move(c, pvo[u], pvi[u]);  // (vo == vi cancels: no data-dependent branch)
             }
             if (NCOL > CH_PF * T) {
-                const uint8_t *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
-                const uint8_t *ri = src_row(p, src, clampi(y + r, 0, H - 1));
+                const PX *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
+                const PX *ri = src_row(p, src, clampi(y + r, 0, H - 1));
                 for (int c = tid + CH_PF * T; c < NCOL; c += T) {
                     const int gx = clampi(X0 - r + c, 0, W - 1);
-                    const unsigned vo = __ldg(ro + gx), vi = __ldg(ri + gx);
+                    const unsigned vo = (unsigned)__ldg(ro + gx) >> KS, vi = (unsigned)__ldg(ri + gx) >> KS;
                     if (vo == vi) continue;
                     move(c, vo, vi);
                 }
@@ -1153,7 +1162,11 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         ch4_gather<G, M>(rec + (R3 + p3) * NCP + tid, n, w0, w1);
         const int d0 = ch4_descend(w0, w1, k);
         const unsigned v = (unsigned)(p3 * 4 + d0);
-        if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
+        if (HI16) {
+            if (x < W) reinterpret_cast<uint32_t *>(dst)[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = (v << 16) | k;
+        } else {
+            if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
+        }
     }
     if (STREAM) stream_signal(p, y0, y1, X0, X0 + T);
 }

@@ -1,0 +1,196 @@
+// kernels_lowsel16.cuh -- 16-bit rank filter on widely spread data, second
+// pass: "low byte from shared candidate buckets".
+//
+// The reference descends a 3-level tree per pixel (_kernels.py:229-253
+// extract_u on the 16-bit tree): the top levels pick the coarse bin, the last
+// one the value inside it.  Here the first pass (k_colhist4p_u8 keyed by the
+// high byte, kernels_colhist.cuh) leaves, per output pixel, the high byte H of
+// the result and the rank k' of the result among the window values whose high
+// byte is H.  On spread data only ~n^2/256 window values have that high byte,
+// and neighbouring pixels want nearby H, so ONE WARP resolves a block of
+// 32 x PH output pixels together:
+//   1. [Hmin, Hmax] = the range of H over the block, taken in chunks of NB
+//      consecutive high bytes (NB buckets of BCAP entries = 512 entries);
+//   2. the warp scans the union of the block's windows, (32 + 2r) x (PH + 2r)
+//      replicate-clamped source values, once per chunk, and drops every value
+//      whose high byte lies in the chunk into that high byte's bucket in
+//      shared memory together with its window coordinates
+//      (value << 16 | dy << 8 | dx);
+//   3. every bucket is sorted by counting ranks (entries are distinct, so an
+//      entry's place is the number of smaller entries of its bucket);
+//   4. every pixel walks the bucket of its H in ascending order, counts the
+//      entries inside its own window, and stops at the k'-th: that entry's
+//      value is the result.
+// The scan is shared by 32 PH pixels, so a pixel pays (32 + 2r)(PH + 2r) /
+// (32 PH) loads instead of the n per level of the gather kernels or the
+// per-column run lookups of k_colhist16c_u16.
+//
+// A bucket that overflows doubles BCAP (half as many high bytes per chunk)
+// and repeats the chunk; a block where one high byte alone overflows 512
+// entries (locally compact data) is flagged in SlabParams::todo and left to
+// k_colhist16_u16, which then works on the tiles holding such blocks only.
+// Exact for any image; the data only decide which kernel resolves a block.
+#pragma once
+#include "common.cuh"
+
+namespace mtb {
+
+constexpr int LS_WARPS = 8;    // warps per CTA, side by side (256 output columns)
+constexpr int LS_CAP = 512;    // bucket entries per warp (NB buckets x BCAP)
+constexpr int LS_MAXLG = 9;    // log2 of the largest bucket (one high byte per chunk)
+constexpr int LS_MINLG = 4;    // log2 of the smallest bucket (32 high bytes per chunk)
+
+// hk: [image][row - row_begin][x] words H << 16 | k' (pitch W); PH output rows
+// per block; lg0: log2 of the bucket size to start with
+template <int PH>
+__global__ void __launch_bounds__(32 * LS_WARPS) k_lowsel_u16(SlabParams p, const uint32_t *__restrict__ hk, int lg0) {
+    __shared__ uint32_t bufs[LS_WARPS][LS_CAP];  // buckets as scanned
+    __shared__ uint32_t srts[LS_WARPS][LS_CAP];  // buckets sorted
+    __shared__ int bcnts[LS_WARPS][32];          // entries per bucket
+    if (gate_off(p)) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r = p.radius, r2 = 2 * r, W = p.W, H = p.H;
+    const int xb = (blockIdx.x * LS_WARPS + warp) * 32;  // first output column of the block
+    if (xb >= W) return;                                  // (warp-uniform; the kernel has no CTA barriers)
+    const int yb = p.row_begin + blockIdx.y * PH;
+    const int ph = min(PH, p.row_end - yb);
+    const int rows = p.row_end - p.row_begin;
+    const uint16_t *src = static_cast<const uint16_t *>(p.src) + blockIdx.z * p.src_img_stride;
+    uint16_t *dst = static_cast<uint16_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
+    const uint16_t *lut = static_cast<const uint16_t *>(p.lut);
+    const uint32_t *hkp = hk + ((int64_t)blockIdx.z * rows + (yb - p.row_begin)) * W + xb + lane;
+    uint32_t *buf = bufs[warp], *srt = srts[warp];
+    int *bcnt = bcnts[warp];
+    const bool valid = xb + lane < W;
+
+    // ---- the block's (H, k') and the range of H
+    uint32_t myhk[PH];
+    int hmin = 255, hmax = 0;
+#pragma unroll
+    for (int py = 0; py < PH; ++py) {
+        myhk[py] = 0xffffffffu;
+        if (valid && py < ph) {
+            myhk[py] = __ldg(hkp + (int64_t)py * W);
+            const int h = (int)(myhk[py] >> 16);
+            hmin = min(hmin, h);
+            hmax = max(hmax, h);
+        }
+    }
+    hmin = __reduce_min_sync(0xffffffffu, hmin);
+    hmax = __reduce_max_sync(0xffffffffu, hmax);
+
+    // the union of the windows: virtual columns xb-r .. xb+31+r (dx = 0 .. UW-1),
+    // virtual rows yb-r .. yb+ph-1+r (dy = 0 .. UH-1), replicate-clamped into
+    // the image.  Only the cells inside the image are scanned (dx in [cL, cR],
+    // dy in [jT, jB]); a border pixel stands for every virtual cell clamped
+    // onto it, and the walk below weighs it by how many of those lie in the
+    // pixel's window.
+    const int UW = 32 + r2, UH = ph + r2;
+    const int cL = max(0, r - xb), cR = min(UW - 1, W - 1 - xb + r);
+    const int jT = max(0, r - yb), jB = min(UH - 1, H - 1 - yb + r);
+    const bool border = cL > 0 || cR < UW - 1 || jT > 0 || jB < UH - 1;  // (warp-uniform)
+    // image borders in window coordinates (out of reach when the border is not in the union)
+    const int dxL = xb - r <= 0 ? r - xb : -1000, dxR = xb + 31 + r >= W - 1 ? W - 1 - xb + r : 1000;
+    const int dyT = yb - r <= 0 ? r - yb : -1000, dyB = yb + ph - 1 + r >= H - 1 ? H - 1 - yb + r : 1000;
+    constexpr int NI = 5;  // column steps of 32: UW <= 158 (r <= 63)
+    int gx[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) gx[i] = clampi(xb - r + lane + 32 * i, 0, W - 1);
+
+    int lg = lg0;
+    for (int h0 = hmin; h0 <= hmax;) {
+        const int NB = LS_CAP >> lg, BCAP = 1 << lg;
+        const int h1 = min(h0 + NB - 1, hmax);
+        const unsigned hspan = (unsigned)(h1 - h0);
+        bool want = false;
+#pragma unroll
+        for (int py = 0; py < PH; ++py) want |= (myhk[py] >> 16) - (unsigned)h0 <= hspan;
+        if (!__any_sync(0xffffffffu, want)) {  // no pixel of the block has its H here
+            h0 = h1 + 1;
+            continue;
+        }
+        bcnt[lane] = 0;
+        __syncwarp();
+        // ---- scan
+        for (int j = jT; j <= jB; ++j) {
+            const uint16_t *row = src_row(p, src, yb - r + j);
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                if (32 * i < UW) {  // (warp-uniform)
+                    const int c = lane + 32 * i;
+                    const unsigned v = __ldg(row + gx[i]);
+                    const unsigned b = (v >> 8) - (unsigned)h0;
+                    if (c >= cL && c <= cR && b <= hspan) {
+                        const int slot = atomicAdd(bcnt + b, 1);
+                        if (slot < BCAP) buf[(b << lg) + slot] = (v << 16) | ((unsigned)j << 8) | (unsigned)c;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (__any_sync(0xffffffffu, bcnt[lane] > BCAP)) {
+            if (lg == LS_MAXLG) {  // locally compact data: leave the block to the two-phase kernel
+                if (lane == 0) p.todo[((size_t)blockIdx.z * p.todo_nby + blockIdx.y) * p.todo_nbx + (xb >> 5)] = 1;
+                return;
+            }
+            ++lg;  // larger buckets, fewer high bytes per chunk; repeat from h0
+            __syncwarp();
+            continue;
+        }
+        // ---- sort every bucket: an entry goes to the count of smaller entries
+        for (int t = lane; t < (NB << lg); t += 32) {
+            const int b = t >> lg, i = t & (BCAP - 1), nb = bcnt[b];
+            if (i < nb) {
+                const uint32_t *bk = buf + (b << lg);
+                const uint32_t e = bk[i];
+                int rank = 0;
+                for (int q = 0; q < nb; ++q) rank += bk[q] < e ? 1 : 0;
+                srt[(b << lg) + rank] = e;
+            }
+        }
+        __syncwarp();
+        // ---- every pixel of the chunk: the k'-th entry of its bucket inside its
+        // window (pixel (lane, py): dx in [lane, lane + 2r], dy in [py, py + 2r])
+#pragma unroll
+        for (int py = 0; py < PH; ++py) {
+            const unsigned b = (myhk[py] >> 16) - (unsigned)h0;
+            if (b > hspan) continue;
+            const uint32_t k = myhk[py] & 0xffffu;
+            const uint32_t *bk = srt + (b << lg);
+            const int nb = bcnt[b];
+            uint32_t c = 0, res = 0;
+            if (!border) {
+                for (int i = 0; i < nb; ++i) {
+                    const uint32_t e = bk[i];
+                    const bool inw = (e & 0xffu) - (unsigned)lane <= (unsigned)r2 && ((e >> 8) & 0xffu) - (unsigned)py <= (unsigned)r2;
+                    c += inw ? 1u : 0u;
+                    if (c == k) {
+                        res = e >> 16;
+                        break;
+                    }
+                }
+            } else {
+                // weight of an entry = virtual cells of the window clamped onto it:
+                // [dx, dx] x [dy, dy] for an interior pixel, open-ended towards a border it lies on
+                for (int i = 0; i < nb; ++i) {
+                    const uint32_t e = bk[i];
+                    const int dx = (int)(e & 0xffu), dy = (int)((e >> 8) & 0xffu);
+                    const int xa = dx == dxL ? -1000 : dx, xz = dx == dxR ? 1000 : dx;
+                    const int ya = dy == dyT ? -1000 : dy, yz = dy == dyB ? 1000 : dy;
+                    const int wx = max(0, min(xz, lane + r2) - max(xa, lane) + 1);
+                    const int wy = max(0, min(yz, py + r2) - max(ya, py) + 1);
+                    c += (uint32_t)(wx * wy);
+                    if (c >= k) {
+                        res = e >> 16;
+                        break;
+                    }
+                }
+            }
+            dst[(int64_t)(yb + py - p.row_begin) * p.dst_pitch + xb + lane] = lut ? __ldg(lut + res) : (uint16_t)res;
+        }
+        __syncwarp();  // the buckets are reused by the next chunk
+        h0 = h1 + 1;
+    }
+}
+
+}  // namespace mtb

@@ -273,12 +273,16 @@ static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
     if (force == "colhist") return run_colhist16_u16(p, B, s, 1);
     if (force == "colhist16s") return run_colhist16s_u16(p, B, s);
     if (force == "colhist16c") return run_colhist16c_u16(p, B, s);
+    if (force == "lowsel") return run_lowsel16_u16(p, B, s);
+    // widely spread data: the candidate-list path where it applies (r = 3..63, not the streaming
+    // launch; MTB_U16_LIST=0 for comparison), else the candidate-run kernel up to r = 23, else the
+    // two-phase kernel without the window-keyed sweep
+    const bool list = lowsel16_applies(p) && env_int("MTB_U16_LIST", 1) != 0;
     const bool small_r = p.radius <= env_int("MTB_U16C_MAX_R", 23);
-    if (g_spread_hint >= 0) {
-        const bool wide = g_spread_hint > SPREAD_WIDE;
-        if (wide && small_r) return run_colhist16c_u16(p, B, s);
-        return run_colhist16_u16(p, B, s, wide ? 0 : 1);
-    }
+    auto run_wide = [&](const SlabParams &q) {
+        return list ? run_lowsel16_u16(q, B, s) : (small_r ? run_colhist16c_u16(q, B, s) : run_colhist16_u16(q, B, s, 0));
+    };
+    if (g_spread_hint >= 0) return g_spread_hint > SPREAD_WIDE ? run_wide(p) : run_colhist16_u16(p, B, s, 1);
     int *d_spread = nullptr;
     keep_pool_memory();
     if (cudaMallocAsync(reinterpret_cast<void **>(&d_spread), sizeof(int), s) != cudaSuccess)
@@ -289,18 +293,15 @@ static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
     int rc = e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string("k_highbyte_spread: ") + cudaGetErrorString(e));
     if (!rc) g_launches.fetch_add(1, std::memory_order_relaxed);
     p.spread = d_spread;
-    if (!rc && small_r) {
-        p.gate = GATE_WIDE;  // candidate kernel runs on widely spread data only
-        rc = run_colhist16c_u16(p, B, s);
-        p.gate = GATE_COMPACT;  // two-phase kernel (window-keyed sweep) otherwise
+    if (!rc) {
+        p.gate = GATE_WIDE;  // these launches exit at once unless the data is widely spread
+        rc = run_wide(p);
+        p.gate = GATE_COMPACT;  // compact data: the two-phase kernel with its window-keyed sweep
         if (!rc) rc = run_colhist16_u16(p, B, s, 1);
-        if (!rc) g_kernel = "k_colhist16c_u16|k_colhist16_u16 (device-selected)";
-    } else if (!rc) {
-        p.gate = GATE_WIDE;  // spread data: per-H phase-B sweeps
-        rc = run_colhist16_u16(p, B, s, 0);
-        p.gate = GATE_COMPACT;  // compact data: the window-keyed sweep
-        if (!rc) rc = run_colhist16_u16(p, B, s, 1);
-        if (!rc) g_kernel = "k_colhist16_u16 (device-selected)";
+        if (!rc)
+            g_kernel = list      ? "k_lowsel_u16|k_colhist16_u16 (device-selected)"
+                       : small_r ? "k_colhist16c_u16|k_colhist16_u16 (device-selected)"
+                                 : "k_colhist16_u16 (device-selected)";
     }
     cudaFreeAsync(d_spread, s);
     return rc;
@@ -312,6 +313,10 @@ constexpr int BANDMMA_MIN_R = 32;
 // smallest radius sent to the tcgen05 kernel k_bandtc_u8 (config 2: 0.58 ms against 0.63 for
 // k_bandmma_u8 at r = 80, 0.58 against 0.77 at r = 127; 0.59 against 0.54 at r = 72)
 constexpr int BANDTC_MIN_R = 76;
+// ... and only for launches of at least this many output pixels: its one round of wide CTAs leaves
+// SMs idle on small frames (r = 80: 1080p 0.175 ms against 0.133 for k_bandmma_u8, 1024^2 0.165
+// against 0.112; 2048^2 0.183 against 0.239 -- tools/small_frames.py)
+constexpr int64_t BANDTC_MIN_PIXELS = 3 << 20;
 
 template <typename P>
 static int run(SlabParams p, int B, cudaStream_t s) {
@@ -327,7 +332,7 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     //   median, r = 1 (16-bit)                    -> selection network (k_sortnet<3>)
     //   8-bit, r < 32 (any rank)                  -> column-histogram gather
     //   8-bit, 32 <= r <= 75                      -> band-matrix products on the tensor cores, mma.sync (k_bandmma_u8)
-    //   8-bit, 76 <= r <= 127                     -> the same with tcgen05.mma / tensor memory (k_bandtc_u8)
+    //   8-bit, 76 <= r <= 127, >= 3 Mpixel launches  -> the same with tcgen05.mma / tensor memory (k_bandtc_u8)
     //   (CTMF tiles, O(1) in r: MTB_KERNEL=ctmf only -- superseded by k_bandmma_u8)
     //   16-bit, n <= 255                          -> column histograms (two kernels, by value spread)
     //   otherwise (n > 255)                       -> per-column vertical histograms
@@ -338,7 +343,8 @@ static int run(SlabParams p, int B, cudaStream_t s) {
     if (sizeof(P) == 1 && n <= 255 && (force == "colhist" || (force.empty() && p.radius < BANDMMA_MIN_R)))
         return run_colhist_u8(p, B, s);
     if (sizeof(P) == 1 && n <= 255 && p.radius >= 1 &&
-        (force == "bandtc" || (force.empty() && p.radius >= BANDTC_MIN_R)))
+        (force == "bandtc" || (force.empty() && p.radius >= BANDTC_MIN_R &&
+                               (int64_t)(p.row_end - p.row_begin) * p.W * B >= BANDTC_MIN_PIXELS)))
         return run_bandtc_u8(p, B, s);
     if (sizeof(P) == 1 && n <= 255 && p.radius >= 1 && (force == "bandmma" || force.empty()))
         return run_bandmma_u8(p, B, s);

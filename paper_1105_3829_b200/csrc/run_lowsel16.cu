@@ -1,0 +1,73 @@
+// run_lowsel16.cu -- 16-bit, widely spread data: the candidate-list path.
+//   pass 1  k_colhist4p_u8<..., uint16_t>   high byte H and rank k' within it, per pixel
+//   pass 2  k_lowsel_u16                    low byte from a per-block candidate list
+//   pass 3  k_colhist16_u16 (todo-gated)    the blocks pass 2 flagged (locally compact data)
+// All three on the caller's stream; the scratch planes come from the
+// stream-ordered pool.
+#include <algorithm>
+
+#include "host.h"
+#include "kernels_lowsel16.cuh"
+
+namespace mtb {
+
+int run_hi16_fixed_a(SlabParams p, int B, cudaStream_t s);
+int run_hi16_fixed_b(SlabParams p, int B, cudaStream_t s);
+
+bool lowsel16_applies(const SlabParams &p) {
+    return !p.in_rows && p.radius >= LOWSEL_MIN_R && p.radius <= LOWSEL_MAX_R;
+}
+
+template <int PH>
+static int launch_lowsel(const SlabParams &p, int B, cudaStream_t s, const uint32_t *hk) {
+    dim3 grid((p.todo_nbx + LS_WARPS - 1) / LS_WARPS, p.todo_nby, B);
+    // buckets to start with: twice the mean count of one high byte on uniformly spread data
+    const int mean = (32 + 2 * p.radius) * (PH + 2 * p.radius) / 256;
+    int lg = LS_MINLG;
+    while (lg < LS_MAXLG && (1 << lg) < 2 * mean + 8) ++lg;
+    lg = std::min(LS_MAXLG, std::max(LS_MINLG, env_int("MTB_LS_LG", lg)));
+    k_lowsel_u16<PH><<<grid, 32 * LS_WARPS, 0, s>>>(p, hk, lg);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_lowsel_u16: ") + cudaGetErrorString(e));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return MTB_OK;
+}
+
+int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s) {
+    if (!lowsel16_applies(p)) return run_colhist16_u16(p, B, s, 0);
+    const int rows = p.row_end - p.row_begin;
+    // block height: taller blocks share the scan among more pixels, but widen
+    // the range of high bytes (longer lists)
+    const int ph = env_int("MTB_LS_PH", p.radius >= 24 ? 8 : 4);
+    const int PH = ph >= 16 ? 16 : (ph >= 8 ? 8 : 4);
+    p.todo_bh = PH;
+    p.todo_nbx = (p.W + 31) / 32;
+    p.todo_nby = (rows + PH - 1) / PH;
+    const size_t hk_bytes = (size_t)rows * p.W * B * sizeof(uint32_t);
+    const size_t flag_bytes = (size_t)p.todo_nbx * p.todo_nby * B;
+    unsigned char *scratch = nullptr;
+    keep_pool_memory();
+    if (cudaMallocAsync(reinterpret_cast<void **>(&scratch), hk_bytes + flag_bytes, s) != cudaSuccess)
+        return fail(MTB_E_CUDA, "k_lowsel_u16: scratch allocation failed");
+    uint32_t *hk = reinterpret_cast<uint32_t *>(scratch);
+    p.todo = scratch + hk_bytes;
+    cudaMemsetAsync(p.todo, 0, flag_bytes, s);
+
+    SlabParams a = p;  // pass 1 writes H << 16 | k' words
+    a.dst = hk;
+    a.dst_pitch = p.W;
+    a.dst_img_stride = (int64_t)rows * p.W;
+    a.lut = nullptr;
+    a.todo = nullptr;
+    int rc = run_hi16_fixed_a(a, B, s);
+    if (rc == 1) rc = run_hi16_fixed_b(a, B, s);
+    if (rc == 1) rc = fail(MTB_E_INVAL, "k_lowsel_u16: radius outside the candidate-list path");
+    if (!rc) rc = PH == 16 ? launch_lowsel<16>(p, B, s, hk) : (PH == 8 ? launch_lowsel<8>(p, B, s, hk) : launch_lowsel<4>(p, B, s, hk));
+    // pass 3: flagged blocks are locally compact, where the window-keyed sweep pays
+    if (!rc) rc = run_colhist16_u16(p, B, s, 1);
+    cudaFreeAsync(scratch, s);
+    if (!rc) g_kernel = "k_lowsel_u16";
+    return rc;
+}
+
+}  // namespace mtb
