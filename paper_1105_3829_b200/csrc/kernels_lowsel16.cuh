@@ -40,27 +40,20 @@ constexpr int LS_CAP = 512;    // bucket entries per warp (NB buckets x BCAP)
 constexpr int LS_MAXLG = 9;    // log2 of the largest bucket (one high byte per chunk)
 constexpr int LS_MINLG = 4;    // log2 of the smallest bucket (32 high bytes per chunk)
 
-// hk: [image][row - row_begin][x] words H << 16 | k' (pitch W); PH output rows
-// per block; lg0: log2 of the bucket size to start with
-template <int PH>
-__global__ void __launch_bounds__(32 * LS_WARPS) k_lowsel_u16(SlabParams p, const uint32_t *__restrict__ hk, int lg0) {
-    __shared__ uint32_t bufs[LS_WARPS][LS_CAP];  // buckets as scanned
-    __shared__ uint32_t srts[LS_WARPS][LS_CAP];  // buckets sorted
-    __shared__ int bcnts[LS_WARPS][32];          // entries per bucket
-    if (gate_off(p)) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// One block: the 32 x PH output pixels at columns xb.., block row `by` of image
+// blockIdx.z; called by a whole warp.  buf / srt / bcnt: the warp's buckets.
+template <int PH, int NI>
+__device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__restrict__ hk, int lg0, int xb, int by,
+                                         uint32_t *buf, uint32_t *srt, int *bcnt) {
+    const int lane = threadIdx.x & 31;
     const int r = p.radius, r2 = 2 * r, W = p.W, H = p.H;
-    const int xb = (blockIdx.x * LS_WARPS + warp) * 32;  // first output column of the block
-    if (xb >= W) return;                                  // (warp-uniform; the kernel has no CTA barriers)
-    const int yb = p.row_begin + blockIdx.y * PH;
+    const int yb = p.row_begin + by * PH;
     const int ph = min(PH, p.row_end - yb);
     const int rows = p.row_end - p.row_begin;
     const uint16_t *src = static_cast<const uint16_t *>(p.src) + blockIdx.z * p.src_img_stride;
     uint16_t *dst = static_cast<uint16_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint16_t *lut = static_cast<const uint16_t *>(p.lut);
     const uint32_t *hkp = hk + ((int64_t)blockIdx.z * rows + (yb - p.row_begin)) * W + xb + lane;
-    uint32_t *buf = bufs[warp], *srt = srts[warp];
-    int *bcnt = bcnts[warp];
     const bool valid = xb + lane < W;
 
     // ---- the block's (H, k') and the range of H
@@ -92,10 +85,15 @@ __global__ void __launch_bounds__(32 * LS_WARPS) k_lowsel_u16(SlabParams p, cons
     // image borders in window coordinates (out of reach when the border is not in the union)
     const int dxL = xb - r <= 0 ? r - xb : -1000, dxR = xb + 31 + r >= W - 1 ? W - 1 - xb + r : 1000;
     const int dyT = yb - r <= 0 ? r - yb : -1000, dyB = yb + ph - 1 + r >= H - 1 ? H - 1 - yb + r : 1000;
-    constexpr int NI = 5;  // column steps of 32: UW <= 158 (r <= 63)
     int gx[NI];
+    unsigned okc = 0;  // bit i: this lane's column of step i is inside the image
 #pragma unroll
-    for (int i = 0; i < NI; ++i) gx[i] = clampi(xb - r + lane + 32 * i, 0, W - 1);
+    for (int i = 0; i < NI; ++i) {
+        const int c = lane + 32 * i;
+        gx[i] = clampi(xb - r + c, 0, W - 1);
+        okc |= (c >= cL && c <= cR) ? 1u << i : 0u;
+    }
+    const uint16_t *row0 = src_row(p, src, yb - r + jT);
 
     int lg = lg0;
     for (int h0 = hmin; h0 <= hmax;) {
@@ -111,26 +109,33 @@ __global__ void __launch_bounds__(32 * LS_WARPS) k_lowsel_u16(SlabParams p, cons
         }
         bcnt[lane] = 0;
         __syncwarp();
-        // ---- scan
-        for (int j = jT; j <= jB; ++j) {
-            const uint16_t *row = src_row(p, src, yb - r + j);
+        // ---- scan, two rows per step (all loads of a step in flight together)
+        auto drop = [&](unsigned v, int j, int i) {
+            const unsigned b = (v >> 8) - (unsigned)h0;
+            if (((okc >> i) & 1u) && b <= hspan) {
+                const int slot = atomicAdd(bcnt + b, 1);
+                if (slot < BCAP) buf[(b << lg) + slot] = (v << 16) | ((unsigned)j << 8) | (unsigned)(lane + 32 * i);
+            }
+        };
+        const uint16_t *row = row0;
+        for (int j = jT; j <= jB; j += 2, row += 2 * p.src_pitch) {
+            const bool two = j < jB;
+            unsigned v0[NI], v1[NI];
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
-                if (32 * i < UW) {  // (warp-uniform)
-                    const int c = lane + 32 * i;
-                    const unsigned v = __ldg(row + gx[i]);
-                    const unsigned b = (v >> 8) - (unsigned)h0;
-                    if (c >= cL && c <= cR && b <= hspan) {
-                        const int slot = atomicAdd(bcnt + b, 1);
-                        if (slot < BCAP) buf[(b << lg) + slot] = (v << 16) | ((unsigned)j << 8) | (unsigned)c;
-                    }
-                }
+                v0[i] = __ldg(row + gx[i]);
+                v1[i] = two ? (unsigned)__ldg(row + p.src_pitch + gx[i]) : 0xffffffffu;  // (no bucket)
             }
+#pragma unroll
+            for (int i = 0; i < NI; ++i) drop(v0[i], j, i);
+#pragma unroll
+            for (int i = 0; i < NI; ++i) drop(v1[i], j + 1, i);
         }
         __syncwarp();
         if (__any_sync(0xffffffffu, bcnt[lane] > BCAP)) {
             if (lg == LS_MAXLG) {  // locally compact data: leave the block to the two-phase kernel
-                if (lane == 0) p.todo[((size_t)blockIdx.z * p.todo_nby + blockIdx.y) * p.todo_nbx + (xb >> 5)] = 1;
+                if (lane == 0) p.todo[((size_t)blockIdx.z * p.todo_nby + by) * p.todo_nbx + (xb >> 5)] = 1;
+                __syncwarp();
                 return;
             }
             ++lg;  // larger buckets, fewer high bytes per chunk; repeat from h0
@@ -160,14 +165,19 @@ __global__ void __launch_bounds__(32 * LS_WARPS) k_lowsel_u16(SlabParams p, cons
             const int nb = bcnt[b];
             uint32_t c = 0, res = 0;
             if (!border) {
-                for (int i = 0; i < nb; ++i) {
-                    const uint32_t e = bk[i];
-                    const bool inw = (e & 0xffu) - (unsigned)lane <= (unsigned)r2 && ((e >> 8) & 0xffu) - (unsigned)py <= (unsigned)r2;
-                    c += inw ? 1u : 0u;
-                    if (c == k) {
-                        res = e >> 16;
+                // two entries per step (buckets are 64-byte aligned; an odd bucket's last
+                // partner is not counted)
+                for (int i = 0; i < nb; i += 2) {
+                    const uint2 ee = *reinterpret_cast<const uint2 *>(bk + i);
+                    const bool in0 = (ee.x & 0xffu) - (unsigned)lane <= (unsigned)r2 && ((ee.x >> 8) & 0xffu) - (unsigned)py <= (unsigned)r2;
+                    const bool in1 = i + 1 < nb && (ee.y & 0xffu) - (unsigned)lane <= (unsigned)r2 &&
+                                     ((ee.y >> 8) & 0xffu) - (unsigned)py <= (unsigned)r2;
+                    const uint32_t c0 = c + (in0 ? 1u : 0u), c1 = c0 + (in1 ? 1u : 0u);
+                    if (c1 >= k) {  // (c < k before: the first of the two to reach k)
+                        res = (c0 == k ? ee.x : ee.y) >> 16;
                         break;
                     }
+                    c = c1;
                 }
             } else {
                 // weight of an entry = virtual cells of the window clamped onto it:
@@ -190,6 +200,29 @@ __global__ void __launch_bounds__(32 * LS_WARPS) k_lowsel_u16(SlabParams p, cons
         }
         __syncwarp();  // the buckets are reused by the next chunk
         h0 = h1 + 1;
+    }
+}
+
+// hk: [image][row - row_begin][x] words H << 16 | k' (pitch W); PH output rows
+// per block; NI = ceil((32 + 2r) / 32) column steps of the scan; lg0: log2 of
+// the bucket size to start with.  A CTA takes `seg` vertically adjacent block
+// rows of its 256 columns (grid.y = ceil(block rows / seg)): consecutive
+// blocks share all but PH of their PH + 2r source rows in L1, and a gated
+// launch that has nothing to do (compact data) is a few thousand CTAs, not
+// one per block row.
+template <int PH, int NI>
+__global__ void __launch_bounds__(32 * LS_WARPS, 4) k_lowsel_u16(SlabParams p, const uint32_t *__restrict__ hk, int lg0, int seg) {
+    __shared__ uint32_t bufs[LS_WARPS][LS_CAP];  // buckets as scanned
+    __shared__ uint32_t srts[LS_WARPS][LS_CAP];  // buckets sorted
+    __shared__ int bcnts[LS_WARPS][32];          // entries per bucket
+    if (gate_off(p)) return;
+    const int warp = threadIdx.x >> 5;
+    const int xb = (blockIdx.x * LS_WARPS + warp) * 32;  // first output column of the warp's blocks
+    if (xb >= p.W) return;                                // (warp-uniform; the kernel has no CTA barriers)
+    const int by1 = min((int)(blockIdx.y + 1) * seg, p.todo_nby);
+    for (int by = blockIdx.y * seg; by < by1; ++by) {
+        ls_block<PH, NI>(p, hk, lg0, xb, by, bufs[warp], srts[warp], bcnts[warp]);
+        __syncwarp();  // the buckets are reused by the next block
     }
 }
 

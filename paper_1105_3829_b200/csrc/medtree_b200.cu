@@ -742,7 +742,11 @@ static int host_pipeline(const void *src, void *dst, int bit_depth, int H, int W
     // the bands, whose launches never wait on copies.  MTB_HOST_STREAM=0/1
     // forces.
     const int stream_mode = env_int("MTB_HOST_STREAM", -1);
-    const bool want_stream = (stream_mode < 0 ? radius >= 12 : stream_mode != 0) && host_pinned(src);
+    // (widely spread 16-bit frames take the bands: the candidate-bucket path, several launches
+    // over scratch planes, has no streaming form and is 2-5x faster than the kernels that do)
+    const bool list16 = bit_depth == 16 && g_spread_hint > SPREAD_WIDE && radius >= LOWSEL_MIN_R &&
+                        radius <= LOWSEL_MAX_R && env_int("MTB_U16_LIST", 1) != 0;
+    const bool want_stream = (stream_mode < 0 ? radius >= 12 && !list16 : stream_mode != 0) && host_pinned(src);
     if (want_stream) {
         const int rs = host_stream(ctx, j);
         if (rs != 1) return rs;
@@ -982,8 +986,14 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
         unsigned int *fl = ctx->dflags + j * FramesCtx::NFLAGS;
         // smode 1: every frame streams; 2: the first and last (the copies
         // nothing else hides); 3: the last only
-        const bool streaming = can_stream && (smode == 1 || (smode == 2 && (q == 0 || q == n - 1)) ||
-                                              (smode == 3 && q == n - 1) || (smode == 4 && q == 0));
+        // (16-bit kernel choice from the host frame; widely spread frames in the candidate-bucket
+        // path's radii do not stream -- that path has no streaming form)
+        const int hint = bit_depth == 16 ? spread_distinct_host(static_cast<const uint16_t *>(srcs[i]), W, H, W) : -1;
+        const bool list16 = hint > SPREAD_WIDE && radii[i] >= LOWSEL_MIN_R && radii[i] <= LOWSEL_MAX_R &&
+                            env_int("MTB_U16_LIST", 1) != 0;
+        const bool streaming = can_stream && !list16 &&
+                               (smode == 1 || (smode == 2 && (q == 0 || q == n - 1)) ||
+                                (smode == 3 && q == n - 1) || (smode == 4 && q == 0));
         if (q >= NB) cudaStreamWaitEvent(ctx->sh, ctx->ek[j], 0);  // job i-NB done reading dsrc[j]
         if (streaming) {
             // counters reset before this frame's kernel or copy-out can look
@@ -1013,8 +1023,7 @@ static int host_frames(const void *const *srcs, void *const *dsts, const int32_t
         if (rc) break;
         cudaStreamWaitEvent(ctx->sc, ctx->ein[j], 0);
         if (q >= NB) cudaStreamWaitEvent(ctx->sc, ctx->eout[j], 0);  // job i-NB's result copied out
-        if (bit_depth == 16)
-            g_spread_hint = spread_distinct_host(static_cast<const uint16_t *>(srcs[i]), W, H, W);
+        g_spread_hint = hint;
         SlabParams p = make_params(ctx->dsrc[j], W, 0, H, ctx->ddst[j], W, H, W, 0, H, radii[i],
                                    ranks ? ranks[i] : 0, lut ? ctx->dlut : nullptr);
         if (!ranks) {

@@ -5,6 +5,7 @@
 // All three on the caller's stream; the scratch planes come from the
 // stream-ordered pool.
 #include <algorithm>
+#include <cmath>
 
 #include "host.h"
 #include "kernels_lowsel16.cuh"
@@ -18,19 +19,38 @@ bool lowsel16_applies(const SlabParams &p) {
     return !p.in_rows && p.radius >= LOWSEL_MIN_R && p.radius <= LOWSEL_MAX_R;
 }
 
-template <int PH>
-static int launch_lowsel(const SlabParams &p, int B, cudaStream_t s, const uint32_t *hk) {
-    dim3 grid((p.todo_nbx + LS_WARPS - 1) / LS_WARPS, p.todo_nby, B);
-    // buckets to start with: twice the mean count of one high byte on uniformly spread data
-    const int mean = (32 + 2 * p.radius) * (PH + 2 * p.radius) / 256;
+template <int PH, int NI>
+static int launch_lowsel_ni(const SlabParams &p, int B, cudaStream_t s, const uint32_t *hk) {
+    // a CTA takes `seg` vertically adjacent block rows.  One block row per CTA schedules best
+    // (config 3 r = 31: 1.38 / 1.43 / 1.57 ms at seg = 1 / 2 / 4: the blocks' costs vary); larger
+    // launches take more, so that a gated launch with nothing to do (compact data, device-selected
+    // dispatch) stays at <= 16 K CTAs to retire
+    const int gx = (p.todo_nbx + LS_WARPS - 1) / LS_WARPS;
+    const int64_t want = 16384;
+    const int seg = std::max(1, env_int("MTB_LS_SEG", (int)(((int64_t)gx * p.todo_nby * B + want - 1) / want)));
+    dim3 grid(gx, (p.todo_nby + seg - 1) / seg, B);
+    // buckets to start with: the mean count of one high byte on uniformly spread data plus four
+    // standard deviations (an overflowing chunk is repeated with larger buckets; config 3 r = 23
+    // 1.30 -> 1.12 ms against twice the mean)
+    const double mean = (32 + 2 * p.radius) * (PH + 2 * p.radius) / 256.0;
     int lg = LS_MINLG;
-    while (lg < LS_MAXLG && (1 << lg) < 2 * mean + 8) ++lg;
+    while (lg < LS_MAXLG && (1 << lg) < mean + 4.0 * std::sqrt(mean)) ++lg;
     lg = std::min(LS_MAXLG, std::max(LS_MINLG, env_int("MTB_LS_LG", lg)));
-    k_lowsel_u16<PH><<<grid, 32 * LS_WARPS, 0, s>>>(p, hk, lg);
+    k_lowsel_u16<PH, NI><<<grid, 32 * LS_WARPS, 0, s>>>(p, hk, lg, seg);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_lowsel_u16: ") + cudaGetErrorString(e));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return MTB_OK;
+}
+
+template <int PH>
+static int launch_lowsel(const SlabParams &p, int B, cudaStream_t s, const uint32_t *hk) {
+    switch ((32 + 2 * p.radius + 31) / 32) {  // column steps of the scan
+        case 2: return launch_lowsel_ni<PH, 2>(p, B, s, hk);
+        case 3: return launch_lowsel_ni<PH, 3>(p, B, s, hk);
+        case 4: return launch_lowsel_ni<PH, 4>(p, B, s, hk);
+        default: return launch_lowsel_ni<PH, 5>(p, B, s, hk);
+    }
 }
 
 int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s) {
@@ -38,8 +58,7 @@ int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s) {
     const int rows = p.row_end - p.row_begin;
     // block height: taller blocks share the scan among more pixels, but widen
     // the range of high bytes (longer lists)
-    const int ph = env_int("MTB_LS_PH", p.radius >= 24 ? 8 : 4);
-    const int PH = ph >= 16 ? 16 : (ph >= 8 ? 8 : 4);
+    const int PH = env_int("MTB_LS_PH", 8) >= 8 ? 8 : 4;
     p.todo_bh = PH;
     p.todo_nbx = (p.W + 31) / 32;
     p.todo_nby = (rows + PH - 1) / PH;
@@ -62,7 +81,7 @@ int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s) {
     int rc = run_hi16_fixed_a(a, B, s);
     if (rc == 1) rc = run_hi16_fixed_b(a, B, s);
     if (rc == 1) rc = fail(MTB_E_INVAL, "k_lowsel_u16: radius outside the candidate-list path");
-    if (!rc) rc = PH == 16 ? launch_lowsel<16>(p, B, s, hk) : (PH == 8 ? launch_lowsel<8>(p, B, s, hk) : launch_lowsel<4>(p, B, s, hk));
+    if (!rc) rc = PH == 8 ? launch_lowsel<8>(p, B, s, hk) : launch_lowsel<4>(p, B, s, hk);
     // pass 3: flagged blocks are locally compact, where the window-keyed sweep pays
     if (!rc) rc = run_colhist16_u16(p, B, s, 1);
     cudaFreeAsync(scratch, s);

@@ -406,7 +406,7 @@ def test_full_size_off_centre_ranks():
 _FAMILY_CASES = [c for c in G.small_cases() if c[0]["rank"] is None and c[0]["percentile"] is None]
 
 
-@pytest.mark.parametrize("family", ["vert", "ctmf", "bandmma", "bandtc", "sortnet", "colhist", "colhist16s", "colhist16c"])
+@pytest.mark.parametrize("family", ["vert", "ctmf", "bandmma", "bandtc", "sortnet", "colhist", "colhist16s", "colhist16c", "lowsel"])
 def test_each_kernel_family_is_exact(family, monkeypatch):
     """MTB_KERNEL forces one family; families that do not apply to a case
     (ctmf: 8-bit only; sortnet: median of n <= 7) fall through to the
@@ -430,7 +430,7 @@ def test_each_kernel_family_is_exact(family, monkeypatch):
         out16 = mtb.rank_filter(torch.from_numpy(px16).cuda(), min(r, 34)).cpu().numpy()
         assert np.array_equal(out16, O.iot_filter(px16, 2 * min(r, 34) + 1)), (family, r)
     expect = {"vert": "k_vert_u8", "ctmf": "k_ctmf_u8", "bandmma": "k_bandmma_u8", "bandtc": "k_bandtc_u8", "sortnet": "k_sortnet", "colhist": "k_colhist_u8",
-              "colhist16s": "k_colhist16s_u16", "colhist16c": "k_colhist16c_u16"}[family]
+              "colhist16s": "k_colhist16s_u16", "colhist16c": "k_colhist16c_u16", "lowsel": "k_lowsel_u16"}[family]
     assert expect in seen, seen
 
 
@@ -553,6 +553,86 @@ def test_colhist16_sorted_span_kernels(kind, family, monkeypatch):
             expect = "k_colhist16_u16" if fallback else f"k_{family}_u16"
             assert _lib.last_kernel() == expect, _lib.last_kernel()
             assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (kind, r, rank)
+
+
+def _lowsel_frames(rng, h, w):
+    """Spread, compact, mixed (spread with a compact band and a saturated
+    corner: blocks whose buckets overflow go to the two-phase kernel) and
+    12-bit-in-16 frames."""
+    noise = rng.integers(0, 65536, (h, w)).astype(np.uint16)
+    compact = (30000 + rng.normal(0, 300, (h, w))).clip(0, 65535).astype(np.uint16)
+    mixed = noise.copy()
+    mixed[:, w // 3: 2 * w // 3] = compact[:, w // 3: 2 * w // 3]
+    mixed[h // 2:, : w // 4] = 65535
+    twelve = (rng.integers(0, 4096, (h, w)) * 16).astype(np.uint16)
+    return {"noise": noise, "compact": compact, "mixed": mixed, "twelve": twelve}
+
+
+@pytest.mark.parametrize("ph", ["4", "8"])
+@pytest.mark.parametrize("kind", ["noise", "compact", "mixed", "twelve"])
+def test_lowsel_u16_candidate_buckets(kind, ph, monkeypatch):
+    """The 16-bit candidate-bucket path (high-byte pair records ->
+    k_lowsel_u16 -> todo-gated k_colhist16_u16) on ragged frames: radii over
+    every column-step count of the scan (2..5) and both pair-record layouts
+    of the first pass, min / max / off-centre ranks, frames narrower than a
+    block and lower than a block row, the clamped borders (weighted border
+    entries) and data whose buckets overflow."""
+    from paper_1105_3829_b200 import _lib
+
+    monkeypatch.setenv("MTB_KERNEL", "lowsel")
+    monkeypatch.setenv("MTB_LS_PH", ph)
+    rng = np.random.default_rng(123)
+    for (h, w) in ((97, 333), (300, 64), (5, 20), (131, 257)):
+        px = _lowsel_frames(rng, h, w)[kind]
+        src = torch.from_numpy(px).cuda()
+        for r in (3, 4, 7, 15, 16, 17, 24, 32, 40, 49, 63):
+            n = 2 * r + 1
+            if n > 2 * min(h, w) + 1:
+                continue
+            for rank in (None, 1, n * n, (n * n) // 3 + 1):
+                out = mtb.rank_filter(src, r, rank=rank).cpu().numpy()
+                assert _lib.last_kernel() == "k_lowsel_u16", _lib.last_kernel()
+                assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (kind, h, w, r, rank)
+    # outside its radii the family falls back to the two-phase kernel
+    px = _lowsel_frames(rng, 70, 90)[kind]
+    for r in (2, 64):
+        out = mtb.rank_filter(torch.from_numpy(px).cuda(), r, rank=5).cpu().numpy()
+        assert _lib.last_kernel() == "k_colhist16_u16", _lib.last_kernel()
+        assert np.array_equal(out, O.iot_filter(px, 2 * r + 1, rank=5)), (kind, r)
+
+
+@pytest.mark.parametrize("lg", ["4", "9"])
+def test_lowsel_u16_bucket_sizes_batch_slab_and_lut(lg, monkeypatch):
+    """k_lowsel_u16 starting from the smallest buckets (every chunk of a
+    wide window overflows and is repeated with larger ones) and from the
+    largest (one high byte per chunk); the batch entry (per-image scratch
+    planes and flags), a row slab with a pitched output, a value map, and
+    the default device-selected dispatch on a batch that mixes spread and
+    compact images."""
+    from paper_1105_3829_b200 import _lib
+
+    monkeypatch.setenv("MTB_LS_LG", lg)
+    rng = np.random.default_rng(321)
+    frames = _lowsel_frames(rng, 120, 200)
+    stack = np.stack(list(frames.values()))
+    out = mtb.rank_filter(torch.from_numpy(stack).cuda(), 9).cpu().numpy()
+    assert "k_lowsel_u16" in _lib.last_kernel(), _lib.last_kernel()
+    for i in range(stack.shape[0]):
+        assert np.array_equal(out[i], O.iot_filter(stack[i], 19)), i
+    monkeypatch.setenv("MTB_KERNEL", "lowsel")
+    for r in (6, 31):
+        n = 2 * r + 1
+        out = mtb.rank_filter(torch.from_numpy(stack).cuda(), r).cpu().numpy()
+        for i in range(stack.shape[0]):
+            assert np.array_equal(out[i], O.iot_filter(stack[i], n)), (r, i)
+        px = frames["mixed"]
+        ref = O.iot_filter(px, n)
+        big = torch.zeros((120, 240), dtype=torch.uint16, device="cuda")
+        sl = mtb.rank_filter(torch.from_numpy(px).cuda(), r, rows=(19, 77), out=big[19:77, :200])
+        assert np.array_equal(sl.cpu().numpy(), ref[19:77]), r
+        lut = torch.from_numpy((np.arange(65536) & ~np.uint32(15)).astype(np.uint16)).cuda()
+        q = mtb.rank_filter(torch.from_numpy(px).cuda(), r, lut=lut).cpu().numpy()
+        assert np.array_equal(q, ref & ~np.uint16(15)), r
 
 
 # ------------------------------------------ 3x3 kernels (k_med3_u8 / k_med3t_u8)
