@@ -18,7 +18,7 @@ cp gpurun_out/ncu_issue_manifest.json $out/ 2>/dev/null
 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-extra > $out/launch_plain.log 2>&1 &&
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-extra > $out/launch_ncu.log 2>&1
-for spec in "cfg2_r63 2 63 k_bandmma" "cfg2_r100 2 100 k_bandtc"; do
+for spec in "cfg2_r63 2 63 k_bandmma" "cfg2_r100 2 100 k_bandtc" "cfg3_r31 3 31 k_lowsel" "cfg3_r15 3 15 k_lowsel" "cfg3_r31hi 3 31 k_colhist4p"; do
   set -- $spec
   python tools/one_launch.py $2 $3 > /dev/null 2>&1 &&
     ncu --set full --import-source on --clock-control none -k regex:$4 -s 1 -c 1 -o $out/prof_$1 \
