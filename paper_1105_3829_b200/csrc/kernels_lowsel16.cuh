@@ -42,10 +42,7 @@ constexpr int LS_MINLG = 4;    // log2 of the smallest bucket (32 high bytes per
 
 // One block: the 32 x PH output pixels at columns xb.., block row `by` of image
 // blockIdx.z; called by a whole warp.  buf / srt / bcnt: the warp's buckets.
-// VEC: the scan loads pixel PAIRS (one 32-bit load per two columns; NI counts
-// steps of 32 pairs): needs an even width and 4-byte aligned rows, and starts
-// the union at an even column (one column early when r is odd).
-template <int PH, int NI, bool VEC>
+template <int PH, int NI>
 __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__restrict__ hk, int lg0, int xb, int by,
                                          uint32_t *buf, uint32_t *srt, int *bcnt) {
     const int lane = threadIdx.x & 31;
@@ -81,31 +78,20 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
     // dy in [jT, jB]); a border pixel stands for every virtual cell clamped
     // onto it, and the walk below weighs it by how many of those lie in the
     // pixel's window.
-    const int odd = VEC ? (r & 1) : 0;  // union origin xo = xb - r - odd; a window starts at dx = lane + odd
-    const int xo = xb - r - odd, lx = lane + odd;
-    const int UW = 32 + r2 + odd, UH = ph + r2;
-    const int cL = max(odd, -xo), cR = min(UW - 1, W - 1 - xo);
+    const int UW = 32 + r2, UH = ph + r2;
+    const int cL = max(0, r - xb), cR = min(UW - 1, W - 1 - xb + r);
     const int jT = max(0, r - yb), jB = min(UH - 1, H - 1 - yb + r);
-    const bool border = cL > odd || cR < UW - 1 || jT > 0 || jB < UH - 1;  // (warp-uniform)
+    const bool border = cL > 0 || cR < UW - 1 || jT > 0 || jB < UH - 1;  // (warp-uniform)
     // image borders in window coordinates (out of reach when the border is not in the union)
-    const int dxL = xo + odd <= 0 ? -xo : -1000, dxR = xo + UW - 1 >= W - 1 ? W - 1 - xo : 1000;
+    const int dxL = xb - r <= 0 ? r - xb : -1000, dxR = xb + 31 + r >= W - 1 ? W - 1 - xb + r : 1000;
     const int dyT = yb - r <= 0 ? r - yb : -1000, dyB = yb + ph - 1 + r >= H - 1 ? H - 1 - yb + r : 1000;
-    // this lane's columns (VEC: column pairs) of every step: element offset in a
-    // row, and whether each column is inside the image
     int gx[NI];
-    unsigned okc = 0;  // bit i (VEC: bits 2i, 2i + 1)
+    unsigned okc = 0;  // bit i: this lane's column of step i is inside the image
 #pragma unroll
     for (int i = 0; i < NI; ++i) {
-        if (VEC) {
-            const int c = 2 * (lane + 32 * i);
-            gx[i] = clampi(xo + c, 0, W - 2);  // (even: xo and W are)
-            okc |= (c >= cL && c <= cR) ? 1u << (2 * i) : 0u;
-            okc |= (c + 1 >= cL && c + 1 <= cR) ? 2u << (2 * i) : 0u;
-        } else {
-            const int c = lane + 32 * i;
-            gx[i] = clampi(xo + c, 0, W - 1);
-            okc |= (c >= cL && c <= cR) ? 1u << i : 0u;
-        }
+        const int c = lane + 32 * i;
+        gx[i] = clampi(xb - r + c, 0, W - 1);
+        okc |= (c >= cL && c <= cR) ? 1u << i : 0u;
     }
     const uint16_t *row0 = src_row(p, src, yb - r + jT);
 
@@ -124,22 +110,11 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
         bcnt[lane] = 0;
         __syncwarp();
         // ---- scan, two rows per step (all loads of a step in flight together)
-        auto drop = [&](unsigned v, int j, int bit, int c) {
+        auto drop = [&](unsigned v, int j, int i) {
             const unsigned b = (v >> 8) - (unsigned)h0;
-            if (((okc >> bit) & 1u) && b <= hspan) {
+            if (((okc >> i) & 1u) && b <= hspan) {
                 const int slot = atomicAdd(bcnt + b, 1);
-                if (slot < BCAP) buf[(b << lg) + slot] = (v << 16) | ((unsigned)j << 8) | (unsigned)c;
-            }
-        };
-        auto load = [&](const uint16_t *rw, int i) -> unsigned {
-            return VEC ? __ldg(reinterpret_cast<const unsigned *>(rw + gx[i])) : (unsigned)__ldg(rw + gx[i]);
-        };
-        auto drop_step = [&](unsigned v, int j, int i) {
-            if (VEC) {
-                drop(v & 0xffffu, j, 2 * i, 2 * (lane + 32 * i));
-                drop(v >> 16, j, 2 * i + 1, 2 * (lane + 32 * i) + 1);
-            } else {
-                drop(v, j, i, lane + 32 * i);
+                if (slot < BCAP) buf[(b << lg) + slot] = (v << 16) | ((unsigned)j << 8) | (unsigned)(lane + 32 * i);
             }
         };
         const uint16_t *row = row0;
@@ -148,13 +123,13 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
             unsigned v0[NI], v1[NI];
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
-                v0[i] = load(row, i);
-                v1[i] = two ? load(row + p.src_pitch, i) : 0xffffffffu;  // (no bucket)
+                v0[i] = __ldg(row + gx[i]);
+                v1[i] = two ? (unsigned)__ldg(row + p.src_pitch + gx[i]) : 0xffffffffu;  // (no bucket)
             }
 #pragma unroll
-            for (int i = 0; i < NI; ++i) drop_step(v0[i], j, i);
+            for (int i = 0; i < NI; ++i) drop(v0[i], j, i);
 #pragma unroll
-            for (int i = 0; i < NI; ++i) drop_step(v1[i], j + 1, i);
+            for (int i = 0; i < NI; ++i) drop(v1[i], j + 1, i);
         }
         __syncwarp();
         if (__any_sync(0xffffffffu, bcnt[lane] > BCAP)) {
@@ -194,8 +169,8 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
                 // partner is not counted)
                 for (int i = 0; i < nb; i += 2) {
                     const uint2 ee = *reinterpret_cast<const uint2 *>(bk + i);
-                    const bool in0 = (ee.x & 0xffu) - (unsigned)lx <= (unsigned)r2 && ((ee.x >> 8) & 0xffu) - (unsigned)py <= (unsigned)r2;
-                    const bool in1 = i + 1 < nb && (ee.y & 0xffu) - (unsigned)lx <= (unsigned)r2 &&
+                    const bool in0 = (ee.x & 0xffu) - (unsigned)lane <= (unsigned)r2 && ((ee.x >> 8) & 0xffu) - (unsigned)py <= (unsigned)r2;
+                    const bool in1 = i + 1 < nb && (ee.y & 0xffu) - (unsigned)lane <= (unsigned)r2 &&
                                      ((ee.y >> 8) & 0xffu) - (unsigned)py <= (unsigned)r2;
                     const uint32_t c0 = c + (in0 ? 1u : 0u), c1 = c0 + (in1 ? 1u : 0u);
                     if (c1 >= k) {  // (c < k before: the first of the two to reach k)
@@ -212,7 +187,7 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
                     const int dx = (int)(e & 0xffu), dy = (int)((e >> 8) & 0xffu);
                     const int xa = dx == dxL ? -1000 : dx, xz = dx == dxR ? 1000 : dx;
                     const int ya = dy == dyT ? -1000 : dy, yz = dy == dyB ? 1000 : dy;
-                    const int wx = max(0, min(xz, lx + r2) - max(xa, lx) + 1);
+                    const int wx = max(0, min(xz, lane + r2) - max(xa, lane) + 1);
                     const int wy = max(0, min(yz, py + r2) - max(ya, py) + 1);
                     c += (uint32_t)(wx * wy);
                     if (c >= k) {
@@ -229,13 +204,13 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
 }
 
 // hk: [image][row - row_begin][x] words H << 16 | k' (pitch W); PH output rows
-// per block; NI = column steps of the scan (32 columns, VEC: 32 column pairs
-// each); lg0: log2 of the bucket size to start with.  A CTA takes `seg` vertically adjacent block
+// per block; NI = ceil((32 + 2r) / 32) column steps of the scan; lg0: log2 of
+// the bucket size to start with.  A CTA takes `seg` vertically adjacent block
 // rows of its 256 columns (grid.y = ceil(block rows / seg)): consecutive
 // blocks share all but PH of their PH + 2r source rows in L1, and a gated
 // launch that has nothing to do (compact data) is a few thousand CTAs, not
 // one per block row.
-template <int PH, int NI, bool VEC>
+template <int PH, int NI>
 __global__ void __launch_bounds__(32 * LS_WARPS, 4) k_lowsel_u16(SlabParams p, const uint32_t *__restrict__ hk, int lg0, int seg) {
     __shared__ uint32_t bufs[LS_WARPS][LS_CAP];  // buckets as scanned
     __shared__ uint32_t srts[LS_WARPS][LS_CAP];  // buckets sorted
@@ -246,7 +221,7 @@ __global__ void __launch_bounds__(32 * LS_WARPS, 4) k_lowsel_u16(SlabParams p, c
     if (xb >= p.W) return;                                // (warp-uniform; the kernel has no CTA barriers)
     const int by1 = min((int)(blockIdx.y + 1) * seg, p.todo_nby);
     for (int by = blockIdx.y * seg; by < by1; ++by) {
-        ls_block<PH, NI, VEC>(p, hk, lg0, xb, by, bufs[warp], srts[warp], bcnts[warp]);
+        ls_block<PH, NI>(p, hk, lg0, xb, by, bufs[warp], srts[warp], bcnts[warp]);
         __syncwarp();  // the buckets are reused by the next block
     }
 }

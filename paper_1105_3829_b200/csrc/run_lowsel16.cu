@@ -19,7 +19,7 @@ bool lowsel16_applies(const SlabParams &p) {
     return !p.in_rows && p.radius >= LOWSEL_MIN_R && p.radius <= LOWSEL_MAX_R;
 }
 
-template <int PH, int NI, bool VEC>
+template <int PH, int NI>
 static int launch_lowsel_ni(const SlabParams &p, int B, cudaStream_t s, const uint32_t *hk) {
     // a CTA takes `seg` vertically adjacent block rows.  One block row per CTA schedules best
     // (config 3 r = 31: 1.38 / 1.43 / 1.57 ms at seg = 1 / 2 / 4: the blocks' costs vary); larger
@@ -36,7 +36,7 @@ static int launch_lowsel_ni(const SlabParams &p, int B, cudaStream_t s, const ui
     int lg = LS_MINLG;
     while (lg < LS_MAXLG && (1 << lg) < mean + 4.0 * std::sqrt(mean)) ++lg;
     lg = std::min(LS_MAXLG, std::max(LS_MINLG, env_int("MTB_LS_LG", lg)));
-    k_lowsel_u16<PH, NI, VEC><<<grid, 32 * LS_WARPS, 0, s>>>(p, hk, lg, seg);
+    k_lowsel_u16<PH, NI><<<grid, 32 * LS_WARPS, 0, s>>>(p, hk, lg, seg);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_lowsel_u16: ") + cudaGetErrorString(e));
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -45,22 +45,11 @@ static int launch_lowsel_ni(const SlabParams &p, int B, cudaStream_t s, const ui
 
 template <int PH>
 static int launch_lowsel(const SlabParams &p, int B, cudaStream_t s, const uint32_t *hk) {
-    // pixel-pair loads when every row starts 4-byte aligned and the width is even
-    const bool vec = p.W % 2 == 0 && p.src_pitch % 2 == 0 && p.src_img_stride % 2 == 0 &&
-                     reinterpret_cast<uintptr_t>(p.src) % 4 == 0 && env_int("MTB_LS_VEC", 1) != 0;
-    if (vec) {
-        const int uw = 32 + 2 * p.radius + (p.radius & 1);
-        switch (((uw + 1) / 2 + 31) / 32) {  // steps of 32 column pairs
-            case 1: return launch_lowsel_ni<PH, 1, true>(p, B, s, hk);
-            case 2: return launch_lowsel_ni<PH, 2, true>(p, B, s, hk);
-            default: return launch_lowsel_ni<PH, 3, true>(p, B, s, hk);
-        }
-    }
-    switch ((32 + 2 * p.radius + 31) / 32) {  // steps of 32 columns
-        case 2: return launch_lowsel_ni<PH, 2, false>(p, B, s, hk);
-        case 3: return launch_lowsel_ni<PH, 3, false>(p, B, s, hk);
-        case 4: return launch_lowsel_ni<PH, 4, false>(p, B, s, hk);
-        default: return launch_lowsel_ni<PH, 5, false>(p, B, s, hk);
+    switch ((32 + 2 * p.radius + 31) / 32) {  // column steps of the scan
+        case 2: return launch_lowsel_ni<PH, 2>(p, B, s, hk);
+        case 3: return launch_lowsel_ni<PH, 3>(p, B, s, hk);
+        case 4: return launch_lowsel_ni<PH, 4>(p, B, s, hk);
+        default: return launch_lowsel_ni<PH, 5>(p, B, s, hk);
     }
 }
 

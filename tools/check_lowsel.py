@@ -31,11 +31,10 @@ def frames(H, W):
     return (("noise", noise), ("compact", compact), ("mixed", mixed), ("twelve", twelve))
 
 
-for ph in ("4", "8", "8s"):
-    os.environ["MTB_LS_PH"] = ph[0]
-    os.environ["MTB_LS_VEC"] = "0" if ph.endswith("s") else "1"
+for ph in ("4", "8"):
+    os.environ["MTB_LS_PH"] = ph
     os.environ["MTB_KERNEL"] = "lowsel"
-    for (H, W) in ((97, 334), (40, 700), (300, 64), (131, 257)):
+    for (H, W) in ((97, 333), (40, 700), (300, 64), (131, 257)):
         for name, px in frames(H, W):
             src = torch.from_numpy(px).cuda()
             for r in radii:
@@ -53,7 +52,6 @@ for ph in ("4", "8", "8s"):
                         print(f"MISMATCH PH={ph} {name} {H}x{W} r={r} rank={rank}: {len(d)} px, first {d[0]} got {got[tuple(d[0])]} ref {ref[tuple(d[0])]} kernel {_lib.last_kernel()}", flush=True)
         print("PH", ph, H, W, "done; kernel", _lib.last_kernel(), "bad", bad, flush=True)
 os.environ.pop("MTB_LS_PH")
-os.environ.pop("MTB_LS_VEC")
 # default dispatch (device-selected), a batch
 os.environ.pop("MTB_KERNEL")
 stack = np.stack([f for _, f in frames(120, 200)])
@@ -73,10 +71,10 @@ if "--time" in sys.argv:
         for r in (4, 7, 15, 23, 31, 47, 63):
             row = []
             for label, env in (("old", {"MTB_U16_LIST": "0"}), ("ph4", {"MTB_LS_PH": "4"}), ("ph8", {"MTB_LS_PH": "8"}),
-                               ("novec", {"MTB_LS_VEC": "0"}), ("ph4novec", {"MTB_LS_VEC": "0", "MTB_LS_PH": "4"})):
+                               ("seg1", {"MTB_LS_SEG": "1"}), ("seg2", {"MTB_LS_SEG": "2"}), ("seg4", {"MTB_LS_SEG": "4"})):
                 if cfg == 4 and label not in ("old", "ph8"):
                     continue
-                for k in ("MTB_U16_LIST", "MTB_LS_PH", "MTB_LS_LG", "MTB_LS_SEG", "MTB_LS_VEC"):
+                for k in ("MTB_U16_LIST", "MTB_LS_PH", "MTB_LS_LG", "MTB_LS_SEG"):
                     os.environ.pop(k, None)
                 os.environ.update(env)
                 mtb.rank_filter(src, r, out=out)
