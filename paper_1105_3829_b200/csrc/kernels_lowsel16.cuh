@@ -25,9 +25,9 @@
 // (32 PH) loads instead of the n per level of the gather kernels or the
 // per-column run lookups of k_colhist16c_u16.
 //
-// A bucket that overflows doubles BCAP (half as many high bytes per chunk)
-// and repeats the chunk; a block where one high byte alone overflows 512
-// entries (locally compact data) is flagged in SlabParams::todo and left to
+// A chunk with an overflowing bucket is repeated with buckets large enough for
+// it (fewer high bytes per chunk); a block where one high byte alone overflows
+// 512 entries (locally compact data) is flagged in SlabParams::todo and left to
 // k_colhist16_u16, which then works on the tiles holding such blocks only.
 // Exact for any image; the data only decide which kernel resolves a block.
 #pragma once
@@ -132,19 +132,25 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
             for (int i = 0; i < NI; ++i) drop(v1[i], j + 1, i);
         }
         __syncwarp();
-        if (__any_sync(0xffffffffu, bcnt[lane] > BCAP)) {
-            if (lg == LS_MAXLG) {  // locally compact data: leave the block to the two-phase kernel
+        const int maxc = __reduce_max_sync(0xffffffffu, bcnt[lane]);  // the fullest bucket
+        if (maxc > BCAP) {
+            if (maxc > LS_CAP) {  // locally compact data: leave the block to the two-phase kernel
                 if (lane == 0) p.todo[((size_t)blockIdx.z * p.todo_nby + by) * p.todo_nbx + (xb >> 5)] = 1;
                 __syncwarp();
                 return;
             }
-            ++lg;  // larger buckets, fewer high bytes per chunk; repeat from h0
+            while ((1 << lg) < maxc) ++lg;  // buckets that hold it, fewer high bytes per chunk; repeat from h0
             __syncwarp();
             continue;
         }
-        // ---- sort every bucket: an entry goes to the count of smaller entries
-        for (int t = lane; t < (NB << lg); t += 32) {
-            const int b = t >> lg, i = t & (BCAP - 1), nb = bcnt[b];
+        // ---- sort every bucket: an entry goes to the count of smaller entries.
+        // Lanes take (bucket, slot) pairs over the first 2^elg slots of every
+        // bucket, 2^elg >= the fullest bucket's count (fewer idle lanes than over
+        // all BCAP slots)
+        int elg = 0;
+        while ((1 << elg) < maxc) ++elg;
+        for (int t = lane; t < (NB << elg); t += 32) {
+            const int b = t >> elg, i = t & ((1 << elg) - 1), nb = bcnt[b];
             if (i < nb) {
                 const uint32_t *bk = buf + (b << lg);
                 const uint32_t e = bk[i];
