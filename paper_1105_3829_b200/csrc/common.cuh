@@ -38,6 +38,10 @@ struct SlabParams {
     // data is widely spread / compact (two launches, one does the work).
     const int *spread;
     int32_t gate;
+    // candidate-bucket path: the coarse key of a 16-bit pixel is min(v >> s, 255), s = 8 unless the
+    // sampled values leave the top bits empty (10- / 12-bit data in 16-bit words): then s follows the
+    // occupied range.  Device-selected dispatch: s = spread[1]; host-selected: s = 8 - key_down.
+    int32_t key_down;
     // 16-bit candidate-list path (kernels_lowsel16.cuh): one byte per block of
     // 32 x todo_bh output pixels ([image][block row][block column], todo_nbx
     // block columns), non-zero where the list kernel left the block to the
@@ -53,6 +57,11 @@ constexpr int WK_FROM_SPREAD = 2;  // k_colhist16_u16 wk mode: window-keyed swee
 
 __device__ __forceinline__ bool spread_is_wide(const SlabParams &p) {
     return *reinterpret_cast<const volatile int *>(p.spread) > SPREAD_WIDE;
+}
+
+// shift of the coarse key (candidate-bucket path)
+__device__ __forceinline__ int key_shift(const SlabParams &p) {
+    return p.spread ? reinterpret_cast<const volatile int *>(p.spread)[1] : 8 - p.key_down;
 }
 
 // true when a gated launch has nothing to do (uniform over the grid)

@@ -1018,15 +1018,16 @@ namespace mtb {
 // then fit two 256-thread CTAs per SM up to r = 32 (PL = 2 before), and a
 // row update is 12 shared-memory atomics instead of 14.
 
-// PX = uint16_t: the same kernel keyed by the HIGH byte of 16-bit pixels
-// (first pass of the 16-bit candidate-list path, kernels_lowsel16.cuh):
-// instead of a result pixel it writes H << 16 | k' per pixel to a u32 plane
-// (p.dst, pitch in words), H = the result's high byte, k' = the rank of the
-// result among the window values with that high byte.
+// PX = uint16_t: the same kernel keyed by the coarse key of 16-bit pixels,
+// min(v >> s, 255) -- the high byte, s = 8, unless the data leaves the top
+// bits empty (key_shift) -- as the first pass of the 16-bit candidate-bucket
+// path (kernels_lowsel16.cuh): instead of a result pixel it writes
+// H << 16 | k' per pixel to a u32 plane (p.dst, pitch in words), H = the
+// result's key, k' = the rank of the result among the window values with
+// that key.
 template <int T, int G, int M, int PL, bool STREAM, int NF = 0, typename PX = uint8_t>
 __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
     constexpr bool HI16 = sizeof(PX) == 2;
-    constexpr int KS = HI16 ? 8 : 0;  // key = pixel >> KS
     constexpr int GP = G / 2;
     constexpr bool DL2 = PL == 4;           // level-2 singles derived from level 3
     constexpr int PLP = DL2 ? 3 : PL;        // pair levels
@@ -1043,6 +1044,9 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
     if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
     if (HI16 && gate_off(p)) return;
+    const int ks = HI16 ? key_shift(p) : 0;
+    // the record key of a pixel: the pixel (8-bit), or its coarse key min(v >> ks, 255) (16-bit)
+    auto keyof = [&](unsigned v) -> unsigned { return HI16 ? min(v >> ks, 255u) : v; };
     const int y1 = min(y0 + p.rows_per_cta, p.row_end);
     if (STREAM) stream_wait_rows(p, y1 + r);
     const PX *src = static_cast<const PX *>(p.src) + blockIdx.z * p.src_img_stride;
@@ -1068,7 +1072,7 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         const int gx = clampi(X0 - r + c, 0, W - 1);
         // (atomic adds here too: measured r = 15 0.358 -> 0.319 ms, r = 31
         // 0.595 -> 0.530 against byte read-modify-writes)
-        for (int j = -r; j <= r; ++j) sbump(c, (unsigned)__ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx) >> KS, 1);
+        for (int j = -r; j <= r; ++j) sbump(c, keyof(__ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx)), 1);
     }
     __syncthreads();
     // level-2 word of column c for record p2, from its four level-3 words
@@ -1114,8 +1118,8 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         const PX *ri = src_row(p, src, clampi(yn + r, 0, H - 1));
 #pragma unroll
         for (int u = 0; u < CH_PF; ++u) {
-            pvo[u] = (unsigned)__ldg(ro + gxs[u]) >> KS;
-            pvi[u] = (unsigned)__ldg(ri + gxs[u]) >> KS;
+            pvo[u] = keyof(__ldg(ro + gxs[u]));
+            pvi[u] = keyof(__ldg(ri + gxs[u]));
         }
     };
     if (y0 + 1 < y1) prefetch(y0 + 1);
@@ -1134,7 +1138,7 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
                 const PX *ri = src_row(p, src, clampi(y + r, 0, H - 1));
                 for (int c = tid + CH_PF * T; c < NCOL; c += T) {
                     const int gx = clampi(X0 - r + c, 0, W - 1);
-                    const unsigned vo = (unsigned)__ldg(ro + gx) >> KS, vi = (unsigned)__ldg(ri + gx) >> KS;
+                    const unsigned vo = keyof(__ldg(ro + gx)), vi = keyof(__ldg(ri + gx));
                     if (vo == vi) continue;
                     move(c, vo, vi);
                 }

@@ -55,6 +55,7 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
     const uint16_t *lut = static_cast<const uint16_t *>(p.lut);
     const uint32_t *hkp = hk + ((int64_t)blockIdx.z * rows + (yb - p.row_begin)) * W + xb + lane;
     const bool valid = xb + lane < W;
+    const int ks = key_shift(p);  // coarse key of a pixel: min(v >> ks, 255) (8: the high byte)
 
     // ---- the block's (H, k') and the range of H
     uint32_t myhk[PH];
@@ -110,9 +111,9 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
         bcnt[lane] = 0;
         __syncwarp();
         // ---- scan, two rows per step (all loads of a step in flight together)
-        auto drop = [&](unsigned v, int j, int i) {
-            const unsigned b = (v >> 8) - (unsigned)h0;
-            if (((okc >> i) & 1u) && b <= hspan) {
+        auto drop = [&](unsigned v, int j, int i, bool on) {
+            const unsigned b = min(v >> ks, 255u) - (unsigned)h0;
+            if (on && ((okc >> i) & 1u) && b <= hspan) {
                 const int slot = atomicAdd(bcnt + b, 1);
                 if (slot < BCAP) buf[(b << lg) + slot] = (v << 16) | ((unsigned)j << 8) | (unsigned)(lane + 32 * i);
             }
@@ -124,12 +125,12 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
                 v0[i] = __ldg(row + gx[i]);
-                v1[i] = two ? (unsigned)__ldg(row + p.src_pitch + gx[i]) : 0xffffffffu;  // (no bucket)
+                v1[i] = two ? (unsigned)__ldg(row + p.src_pitch + gx[i]) : 0u;
             }
 #pragma unroll
-            for (int i = 0; i < NI; ++i) drop(v0[i], j, i);
+            for (int i = 0; i < NI; ++i) drop(v0[i], j, i, true);
 #pragma unroll
-            for (int i = 0; i < NI; ++i) drop(v1[i], j + 1, i);
+            for (int i = 0; i < NI; ++i) drop(v1[i], j + 1, i, two);
         }
         __syncwarp();
         const int maxc = __reduce_max_sync(0xffffffffu, bcnt[lane]);  // the fullest bucket

@@ -27,29 +27,72 @@
 
 namespace mtb {
 
-// Spread of the 16-bit value distribution: number of distinct high bytes
-// among a strided sample of the source rows.  Selects the 16-bit kernel:
-// a wide spread (high byte of the median changes often) favours the
-// sorted-column low byte of k_colhist16s_u16; a compact one the two-phase
-// k_colhist16_u16.  Both are exact.
-__global__ void k_highbyte_spread(const uint16_t *src, int64_t pitch, int rows, int W, int64_t img_stride,
-                                  int B, int *out) {
-    __shared__ int seen[256];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) seen[i] = 0;
+// Spread of the 16-bit value distribution over a strided sample of the source
+// rows: out[0] = number of distinct coarse keys, out[1] = the key shift s
+// (key = min(v >> s, 255)).  With s = 8 the key is the high byte: a wide
+// spread (> SPREAD_WIDE distinct keys: the key of the median changes from
+// pixel to pixel) goes to the candidate-bucket path, a compact one to the
+// two-phase k_colhist16_u16.  Data whose top bits are empty (10- / 12- /
+// 14-bit samples in 16-bit words: compact, or coarsely spread, by its high
+// bytes) is looked at again with s = the bits the largest sample needs
+// beyond 8: if the keys are then
+// widely spread AND flat (no key holds more than 1/64 of the sample, against
+// 1/256 on uniformly spread data), the candidate-bucket path takes it with that shift.
+// Every choice is exact; it only decides the speed.
+constexpr int SPREAD_SAMPLES = 1 << 14;
+constexpr int SPREAD_FLAT_MAX = SPREAD_SAMPLES / 64;
+
+constexpr int SPREAD_THREADS = 1024;
+
+__global__ void __launch_bounds__(SPREAD_THREADS) k_highbyte_spread(const uint16_t *src, int64_t pitch, int rows, int W,
+                                                                    int64_t img_stride, int B, int allow_shift, int *out) {
+    __shared__ uint16_t smp[SPREAD_SAMPLES];  // the sample, read once
+    __shared__ int hist[256];
+    __shared__ int vmax, res[2];
+    const int tid = threadIdx.x;
+    // distinct / fullest of the 256 keys min(v >> s, 255) -> res[0], res[1]
+    auto keys = [&](int s) {
+        if (tid < 256) hist[tid] = 0;
+        __syncthreads();
+        for (int i = tid; i < SPREAD_SAMPLES; i += SPREAD_THREADS) atomicAdd(hist + min((unsigned)smp[i] >> s, 255u), 1);
+        __syncthreads();
+        if (tid < 32) {
+            int d = 0, m = 0;
+            for (int b = tid; b < 256; b += 32) {
+                d += hist[b] ? 1 : 0;
+                m = max(m, hist[b]);
+            }
+            d = __reduce_add_sync(0xffffffffu, d);
+            m = __reduce_max_sync(0xffffffffu, m);
+            if (tid == 0) res[0] = d, res[1] = m;
+        }
+        __syncthreads();
+    };
+    if (tid == 0) vmax = 0;
     __syncthreads();
-    const int total = 1 << 14;
-    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    int mx = 0;
+    for (int i = tid; i < SPREAD_SAMPLES; i += SPREAD_THREADS) {
         const int y = (int)(((int64_t)i * 7919) % rows);
         const int x = (int)(((int64_t)i * 104729) % W);
         const int b = B > 1 ? i % B : 0;
-        seen[src[b * img_stride + (int64_t)y * pitch + x] >> 8] = 1;
+        const uint16_t v = src[b * img_stride + (int64_t)y * pitch + x];
+        smp[i] = v;
+        mx = max(mx, (int)v);
     }
-    __syncthreads();
-    if (threadIdx.x < 32) {  // distinct high bytes
-        int d = 0;
-        for (int b = threadIdx.x; b < 256; b += 32) d += seen[b];
-        for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-        if (threadIdx.x == 0) *out = d;
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((tid & 31) == 0) atomicMax(&vmax, mx);
+    keys(8);  // (its barriers also order smp and vmax)
+    int d = res[0], sh = 8;
+    int s = 0;
+    while (s < 8 && (vmax >> s) > 255) ++s;
+    if (allow_shift && s < 8) {  // (uniform: all from shared memory)
+        __syncthreads();
+        keys(s);
+        if (res[0] > SPREAD_WIDE && res[1] <= SPREAD_FLAT_MAX) d = res[0], sh = s;
+    }
+    if (tid == 0) {
+        out[0] = d;
+        out[1] = sh;
     }
 }
 
@@ -256,16 +299,40 @@ static int run_sortnet(SlabParams p, int B, cudaStream_t s) {
 // no host synchronisation, stream-ordered scratch, graph-capturable.
 static thread_local int g_spread_hint = -1;
 
+static thread_local int g_shift_hint = 8;
+
+// the same on a host frame: returns the distinct-key count, sets g_shift_hint
 static int spread_distinct_host(const uint16_t *src, int64_t pitch, int rows, int W) {
-    bool seen[256] = {};
-    for (int i = 0; i < (1 << 14); ++i) {
+    auto sample = [&](int i) -> unsigned {
         const int y = (int)(((int64_t)i * 7919) % rows);
         const int x = (int)(((int64_t)i * 104729) % W);
-        seen[src[(int64_t)y * pitch + x] >> 8] = true;
+        return src[(int64_t)y * pitch + x];
+    };
+    auto keys = [&](int s, int &distinct, int &fullest) {
+        int hist[256] = {};
+        for (int i = 0; i < SPREAD_SAMPLES; ++i) ++hist[std::min(sample(i) >> s, 255u)];
+        distinct = fullest = 0;
+        for (int b = 0; b < 256; ++b) {
+            distinct += hist[b] ? 1 : 0;
+            fullest = std::max(fullest, hist[b]);
+        }
+    };
+    unsigned vmax = 0;
+    for (int i = 0; i < SPREAD_SAMPLES; ++i) vmax = std::max(vmax, sample(i));
+    int d8, m8;
+    keys(8, d8, m8);
+    int s = 0;
+    while (s < 8 && (vmax >> s) > 255) ++s;
+    g_shift_hint = 8;
+    if (s < 8) {
+        int ds, ms;
+        keys(s, ds, ms);
+        if (ds > SPREAD_WIDE && ms <= SPREAD_FLAT_MAX) {
+            g_shift_hint = s;
+            return ds;
+        }
     }
-    int d = 0;
-    for (int b = 0; b < 256; ++b) d += seen[b] ? 1 : 0;
-    return d;
+    return d8;
 }
 
 static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
@@ -282,13 +349,19 @@ static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
     auto run_wide = [&](const SlabParams &q) {
         return list ? run_lowsel16_u16(q, B, s) : (small_r ? run_colhist16c_u16(q, B, s) : run_colhist16_u16(q, B, s, 0));
     };
-    if (g_spread_hint >= 0) return g_spread_hint > SPREAD_WIDE ? run_wide(p) : run_colhist16_u16(p, B, s, 1);
+    if (g_spread_hint >= 0) {
+        if (g_spread_hint <= SPREAD_WIDE) return run_colhist16_u16(p, B, s, 1);
+        p.key_down = list ? 8 - g_shift_hint : 0;
+        // (a shifted key only helps the candidate-bucket path: the other kernels split at the high byte)
+        if (!list && g_shift_hint != 8) return run_colhist16_u16(p, B, s, 1);
+        return run_wide(p);
+    }
     int *d_spread = nullptr;
     keep_pool_memory();
-    if (cudaMallocAsync(reinterpret_cast<void **>(&d_spread), sizeof(int), s) != cudaSuccess)
+    if (cudaMallocAsync(reinterpret_cast<void **>(&d_spread), 2 * sizeof(int), s) != cudaSuccess)
         return fail(MTB_E_CUDA, "k_highbyte_spread: scratch allocation failed");
-    k_highbyte_spread<<<1, 256, 0, s>>>(static_cast<const uint16_t *>(p.src), p.src_pitch, p.src_rows, p.W,
-                                        p.src_img_stride, B, d_spread);
+    k_highbyte_spread<<<1, SPREAD_THREADS, 0, s>>>(static_cast<const uint16_t *>(p.src), p.src_pitch, p.src_rows, p.W,
+                                        p.src_img_stride, B, list ? 1 : 0, d_spread);
     cudaError_t e = cudaGetLastError();
     int rc = e == cudaSuccess ? MTB_OK : fail(MTB_E_CUDA, std::string("k_highbyte_spread: ") + cudaGetErrorString(e));
     if (!rc) g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -635,6 +635,37 @@ def test_lowsel_u16_bucket_sizes_batch_slab_and_lut(lg, monkeypatch):
         assert np.array_equal(q, ref & ~np.uint16(15)), r
 
 
+@pytest.mark.parametrize("bits", [8, 10, 12, 14])
+def test_lowsel_u16_key_follows_the_occupied_range(bits):
+    """10- / 12-bit noise in 16-bit words looks compact by its high bytes;
+    the spread probe then shifts the coarse key to the occupied range
+    (key = min(v >> s, 255)) and the candidate-bucket path takes it: host
+    entry (probe on the host frame: the kernel is named) and device entry
+    (probe on the device), a few outliers above the sampled range (clamped
+    into the top key), every rank position."""
+    from paper_1105_3829_b200 import _lib
+
+    rng = np.random.default_rng(1000 + bits)
+    px = rng.integers(0, 1 << bits, (150, 260)).astype(np.uint16)
+    out, _ = mtb.filter_image(px, 11)
+    assert _lib.last_kernel() == "k_lowsel_u16", _lib.last_kernel()
+    assert np.array_equal(out.pixels, O.iot_filter(px, 11))
+    spiky = px.copy()
+    spiky[rng.integers(0, 150, 5), rng.integers(0, 260, 5)] = 65535
+    for img in (px, spiky):
+        src = torch.from_numpy(img).cuda()
+        for r in (4, 15, 33):
+            n = 2 * r + 1
+            for rank in (None, 1, n * n, (n * n) // 3 + 1):
+                got = mtb.rank_filter(src, r, rank=rank).cpu().numpy()
+                assert np.array_equal(got, O.iot_filter(img, n, rank=rank)), (bits, r, rank)
+    # peaked data in a narrow range stays on the two-phase kernel (not flat in key space)
+    peaked = (800 + rng.normal(0, 40, (150, 260))).clip(0, 65535).astype(np.uint16)
+    out, _ = mtb.filter_image(peaked, 11)
+    assert _lib.last_kernel() == "k_colhist16_u16", _lib.last_kernel()
+    assert np.array_equal(out.pixels, O.iot_filter(peaked, 11))
+
+
 # ------------------------------------------ 3x3 kernels (k_med3_u8 / k_med3t_u8)
 
 def _pitched(px, pad):
