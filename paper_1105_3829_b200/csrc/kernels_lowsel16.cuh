@@ -42,13 +42,16 @@ constexpr int LS_MINLG = 4;    // log2 of the smallest bucket (32 high bytes per
 
 // One block: the 32 x PH output pixels at columns xb.., block row `by` of image
 // blockIdx.z; called by a whole warp.  buf / srt / bcnt: the warp's buckets.
+// PH > 0: compile-time block height, the block's (H, k') words in registers;
+// PH == 0: block height p.todo_bh, the words re-read where they are used.
 template <int PH, int NI>
 __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__restrict__ hk, int lg0, int xb, int by,
                                          uint32_t *buf, uint32_t *srt, int *bcnt) {
     const int lane = threadIdx.x & 31;
     const int r = p.radius, r2 = 2 * r, W = p.W, H = p.H;
-    const int yb = p.row_begin + by * PH;
-    const int ph = min(PH, p.row_end - yb);
+    const int PHR = PH ? PH : p.todo_bh;
+    const int yb = p.row_begin + by * PHR;
+    const int ph = min(PHR, p.row_end - yb);
     const int rows = p.row_end - p.row_begin;
     const uint16_t *src = static_cast<const uint16_t *>(p.src) + blockIdx.z * p.src_img_stride;
     uint16_t *dst = static_cast<uint16_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
@@ -58,17 +61,22 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
     const int ks = key_shift(p);  // coarse key of a pixel: min(v >> ks, 255) (8: the high byte)
 
     // ---- the block's (H, k') and the range of H
-    uint32_t myhk[PH];
+    uint32_t myhk[PH ? PH : 1];
+    auto hk_at = [&](int py) -> uint32_t {  // 0xffffffff: no pixel
+        if (PH) return myhk[py];
+        return valid && py < ph ? __ldg(hkp + (int64_t)py * W) : 0xffffffffu;
+    };
     int hmin = 255, hmax = 0;
 #pragma unroll
-    for (int py = 0; py < PH; ++py) {
-        myhk[py] = 0xffffffffu;
+    for (int py = 0; py < PHR; ++py) {
+        uint32_t w = 0xffffffffu;
         if (valid && py < ph) {
-            myhk[py] = __ldg(hkp + (int64_t)py * W);
-            const int h = (int)(myhk[py] >> 16);
+            w = __ldg(hkp + (int64_t)py * W);
+            const int h = (int)(w >> 16);
             hmin = min(hmin, h);
             hmax = max(hmax, h);
         }
+        if (PH) myhk[py] = w;
     }
     hmin = __reduce_min_sync(0xffffffffu, hmin);
     hmax = __reduce_max_sync(0xffffffffu, hmax);
@@ -103,7 +111,7 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
         const unsigned hspan = (unsigned)(h1 - h0);
         bool want = false;
 #pragma unroll
-        for (int py = 0; py < PH; ++py) want |= (myhk[py] >> 16) - (unsigned)h0 <= hspan;
+        for (int py = 0; py < PHR; ++py) want |= (hk_at(py) >> 16) - (unsigned)h0 <= hspan;
         if (!__any_sync(0xffffffffu, want)) {  // no pixel of the block has its H here
             h0 = h1 + 1;
             continue;
@@ -164,10 +172,11 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
         // ---- every pixel of the chunk: the k'-th entry of its bucket inside its
         // window (pixel (lane, py): dx in [lane, lane + 2r], dy in [py, py + 2r])
 #pragma unroll
-        for (int py = 0; py < PH; ++py) {
-            const unsigned b = (myhk[py] >> 16) - (unsigned)h0;
+        for (int py = 0; py < PHR; ++py) {
+            const uint32_t w = hk_at(py);
+            const unsigned b = (w >> 16) - (unsigned)h0;
             if (b > hspan) continue;
-            const uint32_t k = myhk[py] & 0xffffu;
+            const uint32_t k = w & 0xffffu;
             const uint32_t *bk = srt + (b << lg);
             const int nb = bcnt[b];
             uint32_t c = 0, res = 0;

@@ -32,7 +32,7 @@ static int launch_lowsel_ni(const SlabParams &p, int B, cudaStream_t s, const ui
     // buckets to start with: the mean count of one high byte on uniformly spread data plus 3.5
     // standard deviations (an overflowing chunk is repeated with larger buckets; config 3 r = 23
     // 1.30 -> 1.12 ms against twice the mean)
-    const double mean = (32 + 2 * p.radius) * (PH + 2 * p.radius) / 256.0;
+    const double mean = (32 + 2 * p.radius) * (p.todo_bh + 2 * p.radius) / 256.0;
     int lg = LS_MINLG;
     while (lg < LS_MAXLG && (1 << lg) < mean + 3.5 * std::sqrt(mean)) ++lg;
     lg = std::min(LS_MAXLG, std::max(LS_MINLG, env_int("MTB_LS_LG", lg)));
@@ -56,9 +56,12 @@ static int launch_lowsel(const SlabParams &p, int B, cudaStream_t s, const uint3
 int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s) {
     if (!lowsel16_applies(p)) return run_colhist16_u16(p, B, s, 0);
     const int rows = p.row_end - p.row_begin;
-    // block height: taller blocks share the scan among more pixels, but widen
-    // the range of high bytes (longer lists)
-    const int PH = env_int("MTB_LS_PH", 8) >= 8 ? 8 : 4;
+    // block height: taller blocks share the scan among more pixels but widen the blocks' key ranges
+    // and lengthen the buckets: 8 rows below r = 28, 16 from there (config 3 r = 31 1.42 -> 1.34 ms,
+    // r = 63 4.42 -> 4.00; r = 15 0.91 / 0.90, r = 23 1.14 / 1.27 at 8 / 16 rows).  Heights above 8
+    // run the variant that keeps the block's (H, k') words out of registers.
+    const int ph_env = env_int("MTB_LS_PH", p.radius >= 28 ? 16 : 8);
+    const int PH = ph_env > 8 ? std::min(ph_env, 64) : (ph_env >= 8 ? 8 : 4);
     p.todo_bh = PH;
     p.todo_nbx = (p.W + 31) / 32;
     p.todo_nby = (rows + PH - 1) / PH;
@@ -81,7 +84,7 @@ int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s) {
     int rc = run_hi16_fixed_a(a, B, s);
     if (rc == 1) rc = run_hi16_fixed_b(a, B, s);
     if (rc == 1) rc = fail(MTB_E_INVAL, "k_lowsel_u16: radius outside the candidate-list path");
-    if (!rc) rc = PH == 8 ? launch_lowsel<8>(p, B, s, hk) : launch_lowsel<4>(p, B, s, hk);
+    if (!rc) rc = PH > 8 ? launch_lowsel<0>(p, B, s, hk) : (PH == 8 ? launch_lowsel<8>(p, B, s, hk) : launch_lowsel<4>(p, B, s, hk));
     // pass 3: flagged blocks are locally compact, where the window-keyed sweep pays
     if (!rc) rc = run_colhist16_u16(p, B, s, 1);
     cudaFreeAsync(scratch, s);

@@ -568,7 +568,7 @@ def _lowsel_frames(rng, h, w):
     return {"noise": noise, "compact": compact, "mixed": mixed, "twelve": twelve}
 
 
-@pytest.mark.parametrize("ph", ["4", "8"])
+@pytest.mark.parametrize("ph", ["4", "8", "16"])
 @pytest.mark.parametrize("kind", ["noise", "compact", "mixed", "twelve"])
 def test_lowsel_u16_candidate_buckets(kind, ph, monkeypatch):
     """The 16-bit candidate-bucket path (high-byte pair records ->
@@ -576,7 +576,8 @@ def test_lowsel_u16_candidate_buckets(kind, ph, monkeypatch):
     every column-step count of the scan (2..5) and both pair-record layouts
     of the first pass, min / max / off-centre ranks, frames narrower than a
     block and lower than a block row, the clamped borders (weighted border
-    entries) and data whose buckets overflow."""
+    entries) and data whose buckets overflow; block heights 4 and 8 (the
+    block's words in registers) and 16 (re-read)."""
     from paper_1105_3829_b200 import _lib
 
     monkeypatch.setenv("MTB_KERNEL", "lowsel")

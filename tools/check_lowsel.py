@@ -31,7 +31,7 @@ def frames(H, W):
     return (("noise", noise), ("compact", compact), ("mixed", mixed), ("twelve", twelve))
 
 
-for ph in ("4", "8"):
+for ph in ("4", "8", "16"):
     os.environ["MTB_LS_PH"] = ph
     os.environ["MTB_KERNEL"] = "lowsel"
     for (H, W) in ((97, 333), (40, 700), (300, 64), (131, 257)):
@@ -72,7 +72,7 @@ if "--time" in sys.argv:
         for r in (4, 7, 15, 23, 31, 47, 63):
             row = []
             for label, env in (("old", {"MTB_U16_LIST": "0"}), ("ph4", {"MTB_LS_PH": "4"}), ("ph8", {"MTB_LS_PH": "8"}),
-                               ("seg1", {"MTB_LS_SEG": "1"}), ("seg2", {"MTB_LS_SEG": "2"}), ("seg4", {"MTB_LS_SEG": "4"})):
+                               ("ph12", {"MTB_LS_PH": "12"}), ("ph16", {"MTB_LS_PH": "16"}), ("ph24", {"MTB_LS_PH": "24"})):
                 if cfg in (4, 12) and label not in ("old", "ph8"):
                     continue
                 for k in ("MTB_U16_LIST", "MTB_LS_PH", "MTB_LS_LG", "MTB_LS_SEG"):
