@@ -78,6 +78,7 @@ int run_colhist16_fixed_b(SlabParams p, int B, cudaStream_t s, int wk);
 int run_colhist16_fixed_c(SlabParams p, int B, cudaStream_t s, int wk);
 int run_ctmf_u8(SlabParams p, int B, cudaStream_t s);
 int run_bandmma_u8(SlabParams p, int B, cudaStream_t s);
+int run_bandmma_hi16(SlabParams p, int B, cudaStream_t s);
 int run_bandtc_u8(SlabParams p, int B, cudaStream_t s);
 
 }  // namespace mtb

@@ -38,6 +38,7 @@
 // n^2 <= 65535 is required (r <= 127).
 #pragma once
 #include <cstdio>
+#include <type_traits>
 #include "common.cuh"
 
 namespace mtb {
@@ -139,9 +140,20 @@ __device__ __forceinline__ void bm_product(const uint8_t *planes, int NP, int xa
 
 // NK: k-tiles of a group of 16 pixels.  Block = 32 * (TW / 16) threads (one
 // warp per 16 output columns); grid = (stripes, row slabs, images).
-template <int NK, bool STREAM>
+// PX = uint16_t: the same kernel on the coarse keys min(v >> s, 255) of 16-bit
+// pixels (key_shift), as the first pass of the 16-bit candidate-bucket path
+// from r = 32 (kernels_lowsel16.cuh): instead of a result pixel it writes
+// H << 16 | k' per pixel to a u32 plane (p.dst, pitch in words), H = the
+// result's key, k' = the rank of the result among the window values with that
+// key (what the last descent leaves).
+template <int NK, bool STREAM, typename PX = uint8_t>
 __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW) {
+    constexpr bool HI16 = sizeof(PX) == 2;
+    using OUT = typename std::conditional<HI16, uint32_t, uint8_t>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (HI16 && gate_off(p)) return;  // (uniform over the grid)
+    const int ks = HI16 ? key_shift(p) : 0;
+    auto keyof = [&](unsigned v) -> unsigned { return HI16 ? min(v >> ks, 255u) : v; };
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NTH = blockDim.x;
     const int r = p.radius, r2 = 2 * r, H = p.H, W = p.W;
     const int NC = TW + r2, NP = bm_pitch(TW, r), NPW = NP >> 2;
@@ -156,8 +168,8 @@ __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW)
     if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
     const int y1 = min(y0 + p.rows_per_cta, p.row_end);
     if (STREAM) stream_wait_rows(p, y1 + r);
-    const uint8_t *src = static_cast<const uint8_t *>(p.src) + blockIdx.z * p.src_img_stride;
-    uint8_t *dst = static_cast<uint8_t *>(p.dst) + blockIdx.z * p.dst_img_stride;
+    const PX *src = static_cast<const PX *>(p.src) + blockIdx.z * p.src_img_stride;
+    OUT *dst = static_cast<OUT *>(p.dst) + blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
 
     // ---- column histograms of row y0: rows clamp(y0-r .. y0+r).  Slot s =
@@ -175,12 +187,12 @@ __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW)
         for (; j + 7 <= r; j += 8) {  // 8 loads in flight (the rows come from L2)
             unsigned v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = __ldg(src_row(p, src, clampi(y0 + j + u, 0, H - 1)) + gx);
+            for (int u = 0; u < 8; ++u) v[u] = keyof(__ldg(src_row(p, src, clampi(y0 + j + u, 0, H - 1)) + gx));
 #pragma unroll
             for (int u = 0; u < 8; ++u) atomicAdd(planew + (16 + v[u]) * NPW + wd, one);
         }
         for (; j <= r; ++j)
-            atomicAdd(planew + (16 + __ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx)) * NPW + wd, one);
+            atomicAdd(planew + (16 + keyof(__ldg(src_row(p, src, clampi(y0 + j, 0, H - 1)) + gx))) * NPW + wd, one);
     }
     __syncthreads();
     // cumulative planes from the value planes: cum[j] = sum of planes below 16 j
@@ -214,7 +226,7 @@ __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW)
     // pixels loaded a row ahead
     uint32_t *pw = nullptr;  // plane word of the slot (row 0), nullptr: no slot
     uint32_t pone = 0;
-    const uint8_t *pin = src;  // the slot's column in source row 0 of this image
+    const PX *pin = src;  // the slot's column in source row 0 of this image
     {
         const int bl = tid / nwords, wd = tid - bl * nwords, c = 4 * wd + bl;
         if (tid < nslots && c < NC) pw = planew + wd;
@@ -224,13 +236,13 @@ __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW)
     unsigned pvo = 0, pvi = 0;
     // running pointers to the slot's column in the leaving / entering row of
     // the next update (a clamped row index repeats the edge row: no step)
-    const uint8_t *pout = pin + (int64_t)(clampi(y0 - r, 0, H - 1) - p.src_row0) * p.src_pitch;
-    const uint8_t *pent = pin + (int64_t)(clampi(y0 + 1 + r, 0, H - 1) - p.src_row0) * p.src_pitch;
+    const PX *pout = pin + (int64_t)(clampi(y0 - r, 0, H - 1) - p.src_row0) * p.src_pitch;
+    const PX *pent = pin + (int64_t)(clampi(y0 + 1 + r, 0, H - 1) - p.src_row0) * p.src_pitch;
     // rows of the update y-1 -> y: leaving y-r-1, entering y+r; called for yn = y0+1, y0+2, ...
     auto prefetch = [&](int yn) {
         if (pw) {
-            pvo = __ldg(pout);
-            pvi = __ldg(pent);
+            pvo = keyof(__ldg(pout));
+            pvi = keyof(__ldg(pent));
         }
         // next update (yn + 1): leaving row yn - r, entering row yn + 1 + r
         if (yn - r > 0 && yn - r <= H - 1) pout += p.src_pitch;
@@ -253,7 +265,7 @@ __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW)
     const bool valid = X0 + xa + px < W;
     const bool live = X0 + xa < W;            // (warp-uniform) some pixel of the warp is in the image
     const unsigned char *myrec = tb + px * BM_REC + half * 32;
-    uint8_t *dpx = dst + (int64_t)(y0 - p.row_begin) * p.dst_pitch + X0 + xa + px;
+    OUT *dpx = dst + (int64_t)(y0 - p.row_begin) * p.dst_pitch + X0 + xa + px;
     int Bp = 0xff;  // predicted window base (coarse bin); 0xff: none yet
     const uint32_t rank = p.rank;
 
@@ -264,13 +276,13 @@ __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW)
         if (y > y0) {
             if (pw) move(pw, pone, pvo, pvi);
             if (nslots > NTH) {
-                const uint8_t *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
-                const uint8_t *ri = src_row(p, src, clampi(y + r, 0, H - 1));
+                const PX *ro = src_row(p, src, clampi(y - r - 1, 0, H - 1));
+                const PX *ri = src_row(p, src, clampi(y + r, 0, H - 1));
                 for (int s = tid + NTH; s < nslots; s += NTH) {
                     const int bl = s / nwords, wd = s - bl * nwords, c = 4 * wd + bl;
                     if (c >= NC) continue;
                     const int gx = clampi(X0 - r + c, 0, W - 1);
-                    move(planew + wd, 1u << (8 * bl), __ldg(ro + gx), __ldg(ri + gx));
+                    move(planew + wd, 1u << (8 * bl), keyof(__ldg(ro + gx)), keyof(__ldg(ri + gx)));
                 }
             }
         }
@@ -319,17 +331,24 @@ __global__ void __launch_bounds__(BM_MAXT, 1) k_bandmma_u8(SlabParams p, int TW)
                 const int b16 = bm_descend(c8, k);
                 const int bin = 16 * half + b16;
                 // (bin 0 is "below the window": a miss, like a rank above the window's total)
-                const unsigned cand = (here && bin > 0) ? (unsigned)(16 * B + bin - 1) : 0xffffu;
+                // (16-bit keys: the rank within the value rides along below the value)
+                const unsigned found = (unsigned)(16 * B + bin - 1);
+                const unsigned cand = (here && bin > 0) ? (HI16 ? (found << 16) | k : found) : 0xffffffffu;
                 const unsigned both = min(cand, __shfl_xor_sync(0xffffffffu, cand, 16));  // the pair's result
-                const bool hit = both != 0xffffu;
+                const bool hit = both != 0xffffffffu;
                 if (hit && ((open >> lane) & 1u)) val = both;
                 open &= ~__ballot_sync(0xffffffffu, hit || !valid);
                 if (!open) break;
             }
             // prediction for the next row: the lowest result of the warp, one below for drift
-            const int lo = __reduce_min_sync(0xffffffffu, valid ? (int)val : 255);
+            const int lo = __reduce_min_sync(0xffffffffu, valid ? (int)(HI16 ? val >> 16 : val) : 255);
             Bp = min(max(lo - 1, 0) >> 4, 15);
-            if (valid && half == 0) *dpx = lut ? __ldg(lut + val) : (uint8_t)val;
+            if (valid && half == 0) {
+                if (HI16)
+                    *dpx = (OUT)val;
+                else
+                    *dpx = (OUT)(lut ? __ldg(lut + val) : (uint8_t)val);
+            }
         }
 #ifdef BM_TIMING
         { const long long t = clock64(); tB += t - t0; t0 = t; }

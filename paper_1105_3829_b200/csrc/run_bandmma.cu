@@ -13,11 +13,12 @@ static_assert(bm_smem(16, 127) <= 227 * 1024, "a stripe at the largest radius");
 static_assert(bm_pitch(512, 63) % 64 == 32 && bm_pitch(512, 63) >= 512 + 126 && bm_pitch(512, 63) >= 512 + 32 * bm_nk(63) - 16,
               "plane pitch: bank rule, halo'd columns, last k-tile");
 
-template <int NK>
+template <int NK, typename PX = uint8_t>
 static int run_bandmma_nk(SlabParams p, int B, cudaStream_t s, int TW) {
+    constexpr bool HI16 = sizeof(PX) == 2;  // 16-bit coarse keys (never a streaming launch)
     const size_t smem = bm_smem(TW, p.radius);
     const int threads = 32 * (TW / 16);
-    auto kern = p.in_rows ? k_bandmma_u8<NK, true> : k_bandmma_u8<NK, false>;
+    auto kern = (p.in_rows && !HI16) ? k_bandmma_u8<NK, !HI16, PX> : k_bandmma_u8<NK, false, PX>;
     if (int rc = set_smem(kern, smem)) return rc;
     const int bx = (p.W + TW - 1) / TW;
     int per_sm = 1;
@@ -32,17 +33,17 @@ static int run_bandmma_nk(SlabParams p, int B, cudaStream_t s, int TW) {
     rpc = std::max(rpc, std::min(rows, p.radius / 2 + 8));  // keep the column build a small share
     p.rows_per_cta = rpc;
     dim3 grid(bx, (rows + rpc - 1) / rpc, B);
-    p.gate = env_int("MTB_BM_DBG", 0);  // (only read by a -DBM_TIMING build)
+    if (!HI16) p.gate = env_int("MTB_BM_DBG", 0);  // (only read by a -DBM_TIMING build)
     kern<<<grid, threads, smem, s>>>(p, TW);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_bandmma_u8: ") + cudaGetErrorString(e));
-    g_kernel = "k_bandmma_u8";
+    g_kernel = HI16 ? "k_bandmma_u8<u16 coarse key>" : "k_bandmma_u8";
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return MTB_OK;
 }
 
-// 8-bit, 1 <= r <= 127, any rank
-int run_bandmma_u8(SlabParams p, int B, cudaStream_t s) {
+template <typename PX>
+static int run_bandmma_px(SlabParams p, int B, cudaStream_t s) {
     const int r = p.radius;
     // stripe width: the widest multiple of 16 whose planes fit one SM's shared
     // memory with one warp per 16 output columns (at most BM_MAXT threads),
@@ -56,16 +57,22 @@ int run_bandmma_u8(SlabParams p, int B, cudaStream_t s) {
     int TW = ((p.W + stripes - 1) / stripes + 15) / 16 * 16;
     if (TW > twmax) TW = twmax;
     switch (bm_nk(r)) {
-        case 1: return run_bandmma_nk<1>(p, B, s, TW);
-        case 2: return run_bandmma_nk<2>(p, B, s, TW);
-        case 3: return run_bandmma_nk<3>(p, B, s, TW);
-        case 4: return run_bandmma_nk<4>(p, B, s, TW);
-        case 5: return run_bandmma_nk<5>(p, B, s, TW);
-        case 6: return run_bandmma_nk<6>(p, B, s, TW);
-        case 7: return run_bandmma_nk<7>(p, B, s, TW);
-        case 8: return run_bandmma_nk<8>(p, B, s, TW);
-        default: return run_bandmma_nk<9>(p, B, s, TW);
+        case 1: return run_bandmma_nk<1, PX>(p, B, s, TW);
+        case 2: return run_bandmma_nk<2, PX>(p, B, s, TW);
+        case 3: return run_bandmma_nk<3, PX>(p, B, s, TW);
+        case 4: return run_bandmma_nk<4, PX>(p, B, s, TW);
+        case 5: return run_bandmma_nk<5, PX>(p, B, s, TW);
+        case 6: return run_bandmma_nk<6, PX>(p, B, s, TW);
+        case 7: return run_bandmma_nk<7, PX>(p, B, s, TW);
+        case 8: return run_bandmma_nk<8, PX>(p, B, s, TW);
+        default: return run_bandmma_nk<9, PX>(p, B, s, TW);
     }
 }
+
+// 8-bit, 1 <= r <= 127, any rank
+int run_bandmma_u8(SlabParams p, int B, cudaStream_t s) { return run_bandmma_px<uint8_t>(p, B, s); }
+
+// 16-bit coarse keys -> (key, rank within it) words (first pass of the candidate-bucket path)
+int run_bandmma_hi16(SlabParams p, int B, cudaStream_t s) { return run_bandmma_px<uint16_t>(p, B, s); }
 
 }  // namespace mtb

@@ -6,6 +6,8 @@
 // stream-ordered pool.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "host.h"
 #include "kernels_lowsel16.cuh"
@@ -81,8 +83,17 @@ int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s) {
     a.dst_img_stride = (int64_t)rows * p.W;
     a.lut = nullptr;
     a.todo = nullptr;
-    int rc = run_hi16_fixed_a(a, B, s);
-    if (rc == 1) rc = run_hi16_fixed_b(a, B, s);
+    // pass 1: pair records up to r = 30, band-matrix products on the tensor cores from r = 31
+    // (config 3, whole path, pair / mma: r = 23 1.14 / 1.17 ms, r = 31 1.33 / 1.31, r = 47 2.23 /
+    // 1.90, r = 63 3.98 / 2.37; MTB_LS_HI=pair|mma forces)
+    const std::string hi = getenv("MTB_LS_HI") ? getenv("MTB_LS_HI") : "";
+    int rc = 1;
+    if (hi == "mma" || (hi.empty() && p.radius >= 31)) {
+        rc = run_bandmma_hi16(a, B, s);
+    } else {
+        rc = run_hi16_fixed_a(a, B, s);
+        if (rc == 1) rc = run_hi16_fixed_b(a, B, s);
+    }
     if (rc == 1) rc = fail(MTB_E_INVAL, "k_lowsel_u16: radius outside the candidate-list path");
     if (!rc) rc = PH > 8 ? launch_lowsel<0>(p, B, s, hk) : (PH == 8 ? launch_lowsel<8>(p, B, s, hk) : launch_lowsel<4>(p, B, s, hk));
     // pass 3: flagged blocks are locally compact, where the window-keyed sweep pays

@@ -31,8 +31,9 @@ def frames(H, W):
     return (("noise", noise), ("compact", compact), ("mixed", mixed), ("twelve", twelve))
 
 
-for ph in ("4", "8", "16"):
-    os.environ["MTB_LS_PH"] = ph
+for ph in ("4", "8", "16m"):
+    os.environ["MTB_LS_PH"] = ph.rstrip("m")
+    os.environ["MTB_LS_HI"] = "mma" if ph.endswith("m") else ""
     os.environ["MTB_KERNEL"] = "lowsel"
     for (H, W) in ((97, 333), (40, 700), (300, 64), (131, 257)):
         for name, px in frames(H, W):
@@ -52,6 +53,7 @@ for ph in ("4", "8", "16"):
                         print(f"MISMATCH PH={ph} {name} {H}x{W} r={r} rank={rank}: {len(d)} px, first {d[0]} got {got[tuple(d[0])]} ref {ref[tuple(d[0])]} kernel {_lib.last_kernel()}", flush=True)
         print("PH", ph, H, W, "done; kernel", _lib.last_kernel(), "bad", bad, flush=True)
 os.environ.pop("MTB_LS_PH")
+os.environ.pop("MTB_LS_HI")
 # default dispatch (device-selected), a batch
 os.environ.pop("MTB_KERNEL")
 stack = np.stack([f for _, f in frames(120, 200)])
@@ -72,10 +74,10 @@ if "--time" in sys.argv:
         for r in (4, 7, 15, 23, 31, 47, 63):
             row = []
             for label, env in (("old", {"MTB_U16_LIST": "0"}), ("ph4", {"MTB_LS_PH": "4"}), ("ph8", {"MTB_LS_PH": "8"}),
-                               ("ph12", {"MTB_LS_PH": "12"}), ("ph16", {"MTB_LS_PH": "16"}), ("ph24", {"MTB_LS_PH": "24"})):
+                               ("pair", {"MTB_LS_HI": "pair"}), ("mma", {"MTB_LS_HI": "mma"})):
                 if cfg in (4, 12) and label not in ("old", "ph8"):
                     continue
-                for k in ("MTB_U16_LIST", "MTB_LS_PH", "MTB_LS_LG", "MTB_LS_SEG"):
+                for k in ("MTB_U16_LIST", "MTB_LS_PH", "MTB_LS_LG", "MTB_LS_SEG", "MTB_LS_HI"):
                     os.environ.pop(k, None)
                 os.environ.update(env)
                 mtb.rank_filter(src, r, out=out)
