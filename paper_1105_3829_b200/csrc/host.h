@@ -72,6 +72,9 @@ int run_colhist16c_u16(SlabParams p, int B, cudaStream_t s);
 constexpr int LOWSEL_MIN_R = 3, LOWSEL_MAX_R = 63;
 bool lowsel16_applies(const SlabParams &p);
 int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s);
+// 16-bit, compact and peaked data: one 8-bit pass per tile keyed by a 254-value window around the
+// tile's median, leftovers by the two-phase kernel (run_lowsel16.cu); same launches and radii
+int run_wk16_u16(SlabParams p, int B, cudaStream_t s);
 // compile-time window sides of k_colhist16_u16; 1 (NOT_COVERED) when n is outside the range
 int run_colhist16_fixed_a(SlabParams p, int B, cudaStream_t s, int wk);
 int run_colhist16_fixed_b(SlabParams p, int B, cudaStream_t s, int wk);

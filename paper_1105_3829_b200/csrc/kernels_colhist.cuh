@@ -1025,9 +1025,20 @@ namespace mtb {
 // H << 16 | k' per pixel to a u32 plane (p.dst, pitch in words), H = the
 // result's key, k' = the rank of the result among the window values with
 // that key.
-template <int T, int G, int M, int PL, bool STREAM, int NF = 0, typename PX = uint8_t>
+// MODE = 1 (PX = uint16_t, "window key"): compact 16-bit data as ONE 8-bit
+// problem.  The CTA estimates the median V0 + 127 of its tile from 256 sampled
+// pixels and keys every pixel by clamp(v - V0 + 1, 0, 255): 0 = below the
+// 254-value window [V0, V0 + 253], 255 = above it, 1..254 exact.  A pixel whose
+// rank lands on a key in 1..254 is resolved exactly (result V0 + key - 1); one
+// that lands on 0 or 255 flags its 32 x todo_bh block in SlabParams::todo for
+// the two-phase kernel (k_colhist16_u16, which then redoes the tiles holding
+// flagged blocks).  With spread[2] == 0 (the sampled histogram is not peaked:
+// few medians would land in the window) the CTA flags its whole tile and exits.
+template <int T, int G, int M, int PL, bool STREAM, int NF = 0, typename PX = uint8_t, int MODE = 0>
 __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
-    constexpr bool HI16 = sizeof(PX) == 2;
+    constexpr bool WK = MODE == 1;
+    constexpr bool HI16 = sizeof(PX) == 2 && !WK;
+    static_assert(!WK || (sizeof(PX) == 2 && T == 256 && !STREAM), "window-key mode: 16-bit pixels, one sample per thread");
     constexpr int GP = G / 2;
     constexpr bool DL2 = PL == 4;           // level-2 singles derived from level 3
     constexpr int PLP = DL2 ? 3 : PL;        // pair levels
@@ -1043,16 +1054,48 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
     const int X0 = blockIdx.x * T;
     const int y0 = p.row_begin + blockIdx.y * p.rows_per_cta;
     if (y0 >= p.row_end) return;  // CTA-uniform (barriers below)
-    if (HI16 && gate_off(p)) return;
+    if ((HI16 || WK) && gate_off(p)) return;
     const int ks = HI16 ? key_shift(p) : 0;
-    // the record key of a pixel: the pixel (8-bit), or its coarse key min(v >> ks, 255) (16-bit)
-    auto keyof = [&](unsigned v) -> unsigned { return HI16 ? min(v >> ks, 255u) : v; };
     const int y1 = min(y0 + p.rows_per_cta, p.row_end);
     if (STREAM) stream_wait_rows(p, y1 + r);
     const PX *src = static_cast<const PX *>(p.src) + blockIdx.z * p.src_img_stride;
-    uint8_t *dst = static_cast<uint8_t *>(p.dst) + (HI16 ? 4 : 1) * blockIdx.z * p.dst_img_stride;
+    uint8_t *dst = static_cast<uint8_t *>(p.dst) + (HI16 ? 4 : (WK ? 2 : 1)) * blockIdx.z * p.dst_img_stride;
     const uint8_t *lut = static_cast<const uint8_t *>(p.lut);
     const int x = X0 + tid;
+    unsigned V0 = 0;  // window-key mode: first value of the tile's window
+    unsigned char *todo = nullptr;
+    if (WK) {
+        todo = p.todo + (size_t)blockIdx.z * p.todo_nbx * p.todo_nby;
+        if (p.spread && reinterpret_cast<const volatile int *>(p.spread)[2] == 0) {
+            // not peaked: the whole tile goes to the two-phase kernel
+            const int bx0 = X0 >> 5, nx = min((X0 + T + 31) >> 5, p.todo_nbx) - bx0;
+            const int by0 = (y0 - p.row_begin) / p.todo_bh, ny = (y1 - p.row_begin + p.todo_bh - 1) / p.todo_bh - by0;
+            for (int i = tid; i < nx * ny; i += T) todo[(size_t)(by0 + i / nx) * p.todo_nbx + bx0 + i % nx] = 1;
+            return;
+        }
+        // the median of 256 pixels sampled over the tile, by counting ranks
+        uint32_t *smp = reinterpret_cast<uint32_t *>(smem_raw);
+        const int yy = y0 + (int)(((int64_t)tid * 97) % (y1 - y0));
+        const int xx = min(X0 + (int)(((int64_t)tid * 61) % T), W - 1);
+        const uint32_t mine = src_row(p, src, yy)[xx];
+        smp[tid] = mine;
+        __syncthreads();
+        int rk = 0;
+        for (int j = 0; j < T; ++j) {
+            const uint32_t o = smp[j];
+            rk += (o < mine || (o == mine && j < tid)) ? 1 : 0;
+        }
+        if (rk == T / 2) smp[T] = mine;
+        __syncthreads();
+        V0 = (unsigned)clampi((int)smp[T] - 127, 0, 65535 - 253);
+        __syncthreads();  // (the records below reuse the sample's memory)
+    }
+    // the record key of a pixel: the pixel (8-bit), its coarse key min(v >> ks, 255) (16-bit,
+    // candidate-bucket path), or its place in the tile's window (16-bit, window-key mode)
+    auto keyof = [&](unsigned v) -> unsigned {
+        if (WK) return v < V0 ? 0u : min(v - V0 + 1u, 255u);
+        return HI16 ? min(v >> ks, 255u) : v;
+    };
     // single-record updates (one atomic per level kept; the word is the
     // thread's own column, so there is no contention)
     auto sbump_upper = [&](int c, unsigned v, int d) {  // levels 1-3
@@ -1168,6 +1211,17 @@ __global__ void __launch_bounds__(T) k_colhist4p_u8(SlabParams p) {
         const unsigned v = (unsigned)(p3 * 4 + d0);
         if (HI16) {
             if (x < W) reinterpret_cast<uint32_t *>(dst)[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = (v << 16) | k;
+        } else if (WK) {
+            if (x < W) {
+                if (v >= 1u && v <= 254u) {
+                    const unsigned val = V0 + v - 1u;
+                    const uint16_t *lut16 = reinterpret_cast<const uint16_t *>(lut);
+                    reinterpret_cast<uint16_t *>(dst)[(int64_t)(y - p.row_begin) * p.dst_pitch + x] =
+                        lut16 ? __ldg(lut16 + val) : (uint16_t)val;
+                } else {  // the rank lies outside the window: leave the block to the two-phase kernel
+                    todo[(size_t)((y - p.row_begin) / p.todo_bh) * p.todo_nbx + (x >> 5)] = 1;
+                }
+            }
         } else {
             if (x < W) dst[(int64_t)(y - p.row_begin) * p.dst_pitch + x] = lut ? __ldg(lut + v) : (uint8_t)v;
         }

@@ -38,6 +38,8 @@ namespace mtb {
 // beyond 8: if the keys are then
 // widely spread AND flat (no key holds more than 1/64 of the sample, against
 // 1/256 on uniformly spread data), the candidate-bucket path takes it with that shift.
+// out[2] = 1 when the sample is peaked (see below): compact AND peaked data takes
+// the window-key pass instead of the two-phase kernel.
 // Every choice is exact; it only decides the speed.
 constexpr int SPREAD_SAMPLES = 1 << 14;
 constexpr int SPREAD_FLAT_MAX = SPREAD_SAMPLES / 64;
@@ -48,7 +50,7 @@ __global__ void __launch_bounds__(SPREAD_THREADS) k_highbyte_spread(const uint16
                                                                     int64_t img_stride, int B, int allow_shift, int *out) {
     __shared__ uint16_t smp[SPREAD_SAMPLES];  // the sample, read once
     __shared__ int hist[256];
-    __shared__ int vmax, res[2];
+    __shared__ int vmax, res[2], med[3], inwin;
     const int tid = threadIdx.x;
     // distinct / fullest of the 256 keys min(v >> s, 255) -> res[0], res[1]
     auto keys = [&](int s) {
@@ -83,6 +85,44 @@ __global__ void __launch_bounds__(SPREAD_THREADS) k_highbyte_spread(const uint16
     if ((tid & 31) == 0) atomicMax(&vmax, mx);
     keys(8);  // (its barriers also order smp and vmax)
     int d = res[0], sh = 8;
+    // out[2]: is the sample peaked -- do at least 2 in 5 of its values lie in the 254-value window
+    // around its median?  (Then most window medians do, and compact data goes through the
+    // window-key pass, run_wk16_u16.)  The median: its high byte from the counts just taken, its
+    // low byte from the counts of the low bytes under that high byte.
+    if (tid == 0) {
+        int acc = 0, h = 0;
+        for (; h < 255; ++h) {
+            if (acc + hist[h] >= SPREAD_SAMPLES / 2) break;
+            acc += hist[h];
+        }
+        med[0] = h;
+        med[1] = acc;
+        inwin = 0;
+    }
+    __syncthreads();
+    if (tid < 256) hist[tid] = 0;
+    __syncthreads();
+    for (int i = tid; i < SPREAD_SAMPLES; i += SPREAD_THREADS)
+        if ((smp[i] >> 8) == med[0]) atomicAdd(hist + (smp[i] & 255), 1);
+    __syncthreads();
+    if (tid == 0) {
+        int acc = med[1], l = 0;
+        for (; l < 255; ++l) {
+            if (acc + hist[l] >= SPREAD_SAMPLES / 2) break;
+            acc += hist[l];
+        }
+        med[2] = med[0] * 256 + l;
+    }
+    __syncthreads();
+    {
+        const unsigned lo = (unsigned)max(med[2] - 127, 0);
+        int c = 0;
+        for (int i = tid; i < SPREAD_SAMPLES; i += SPREAD_THREADS) c += ((unsigned)smp[i] - lo <= 253u) ? 1 : 0;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if ((tid & 31) == 0) atomicAdd(&inwin, c);
+    }
+    __syncthreads();
+    const int peaked = 5 * inwin >= 2 * SPREAD_SAMPLES ? 1 : 0;
     int s = 0;
     while (s < 8 && (vmax >> s) > 255) ++s;
     if (allow_shift && s < 8) {  // (uniform: all from shared memory)
@@ -93,6 +133,7 @@ __global__ void __launch_bounds__(SPREAD_THREADS) k_highbyte_spread(const uint16
     if (tid == 0) {
         out[0] = d;
         out[1] = sh;
+        out[2] = peaked;
     }
 }
 
@@ -300,6 +341,7 @@ static int run_sortnet(SlabParams p, int B, cudaStream_t s) {
 static thread_local int g_spread_hint = -1;
 
 static thread_local int g_shift_hint = 8;
+static thread_local int g_peaked_hint = 0;
 
 // the same on a host frame: returns the distinct-key count, sets g_shift_hint
 static int spread_distinct_host(const uint16_t *src, int64_t pitch, int rows, int W) {
@@ -308,17 +350,30 @@ static int spread_distinct_host(const uint16_t *src, int64_t pitch, int rows, in
         const int x = (int)(((int64_t)i * 104729) % W);
         return src[(int64_t)y * pitch + x];
     };
+    // (the frame is sampled once: 2^14 scattered host reads are the cost of this probe)
+    static thread_local std::vector<uint16_t> all(SPREAD_SAMPLES), tmp(SPREAD_SAMPLES);
+    unsigned vmax = 0;
+    for (int i = 0; i < SPREAD_SAMPLES; ++i) {
+        all[i] = (uint16_t)sample(i);
+        vmax = std::max(vmax, (unsigned)all[i]);
+    }
     auto keys = [&](int s, int &distinct, int &fullest) {
         int hist[256] = {};
-        for (int i = 0; i < SPREAD_SAMPLES; ++i) ++hist[std::min(sample(i) >> s, 255u)];
+        for (int i = 0; i < SPREAD_SAMPLES; ++i) ++hist[std::min((unsigned)all[i] >> s, 255u)];
         distinct = fullest = 0;
         for (int b = 0; b < 256; ++b) {
             distinct += hist[b] ? 1 : 0;
             fullest = std::max(fullest, hist[b]);
         }
     };
-    unsigned vmax = 0;
-    for (int i = 0; i < SPREAD_SAMPLES; ++i) vmax = std::max(vmax, sample(i));
+    {  // peaked: at least 2 in 5 sampled values in the 254-value window around the sample's median
+        tmp = all;
+        std::nth_element(tmp.begin(), tmp.begin() + SPREAD_SAMPLES / 2 - 1, tmp.end());
+        const unsigned lo = (unsigned)std::max((int)tmp[SPREAD_SAMPLES / 2 - 1] - 127, 0);
+        int in = 0;
+        for (uint16_t v : all) in += ((unsigned)v - lo <= 253u) ? 1 : 0;
+        g_peaked_hint = 5 * in >= 2 * SPREAD_SAMPLES ? 1 : 0;
+    }
     int d8, m8;
     keys(8, d8, m8);
     int s = 0;
@@ -341,16 +396,25 @@ static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
     if (force == "colhist16s") return run_colhist16s_u16(p, B, s);
     if (force == "colhist16c") return run_colhist16c_u16(p, B, s);
     if (force == "lowsel") return run_lowsel16_u16(p, B, s);
+    if (force == "wk16") return run_wk16_u16(p, B, s);
     // widely spread data: the candidate-list path where it applies (r = 3..63, not the streaming
     // launch; MTB_U16_LIST=0 for comparison), else the candidate-run kernel up to r = 23, else the
     // two-phase kernel without the window-keyed sweep
     const bool list = lowsel16_applies(p) && env_int("MTB_U16_LIST", 1) != 0;
     const bool small_r = p.radius <= env_int("MTB_U16C_MAX_R", 23);
+    // compact and peaked data, r >= 40: the window-key pass (same launches as the candidate-bucket
+    // path).  Config 4 (8192^2), two-phase kernel / window-key pass + two-phase on the flagged
+    // tiles: r = 15 1.97 / 2.35 ms, r = 31 2.91 / 3.33, r = 47 9.75 / 5.78, r = 63 12.0 / 8.86 --
+    // below r = 40 the two-phase kernel's window-keyed sweep is the faster form of the same idea
+    // (the pass's misses sit along the clamped borders, and redoing those 256-column tiles costs
+    // more than it saves).  MTB_U16_WK8=0 / 1: never / from r = 3.
+    const int wk8_mode = env_int("MTB_U16_WK8", -1);
+    const bool wk8 = lowsel16_applies(p) && (wk8_mode < 0 ? p.radius >= 40 : wk8_mode != 0);
     auto run_wide = [&](const SlabParams &q) {
         return list ? run_lowsel16_u16(q, B, s) : (small_r ? run_colhist16c_u16(q, B, s) : run_colhist16_u16(q, B, s, 0));
     };
     if (g_spread_hint >= 0) {
-        if (g_spread_hint <= SPREAD_WIDE) return run_colhist16_u16(p, B, s, 1);
+        if (g_spread_hint <= SPREAD_WIDE) return (wk8 && g_peaked_hint) ? run_wk16_u16(p, B, s) : run_colhist16_u16(p, B, s, 1);
         p.key_down = list ? 8 - g_shift_hint : 0;
         // (a shifted key only helps the candidate-bucket path: the other kernels split at the high byte)
         if (!list && g_shift_hint != 8) return run_colhist16_u16(p, B, s, 1);
@@ -358,7 +422,7 @@ static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
     }
     int *d_spread = nullptr;
     keep_pool_memory();
-    if (cudaMallocAsync(reinterpret_cast<void **>(&d_spread), 2 * sizeof(int), s) != cudaSuccess)
+    if (cudaMallocAsync(reinterpret_cast<void **>(&d_spread), 3 * sizeof(int), s) != cudaSuccess)
         return fail(MTB_E_CUDA, "k_highbyte_spread: scratch allocation failed");
     k_highbyte_spread<<<1, SPREAD_THREADS, 0, s>>>(static_cast<const uint16_t *>(p.src), p.src_pitch, p.src_rows, p.W,
                                         p.src_img_stride, B, list ? 1 : 0, d_spread);
@@ -369,12 +433,13 @@ static int run_u16_colhist(SlabParams p, int B, cudaStream_t s) {
     if (!rc) {
         p.gate = GATE_WIDE;  // these launches exit at once unless the data is widely spread
         rc = run_wide(p);
-        p.gate = GATE_COMPACT;  // compact data: the two-phase kernel with its window-keyed sweep
-        if (!rc) rc = run_colhist16_u16(p, B, s, 1);
+        p.gate = GATE_COMPACT;  // compact data: the window-key pass (where the sample is peaked: spread[2])
+        if (!rc) rc = wk8 ? run_wk16_u16(p, B, s) : run_colhist16_u16(p, B, s, 1);  // and the two-phase kernel
         if (!rc)
-            g_kernel = list      ? "k_lowsel_u16|k_colhist16_u16 (device-selected)"
-                       : small_r ? "k_colhist16c_u16|k_colhist16_u16 (device-selected)"
-                                 : "k_colhist16_u16 (device-selected)";
+            g_kernel = list && wk8 ? "k_lowsel_u16|k_colhist4p_u8<u16 window key>|k_colhist16_u16 (device-selected)"
+                       : list      ? "k_lowsel_u16|k_colhist16_u16 (device-selected)"
+                       : small_r   ? "k_colhist16c_u16|k_colhist16_u16 (device-selected)"
+                                   : "k_colhist16_u16 (device-selected)";
     }
     cudaFreeAsync(d_spread, s);
     return rc;

@@ -16,6 +16,8 @@ namespace mtb {
 
 int run_hi16_fixed_a(SlabParams p, int B, cudaStream_t s);
 int run_hi16_fixed_b(SlabParams p, int B, cudaStream_t s);
+int run_wk16_fixed_a(SlabParams p, int B, cudaStream_t s);
+int run_wk16_fixed_b(SlabParams p, int B, cudaStream_t s);
 
 bool lowsel16_applies(const SlabParams &p) {
     return !p.in_rows && p.radius >= LOWSEL_MIN_R && p.radius <= LOWSEL_MAX_R;
@@ -100,6 +102,28 @@ int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s) {
     if (!rc) rc = run_colhist16_u16(p, B, s, 1);
     cudaFreeAsync(scratch, s);
     if (!rc) g_kernel = "k_lowsel_u16";
+    return rc;
+}
+
+// Compact, peaked 16-bit data (config 4): pass 1 the pair-record kernel in window-key mode (one
+// 8-bit problem per tile), pass 2 the two-phase kernel on the tiles holding a block pass 1 flagged.
+int run_wk16_u16(SlabParams p, int B, cudaStream_t s) {
+    if (!lowsel16_applies(p)) return run_colhist16_u16(p, B, s, 1);
+    const int rows = p.row_end - p.row_begin;
+    p.todo_bh = 8;
+    p.todo_nbx = (p.W + 31) / 32;
+    p.todo_nby = (rows + p.todo_bh - 1) / p.todo_bh;
+    const size_t flag_bytes = (size_t)p.todo_nbx * p.todo_nby * B;
+    keep_pool_memory();
+    if (cudaMallocAsync(reinterpret_cast<void **>(&p.todo), flag_bytes, s) != cudaSuccess)
+        return fail(MTB_E_CUDA, "window-key pass: scratch allocation failed");
+    cudaMemsetAsync(p.todo, 0, flag_bytes, s);
+    int rc = run_wk16_fixed_a(p, B, s);
+    if (rc == 1) rc = run_wk16_fixed_b(p, B, s);
+    if (rc == 1) rc = fail(MTB_E_INVAL, "window-key pass: radius outside its range");
+    if (!rc) rc = run_colhist16_u16(p, B, s, 1);
+    cudaFreeAsync(p.todo, s);
+    if (!rc) g_kernel = "k_colhist4p_u8<256,u16 window key>";
     return rc;
 }
 

@@ -406,7 +406,7 @@ def test_full_size_off_centre_ranks():
 _FAMILY_CASES = [c for c in G.small_cases() if c[0]["rank"] is None and c[0]["percentile"] is None]
 
 
-@pytest.mark.parametrize("family", ["vert", "ctmf", "bandmma", "bandtc", "sortnet", "colhist", "colhist16s", "colhist16c", "lowsel"])
+@pytest.mark.parametrize("family", ["vert", "ctmf", "bandmma", "bandtc", "sortnet", "colhist", "colhist16s", "colhist16c", "lowsel", "wk16"])
 def test_each_kernel_family_is_exact(family, monkeypatch):
     """MTB_KERNEL forces one family; families that do not apply to a case
     (ctmf: 8-bit only; sortnet: median of n <= 7) fall through to the
@@ -430,7 +430,8 @@ def test_each_kernel_family_is_exact(family, monkeypatch):
         out16 = mtb.rank_filter(torch.from_numpy(px16).cuda(), min(r, 34)).cpu().numpy()
         assert np.array_equal(out16, O.iot_filter(px16, 2 * min(r, 34) + 1)), (family, r)
     expect = {"vert": "k_vert_u8", "ctmf": "k_ctmf_u8", "bandmma": "k_bandmma_u8", "bandtc": "k_bandtc_u8", "sortnet": "k_sortnet", "colhist": "k_colhist_u8",
-              "colhist16s": "k_colhist16s_u16", "colhist16c": "k_colhist16c_u16", "lowsel": "k_lowsel_u16"}[family]
+              "colhist16s": "k_colhist16s_u16", "colhist16c": "k_colhist16c_u16", "lowsel": "k_lowsel_u16",
+              "wk16": "k_colhist4p_u8"}[family]
     assert expect in seen, seen
 
 
@@ -667,6 +668,55 @@ def test_lowsel_u16_key_follows_the_occupied_range(bits):
     out, _ = mtb.filter_image(peaked, 11)
     assert _lib.last_kernel() == "k_colhist16_u16", _lib.last_kernel()
     assert np.array_equal(out.pixels, O.iot_filter(peaked, 11))
+
+
+@pytest.mark.parametrize("kind", ["compact", "drift", "noise", "mixed", "low", "high", "cfg4"])
+def test_wk16_window_key_pass(kind, monkeypatch):
+    """The window-key pass of compact 16-bit data (k_colhist4p_u8<...,
+    uint16_t, 1>: one 8-bit problem per tile around the tile's sampled
+    median) with the two-phase kernel on the flagged tiles: data where every
+    pixel hits (compact, config 4), where tiles drift away from their window,
+    where nothing hits (noise) and windows clamped at 0 and 65535; every rank
+    position, a slab, a batch, a value map; and the default dispatch taking
+    it for peaked data from r = 40."""
+    from paper_1105_3829_b200 import _lib
+
+    rng = np.random.default_rng(77)
+    h, w = 131, 333
+    noise = rng.integers(0, 65536, (h, w)).astype(np.uint16)
+    compact = (30000 + rng.normal(0, 60, (h, w))).clip(0, 65535).astype(np.uint16)
+    px = {"compact": compact,
+          "drift": (np.add.outer(np.arange(h) * 3, np.arange(w) * 2) + rng.normal(0, 40, (h, w)) + 500).clip(0, 65535).astype(np.uint16),
+          "noise": noise,
+          "mixed": np.where(np.arange(w)[None, :] < w // 2, compact, noise).astype(np.uint16),
+          "low": rng.integers(0, 90, (h, w)).astype(np.uint16),
+          "high": (65535 - rng.integers(0, 90, (h, w))).astype(np.uint16),
+          "cfg4": workloads.cfg4_three_gauss_u16(h, w)}[kind]
+    src = torch.from_numpy(px).cuda()
+    if kind in ("compact", "cfg4", "low", "high"):  # peaked: the host entry names the pass
+        out, _ = mtb.filter_image(px, 91)
+        # ("low": values 0..89 are wide and flat once the key follows the occupied range -> buckets)
+        expect = "k_lowsel_u16" if kind == "low" else "k_colhist4p_u8<256,u16 window key>"
+        assert _lib.last_kernel() == expect, _lib.last_kernel()
+        assert np.array_equal(out.pixels, O.iot_filter(px, 91))
+        assert np.array_equal(mtb.rank_filter(src, 45).cpu().numpy(), O.iot_filter(px, 91))
+    monkeypatch.setenv("MTB_KERNEL", "wk16")
+    for r in (3, 8, 16, 17, 33, 63):
+        n = 2 * r + 1
+        for rank in (None, 1, n * n, (n * n) // 3 + 1):
+            out = mtb.rank_filter(src, r, rank=rank).cpu().numpy()
+            assert _lib.last_kernel() == "k_colhist4p_u8<256,u16 window key>", _lib.last_kernel()
+            assert np.array_equal(out, O.iot_filter(px, n, rank=rank)), (kind, r, rank)
+    ref = O.iot_filter(px, 13)
+    big = torch.zeros((h, 400), dtype=torch.uint16, device="cuda")
+    sl = mtb.rank_filter(src, 6, rows=(19, 77), out=big[19:77, :w])
+    assert np.array_equal(sl.cpu().numpy(), ref[19:77])
+    lut = torch.from_numpy((np.arange(65536) & ~np.uint32(15)).astype(np.uint16)).cuda()
+    assert np.array_equal(mtb.rank_filter(src, 6, lut=lut).cpu().numpy(), ref & ~np.uint16(15))
+    stack = np.stack([px, px[::-1].copy(), noise])
+    got = mtb.rank_filter(torch.from_numpy(stack).cuda(), 6).cpu().numpy()
+    for i in range(3):
+        assert np.array_equal(got[i], O.iot_filter(stack[i], 13)), i
 
 
 # ------------------------------------------ 3x3 kernels (k_med3_u8 / k_med3t_u8)
