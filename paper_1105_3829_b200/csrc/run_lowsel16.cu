@@ -77,7 +77,10 @@ int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s) {
         return fail(MTB_E_CUDA, "k_lowsel_u16: scratch allocation failed");
     uint32_t *hk = reinterpret_cast<uint32_t *>(scratch);
     p.todo = scratch + hk_bytes;
-    cudaMemsetAsync(p.todo, 0, flag_bytes, s);
+    if (cudaMemsetAsync(p.todo, 0, flag_bytes, s) != cudaSuccess) {
+        cudaFreeAsync(scratch, s);
+        return fail(MTB_E_CUDA, "k_lowsel_u16: clearing the block flags failed");
+    }
 
     SlabParams a = p;  // pass 1 writes H << 16 | k' words
     a.dst = hk;
@@ -117,7 +120,10 @@ int run_wk16_u16(SlabParams p, int B, cudaStream_t s) {
     keep_pool_memory();
     if (cudaMallocAsync(reinterpret_cast<void **>(&p.todo), flag_bytes, s) != cudaSuccess)
         return fail(MTB_E_CUDA, "window-key pass: scratch allocation failed");
-    cudaMemsetAsync(p.todo, 0, flag_bytes, s);
+    if (cudaMemsetAsync(p.todo, 0, flag_bytes, s) != cudaSuccess) {
+        cudaFreeAsync(p.todo, s);
+        return fail(MTB_E_CUDA, "window-key pass: clearing the block flags failed");
+    }
     int rc = run_wk16_fixed_a(p, B, s);
     if (rc == 1) rc = run_wk16_fixed_b(p, B, s);
     if (rc == 1) rc = fail(MTB_E_INVAL, "window-key pass: radius outside its range");
