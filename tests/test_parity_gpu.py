@@ -663,6 +663,9 @@ def test_lowsel_u16_key_follows_the_occupied_range(bits):
             for rank in (None, 1, n * n, (n * n) // 3 + 1):
                 got = mtb.rank_filter(src, r, rank=rank).cpu().numpy()
                 assert np.array_equal(got, O.iot_filter(img, n, rank=rank)), (bits, r, rank)
+    # row slabs over "devices" (the host rows entry: halos from the host frame, one probe per slab)
+    out, _ = mtb.filter_image(px, 19, devices=[0, 0, 0])
+    assert np.array_equal(out.pixels, O.iot_filter(px, 19))
     # peaked data in a narrow range stays on the two-phase kernel (not flat in key space)
     peaked = (800 + rng.normal(0, 40, (150, 260))).clip(0, 65535).astype(np.uint16)
     out, _ = mtb.filter_image(peaked, 11)
