@@ -9,14 +9,15 @@
 // byte is H.  On spread data only ~n^2/256 window values have that high byte,
 // and neighbouring pixels want nearby H, so ONE WARP resolves a block of
 // 32 x PH output pixels together:
-//   1. [Hmin, Hmax] = the range of H over the block, taken in chunks of NB
-//      consecutive high bytes (NB buckets of BCAP entries = 512 entries);
+//   1. [Hmin, Hmax] = the range of H over the block, taken in chunks of up to
+//      64 consecutive keys;
 //   2. the warp scans the union of the block's windows, (32 + 2r) x (PH + 2r)
-//      replicate-clamped source values, once per chunk, and drops every value
-//      whose high byte lies in the chunk into that high byte's bucket in
-//      shared memory together with its window coordinates
-//      (value << 16 | dy << 8 | dx);
-//   3. every bucket is sorted by counting ranks (entries are distinct, so an
+//      replicate-clamped source values, once per chunk, and stages every value
+//      whose key lies in the chunk in shared memory together with its window
+//      coordinates (value << 16 | dy << 8 | dx; up to 512 entries);
+//   3. the staged entries are counted per key, placed into one bucket per key
+//      (exclusive prefix of the counts: no slot is wasted on an empty key), and
+//      every bucket is sorted by counting ranks (entries are distinct, so an
 //      entry's place is the number of smaller entries of its bucket);
 //   4. every pixel walks the bucket of its H in ascending order, counts the
 //      entries inside its own window, and stops at the k'-th: that entry's
@@ -25,9 +26,8 @@
 // (32 PH) loads instead of the n per level of the gather kernels or the
 // per-column run lookups of k_colhist16c_u16.
 //
-// A chunk with an overflowing bucket is repeated with buckets large enough for
-// it (fewer high bytes per chunk); a block where one high byte alone overflows
-// 512 entries (locally compact data) is flagged in SlabParams::todo and left to
+// A chunk whose entries do not fit is halved (fewer keys per chunk) and
+// repeated; a block where one key alone overflows 512 entries (locally compact data) is flagged in SlabParams::todo and left to
 // k_colhist16_u16, which then works on the tiles holding such blocks only.
 // Exact for any image; the data only decide which kernel resolves a block.
 #pragma once
@@ -37,16 +37,15 @@ namespace mtb {
 
 constexpr int LS_WARPS = 8;    // warps per CTA, side by side (256 output columns)
 constexpr int LS_CAP = 512;    // bucket entries per warp (NB buckets x BCAP)
-constexpr int LS_MAXLG = 9;    // log2 of the largest bucket (one high byte per chunk)
-constexpr int LS_MINLG = 4;    // log2 of the smallest bucket (32 high bytes per chunk)
+constexpr int LS_KEYS = 64;    // keys (buckets) per chunk at most
 
 // One block: the 32 x PH output pixels at columns xb.., block row `by` of image
-// blockIdx.z; called by a whole warp.  buf / srt / bcnt: the warp's buckets.
+// blockIdx.z; called by a whole warp.  buf / srt / ctr / kmap: the warp's buckets and counters.
 // PH > 0: compile-time block height, the block's (H, k') words in registers;
 // PH == 0: block height p.todo_bh, the words re-read where they are used.
 template <int PH, int NI>
-__device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__restrict__ hk, int lg0, int xb, int by,
-                                         uint32_t *buf, uint32_t *srt, int *bcnt) {
+__device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__restrict__ hk, int xb, int by,
+                                         uint32_t *buf, uint32_t *srt, int *ctr, unsigned char *kmap) {
     const int lane = threadIdx.x & 31;
     const int r = p.radius, r2 = 2 * r, W = p.W, H = p.H;
     const int PHR = PH ? PH : p.todo_bh;
@@ -104,10 +103,12 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
     }
     const uint16_t *row0 = src_row(p, src, yb - r + jT);
 
-    int lg = lg0;
+    // chunks of up to LS_KEYS consecutive keys; a chunk whose entries do not fit
+    // LS_CAP is halved and repeated
+    int width = min(hmax - hmin + 1, LS_KEYS);
+    int *kcnt = ctr, *koff = ctr + LS_KEYS, *kfill = ctr + 2 * LS_KEYS, *staged = ctr + 3 * LS_KEYS;
     for (int h0 = hmin; h0 <= hmax;) {
-        const int NB = LS_CAP >> lg, BCAP = 1 << lg;
-        const int h1 = min(h0 + NB - 1, hmax);
+        const int h1 = min(h0 + width - 1, hmax);
         const unsigned hspan = (unsigned)(h1 - h0);
         bool want = false;
 #pragma unroll
@@ -116,14 +117,18 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
             h0 = h1 + 1;
             continue;
         }
-        bcnt[lane] = 0;
+        kcnt[lane] = kcnt[lane + 32] = 0;
+        kfill[lane] = kfill[lane + 32] = 0;
+        for (int i = lane; i < LS_CAP / 4; i += 32) reinterpret_cast<uint32_t *>(kmap)[i] = 0xffffffffu;
+        if (lane == 0) *staged = 0;
         __syncwarp();
-        // ---- scan, two rows per step (all loads of a step in flight together)
+        // ---- scan, two rows per step (all loads of a step in flight together):
+        // matching values are staged in scan order (in srt)
         auto drop = [&](unsigned v, int j, int i, bool on) {
             const unsigned b = min(v >> ks, 255u) - (unsigned)h0;
             if (on && ((okc >> i) & 1u) && b <= hspan) {
-                const int slot = atomicAdd(bcnt + b, 1);
-                if (slot < BCAP) buf[(b << lg) + slot] = (v << 16) | ((unsigned)j << 8) | (unsigned)(lane + 32 * i);
+                const int pos = atomicAdd(staged, 1);
+                if (pos < LS_CAP) srt[pos] = (v << 16) | ((unsigned)j << 8) | (unsigned)(lane + 32 * i);
             }
         };
         const uint16_t *row = row0;
@@ -141,31 +146,55 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
             for (int i = 0; i < NI; ++i) drop(v1[i], j + 1, i, two);
         }
         __syncwarp();
-        const int maxc = __reduce_max_sync(0xffffffffu, bcnt[lane]);  // the fullest bucket
-        if (maxc > BCAP) {
-            if (maxc > LS_CAP) {  // locally compact data: leave the block to the two-phase kernel
+        // ---- entries per key (one lane per staged entry), then the bucket offsets:
+        // exclusive prefix of the counts, every bucket on an even slot (the walk
+        // reads entry pairs); lane l owns keys 2l and 2l + 1
+        const int cnt = *staged;
+        auto key_of = [&](uint32_t e) -> int { return (int)(min((e >> 16) >> ks, 255u) - (unsigned)h0); };
+        for (int t = lane; t < min(cnt, LS_CAP); t += 32) atomicAdd(kcnt + key_of(srt[t]), 1);
+        __syncwarp();
+        const int ca = (kcnt[2 * lane] + 1) & ~1, cb = (kcnt[2 * lane + 1] + 1) & ~1;
+        int incl = ca + cb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int padded = __shfl_sync(0xffffffffu, incl, 31);
+        if (cnt > LS_CAP || padded > LS_CAP) {
+            if (width == 1) {  // locally compact data: leave the block to the two-phase kernel
                 if (lane == 0) p.todo[((size_t)blockIdx.z * p.todo_nby + by) * p.todo_nbx + (xb >> 5)] = 1;
                 __syncwarp();
                 return;
             }
-            while ((1 << lg) < maxc) ++lg;  // buckets that hold it, fewer high bytes per chunk; repeat from h0
+            width = (width + 1) >> 1;  // fewer keys per chunk; repeat from h0
             __syncwarp();
             continue;
         }
-        // ---- sort every bucket: an entry goes to the count of smaller entries.
-        // Lanes take (bucket, slot) pairs over the first 2^elg slots of every
-        // bucket, 2^elg >= the fullest bucket's count (fewer idle lanes than over
-        // all BCAP slots)
-        int elg = 0;
-        while ((1 << elg) < maxc) ++elg;
-        for (int t = lane; t < (NB << elg); t += 32) {
-            const int b = t >> elg, i = t & ((1 << elg) - 1), nb = bcnt[b];
-            if (i < nb) {
-                const uint32_t *bk = buf + (b << lg);
-                const uint32_t e = bk[i];
+        koff[2 * lane] = incl - ca - cb;
+        koff[2 * lane + 1] = incl - cb;
+        __syncwarp();
+        // ---- place the staged entries into their buckets (srt -> buf; kmap: the key
+        // of every occupied slot), then sort every bucket (buf -> srt): an entry goes
+        // to the count of smaller entries of its bucket (entries are distinct).  One
+        // lane per entry / per slot.
+        for (int t = lane; t < cnt; t += 32) {
+            const uint32_t e = srt[t];
+            const int k = key_of(e);
+            const int slot = koff[k] + atomicAdd(kfill + k, 1);
+            buf[slot] = e;
+            kmap[slot] = (unsigned char)k;
+        }
+        __syncwarp();
+        for (int t = lane; t < padded; t += 32) {
+            const int k = kmap[t];
+            if (k != 0xff) {
+                const uint32_t *bk = buf + koff[k];
+                const uint32_t e = buf[t];
+                const int nb = kcnt[k];
                 int rank = 0;
                 for (int q = 0; q < nb; ++q) rank += bk[q] < e ? 1 : 0;
-                srt[(b << lg) + rank] = e;
+                srt[koff[k] + rank] = e;
             }
         }
         __syncwarp();
@@ -177,8 +206,8 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
             const unsigned b = (w >> 16) - (unsigned)h0;
             if (b > hspan) continue;
             const uint32_t k = w & 0xffffu;
-            const uint32_t *bk = srt + (b << lg);
-            const int nb = bcnt[b];
+            const uint32_t *bk = srt + koff[b];
+            const int nb = kcnt[b];
             uint32_t c = 0, res = 0;
             if (!border) {
                 // two entries per step (buckets are 64-byte aligned; an odd bucket's last
@@ -220,24 +249,24 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
 }
 
 // hk: [image][row - row_begin][x] words H << 16 | k' (pitch W); PH output rows
-// per block; NI = ceil((32 + 2r) / 32) column steps of the scan; lg0: log2 of
-// the bucket size to start with.  A CTA takes `seg` vertically adjacent block
+// per block; NI = ceil((32 + 2r) / 32) column steps of the scan.  A CTA takes `seg` vertically adjacent block
 // rows of its 256 columns (grid.y = ceil(block rows / seg)): consecutive
 // blocks share all but PH of their PH + 2r source rows in L1, and a gated
 // launch that has nothing to do (compact data) is a few thousand CTAs, not
 // one per block row.
 template <int PH, int NI>
-__global__ void __launch_bounds__(32 * LS_WARPS, 4) k_lowsel_u16(SlabParams p, const uint32_t *__restrict__ hk, int lg0, int seg) {
+__global__ void __launch_bounds__(32 * LS_WARPS, 4) k_lowsel_u16(SlabParams p, const uint32_t *__restrict__ hk, int seg) {
     __shared__ uint32_t bufs[LS_WARPS][LS_CAP];  // buckets as scanned
     __shared__ uint32_t srts[LS_WARPS][LS_CAP];  // buckets sorted
-    __shared__ int bcnts[LS_WARPS][32];          // entries per bucket
+    __shared__ int ctrs[LS_WARPS][3 * LS_KEYS + 2];      // per key: entries, first slot, placed; then: staged
+    __shared__ __align__(4) unsigned char kmaps[LS_WARPS][LS_CAP];  // the key of every bucket slot
     if (gate_off(p)) return;
     const int warp = threadIdx.x >> 5;
     const int xb = (blockIdx.x * LS_WARPS + warp) * 32;  // first output column of the warp's blocks
     if (xb >= p.W) return;                                // (warp-uniform; the kernel has no CTA barriers)
     const int by1 = min((int)(blockIdx.y + 1) * seg, p.todo_nby);
     for (int by = blockIdx.y * seg; by < by1; ++by) {
-        ls_block<PH, NI>(p, hk, lg0, xb, by, bufs[warp], srts[warp], bcnts[warp]);
+        ls_block<PH, NI>(p, hk, xb, by, bufs[warp], srts[warp], ctrs[warp], kmaps[warp]);
         __syncwarp();  // the buckets are reused by the next block
     }
 }

@@ -33,14 +33,7 @@ static int launch_lowsel_ni(const SlabParams &p, int B, cudaStream_t s, const ui
     const int64_t want = 16384;
     const int seg = std::max(1, env_int("MTB_LS_SEG", (int)(((int64_t)gx * p.todo_nby * B + want - 1) / want)));
     dim3 grid(gx, (p.todo_nby + seg - 1) / seg, B);
-    // buckets to start with: the mean count of one high byte on uniformly spread data plus 3.5
-    // standard deviations (an overflowing chunk is repeated with larger buckets; config 3 r = 23
-    // 1.30 -> 1.12 ms against twice the mean)
-    const double mean = (32 + 2 * p.radius) * (p.todo_bh + 2 * p.radius) / 256.0;
-    int lg = LS_MINLG;
-    while (lg < LS_MAXLG && (1 << lg) < mean + 3.5 * std::sqrt(mean)) ++lg;
-    lg = std::min(LS_MAXLG, std::max(LS_MINLG, env_int("MTB_LS_LG", lg)));
-    k_lowsel_u16<PH, NI><<<grid, 32 * LS_WARPS, 0, s>>>(p, hk, lg, seg);
+    k_lowsel_u16<PH, NI><<<grid, 32 * LS_WARPS, 0, s>>>(p, hk, seg);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(MTB_E_CUDA, std::string("k_lowsel_u16: ") + cudaGetErrorString(e));
     g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -603,18 +603,15 @@ def test_lowsel_u16_candidate_buckets(kind, ph, monkeypatch):
         assert np.array_equal(out, O.iot_filter(px, 2 * r + 1, rank=5)), (kind, r)
 
 
-@pytest.mark.parametrize("lg,hi", [("4", "pair"), ("9", "mma")])
-def test_lowsel_u16_bucket_sizes_batch_slab_and_lut(lg, hi, monkeypatch):
-    """k_lowsel_u16 starting from the smallest buckets (every chunk of a
-    wide window overflows and is repeated with larger ones) and from the
-    largest (one high byte per chunk), with the first pass forced onto the
-    pair records / the band-matrix products at every radius; the batch entry (per-image scratch
+@pytest.mark.parametrize("hi", ["pair", "mma"])
+def test_lowsel_u16_first_passes_batch_slab_and_lut(hi, monkeypatch):
+    """The candidate-bucket path with the first pass forced onto the pair
+    records / the band-matrix products at every radius; the batch entry (per-image scratch
     planes and flags), a row slab with a pitched output, a value map, and
     the default device-selected dispatch on a batch that mixes spread and
     compact images."""
     from paper_1105_3829_b200 import _lib
 
-    monkeypatch.setenv("MTB_LS_LG", lg)
     monkeypatch.setenv("MTB_LS_HI", hi)
     rng = np.random.default_rng(321)
     frames = _lowsel_frames(rng, 120, 200)

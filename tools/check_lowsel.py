@@ -77,7 +77,7 @@ if "--time" in sys.argv:
                                ("pair", {"MTB_LS_HI": "pair"}), ("mma", {"MTB_LS_HI": "mma"})):
                 if cfg in (4, 12) and label not in ("old", "ph8"):
                     continue
-                for k in ("MTB_U16_LIST", "MTB_LS_PH", "MTB_LS_LG", "MTB_LS_SEG", "MTB_LS_HI"):
+                for k in ("MTB_U16_LIST", "MTB_LS_PH", "MTB_LS_SEG", "MTB_LS_HI"):
                     os.environ.pop(k, None)
                 os.environ.update(env)
                 mtb.rank_filter(src, r, out=out)
