@@ -212,11 +212,18 @@ __device__ __forceinline__ void ls_block(const SlabParams &p, const uint32_t *__
             if (!border) {
                 // two entries per step (buckets are 64-byte aligned; an odd bucket's last
                 // partner is not counted)
+                // both coordinate tests of an entry at once: dx and dy spread into two 16-bit
+                // fields g; d >= q sets bit 8 of the field d - q + 256, d <= q + 2r sets bit 8
+                // of q + 2r - d + 256 (no borrow or carry crosses a field: d, q < 256, 2r < 256)
+                const uint32_t P = ((uint32_t)py << 16) | (uint32_t)lane, M = 0x01000100u;
+                const uint32_t C1 = M - P, C2 = P + (((uint32_t)r2 << 16) | (uint32_t)r2) + M;
+                auto inside = [&](uint32_t e) -> bool {
+                    const uint32_t g = __byte_perm(e, 0, 0x4140);  // dx | dy << 16
+                    return ((g + C1) & (C2 - g) & M) == M;
+                };
                 for (int i = 0; i < nb; i += 2) {
                     const uint2 ee = *reinterpret_cast<const uint2 *>(bk + i);
-                    const bool in0 = (ee.x & 0xffu) - (unsigned)lane <= (unsigned)r2 && ((ee.x >> 8) & 0xffu) - (unsigned)py <= (unsigned)r2;
-                    const bool in1 = i + 1 < nb && (ee.y & 0xffu) - (unsigned)lane <= (unsigned)r2 &&
-                                     ((ee.y >> 8) & 0xffu) - (unsigned)py <= (unsigned)r2;
+                    const bool in0 = inside(ee.x), in1 = i + 1 < nb && inside(ee.y);
                     const uint32_t c0 = c + (in0 ? 1u : 0u), c1 = c0 + (in1 ? 1u : 0u);
                     if (c1 >= k) {  // (c < k before: the first of the two to reach k)
                         res = (c0 == k ? ee.x : ee.y) >> 16;
