@@ -66,8 +66,12 @@ int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s) {
     const size_t flag_bytes = (size_t)p.todo_nbx * p.todo_nby * B;
     unsigned char *scratch = nullptr;
     keep_pool_memory();
-    if (cudaMallocAsync(reinterpret_cast<void **>(&scratch), hk_bytes + flag_bytes, s) != cudaSuccess)
-        return fail(MTB_E_CUDA, "k_lowsel_u16: scratch allocation failed");
+    if (cudaMallocAsync(reinterpret_cast<void **>(&scratch), hk_bytes + flag_bytes, s) != cudaSuccess) {
+        // no room for the 4-byte-per-pixel plane: the two-phase kernel (1 byte per pixel) instead
+        cudaGetLastError();
+        p.todo = nullptr;
+        return run_colhist16_u16(p, B, s, 0);
+    }
     uint32_t *hk = reinterpret_cast<uint32_t *>(scratch);
     p.todo = scratch + hk_bytes;
     if (cudaMemsetAsync(p.todo, 0, flag_bytes, s) != cudaSuccess) {
