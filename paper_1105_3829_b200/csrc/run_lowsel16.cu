@@ -54,10 +54,10 @@ int run_lowsel16_u16(SlabParams p, int B, cudaStream_t s) {
     if (!lowsel16_applies(p)) return run_colhist16_u16(p, B, s, 0);
     const int rows = p.row_end - p.row_begin;
     // block height: taller blocks share the scan among more pixels but widen the blocks' key ranges
-    // and lengthen the buckets: 8 rows below r = 28, 16 from there (config 3 r = 31 1.42 -> 1.34 ms,
-    // r = 63 4.42 -> 4.00; r = 15 0.91 / 0.90, r = 23 1.14 / 1.27 at 8 / 16 rows).  Heights above 8
+    // and lengthen the buckets.  16 rows (config 3, 8 / 16 / 24 / 32 rows: r = 7 0.67 / 0.62 / 0.62 /
+    // 0.69 ms, r = 15 0.87 / 0.76 / 0.77 / 0.86, r = 31 1.39 / 1.20 / 1.21 / 1.26).  Heights above 8
     // run the variant that keeps the block's (H, k') words out of registers.
-    const int ph_env = env_int("MTB_LS_PH", p.radius >= 28 ? 16 : 8);
+    const int ph_env = env_int("MTB_LS_PH", 16);
     const int PH = ph_env > 8 ? std::min(ph_env, 64) : (ph_env >= 8 ? 8 : 4);
     p.todo_bh = PH;
     p.todo_nbx = (p.W + 31) / 32;

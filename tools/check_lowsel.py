@@ -74,7 +74,7 @@ if "--time" in sys.argv:
         for r in (4, 7, 15, 23, 31, 47, 63):
             row = []
             for label, env in (("old", {"MTB_U16_LIST": "0"}), ("ph4", {"MTB_LS_PH": "4"}), ("ph8", {"MTB_LS_PH": "8"}),
-                               ("pair", {"MTB_LS_HI": "pair"}), ("mma", {"MTB_LS_HI": "mma"})):
+                               ("ph16", {"MTB_LS_PH": "16"}), ("ph24", {"MTB_LS_PH": "24"}), ("ph32", {"MTB_LS_PH": "32"}), ("pair", {"MTB_LS_HI": "pair"}), ("mma", {"MTB_LS_HI": "mma"})):
                 if cfg in (4, 12) and label not in ("old", "ph8"):
                     continue
                 for k in ("MTB_U16_LIST", "MTB_LS_PH", "MTB_LS_SEG", "MTB_LS_HI"):
